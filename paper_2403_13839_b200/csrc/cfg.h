@@ -1,0 +1,774 @@
+// cfg.h -- control-flow facts per code object (cfg.py:61-328, pipeline.py:17-87,
+// disasm.py:175-214, structurer.py:62-173).
+//
+// Blocks are built in O(N) from the sorted leader set (the reference rescans all
+// instructions per block, cfg.py:94); block ids follow ascending leader offsets
+// exactly as the reference's.  Dominators / loops use the reference's
+// DFS orders (successor order preserved) so every derived fact matches.
+#pragma once
+#include "symexec.h"
+
+struct ExcEntry {
+  u32 start, end, target, depth;
+  bool lasti;
+};
+struct TryRegion {  // structurer.py:34-40
+  u32 start, end, handler;
+  u8 kind;          // 0 except, 1 finally, 2 with, 3 as_cleanup
+  i64 setup_offset;
+};
+enum { RK_EXCEPT = 0, RK_FINALLY = 1, RK_WITH = 2, RK_AS_CLEANUP = 3 };
+
+struct Loop {
+  i32 header;
+  Vec<i32>* body;       // sorted block ids
+  Vec<i32>* back_tails; // back edge sources in discovery order
+};
+
+struct Cfg {
+  Block* blocks;        // indexed by id (dead blocks have alive=false)
+  i32 n_blocks;
+  i32 entry;
+  u32 end_of_code;
+  Vec<ExcEntry>* entries;
+  Vec<Loop>* loops;     // keyed by header (unique)
+  i32* loop_of_header;  // [n_blocks] index into loops or -1
+};
+
+// block_at: start offset -> block id (alive only); binary search over sorted starts
+HD inline i32 block_at(const Cfg* G, u32 off) {
+  i32 lo = 0, hi = G->n_blocks;
+  while (lo < hi) {
+    i32 mid = (lo + hi) >> 1;
+    if (G->blocks[mid].start < off) lo = mid + 1;
+    else hi = mid;
+  }
+  // several leaders cannot share an offset (leaders is a set), so this is unique
+  if (lo < G->n_blocks && G->blocks[lo].start == off && G->blocks[lo].alive) return lo;
+  return -1;
+}
+
+HD inline i32 ins_index_of(const Code* K, u32 off) {  // first instr with offset >= off
+  i32 lo = 0, hi = K->n_ins;
+  while (lo < hi) {
+    i32 mid = (lo + hi) >> 1;
+    if (K->ins[mid].offset < off) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+// _index_of (structurer.py:163-173)
+HD inline i32 index_of(Dc* C, const Code* K, u32 off) {
+  i32 lo = ins_index_of(K, off);
+  if (lo == K->n_ins || K->ins[lo].offset != off) {
+    fail_struct(C, off, "offset is not an instruction boundary");
+    return -1;
+  }
+  return lo;
+}
+
+// ------------------------------------------------------------ instructions
+// Materialize the object's instruction list from the decode kernel's records
+// and surface the decode status (decode_instructions, disasm.py:71-172).
+HD inline bool load_instructions(Dc* C, Code* K, u32 oi) {
+  K->oi = oi;
+  K->o = obj_at(C, oi);
+  K->minor = (int)K->o->minor;
+  K->has_kwnames = false;
+  K->kwnames = nullptr;
+  const upy_decoded& d = C->dec_all[oi];
+  if (d.status != UPY_ST_OK) {
+    // message formatting of the decode errors (errors.py:45-66)
+    Text t;
+    if (fail_begin(C, d.status, d.aux0, d.aux1, &t)) {
+      switch (d.status) {
+        case UPY_ST_UNKNOWN_OPCODE:
+          m_puts(C, &t, "unknown opcode "); m_i64(C, &t, d.aux0);
+          m_puts(C, &t, " at offset "); m_i64(C, &t, d.aux1);
+          break;
+        case UPY_ST_BAD_JUMP_TARGET:
+          m_puts(C, &t, "jump at offset "); m_i64(C, &t, d.aux0);
+          m_puts(C, &t, " targets "); m_i64(C, &t, d.aux1);
+          m_puts(C, &t, ", not an instruction boundary");
+          break;
+        case UPY_ST_TRUNCATED_CODE:
+          // aux0: 1 empty, 2 odd, 3 inside EXTENDED_ARG run at aux1, 4 inside cache of opcode at aux1, 5 none
+          if (d.aux0 == 1) m_puts(C, &t, "empty code object");
+          else if (d.aux0 == 2) m_puts(C, &t, "odd code length");
+          else if (d.aux0 == 3) { m_puts(C, &t, "code ends inside EXTENDED_ARG run at "); m_i64(C, &t, d.aux1); }
+          else if (d.aux0 == 4) {
+            const upy_obj* o = K->o;
+            u32 opb = C->A->bytes[o->code_off + (d.aux1 - 2)];
+            m_puts(C, &t, "code ends inside inline cache of ");
+            m_puts(C, &t, opname_of(UPY_ENT_OP(optab(K->minor, opb))));
+            m_puts(C, &t, " at "); m_i64(C, &t, d.aux1);
+          } else m_puts(C, &t, "code holds no instruction");
+          C->aux0 = C->aux1 = 0;
+          break;
+        default:
+          m_puts(C, &t, "decode failed");
+      }
+      fail_end(C, &t);
+    }
+    return false;
+  }
+  i32 n = d.n_instrs;
+  K->n_ins = n;
+  K->ins = (Ins*)zalloc(C, (u64)n * sizeof(Ins));
+  CKR(C, false);
+  const upy_ins* src = C->ins_all + (K->o->code_off >> 1);
+  for (i32 i = 0; i < n; i++) {
+    const upy_ins& r = src[i];
+    u32 e = optab(K->minor, r.opcode);
+    Ins& x = K->ins[i];
+    x.offset = r.offset;
+    x.arg = r.arg;
+    x.op = UPY_ENT_OP(e);
+    x.kind = (u8)UPY_ENT_KIND(e);
+    x.nprefix = r.n_prefixes;
+    x.flags = r.flags & 3;
+    x.cache = r.cache_units;
+  }
+  return true;
+}
+
+// rewrite_yield_from (pipeline.py:57-87)
+HD inline void rewrite_yield_from(Dc* C, Code* K) {
+  bool any = false;
+  for (i32 i = 0; i < K->n_ins; i++)
+    if (K->ins[i].op == OP_SEND) any = true;
+  if (!any) return;
+  Ins* out = (Ins*)zalloc(C, (u64)K->n_ins * sizeof(Ins));
+  CK(C);
+  i32 n = 0, i = 0;
+  while (i < K->n_ins) {
+    const Ins& in = K->ins[i];
+    if (in.op == OP_SEND) {
+      u8 w0 = i + 1 < K->n_ins ? K->ins[i + 1].op : 0;
+      u8 w1 = i + 2 < K->n_ins ? K->ins[i + 2].op : 0;
+      u8 w2 = i + 3 < K->n_ins ? K->ins[i + 3].op : 0;
+      int skip = 0;
+      if (w0 == OP_YIELD_VALUE && w1 == OP_JUMP_BACKWARD_NO_INTERRUPT) skip = 3;
+      else if (w0 == OP_YIELD_VALUE && w1 == OP_RESUME && w2 == OP_JUMP_BACKWARD_NO_INTERRUPT) skip = 4;
+      if (skip && jump_target(K, K->ins[i + skip - 1]) == in.offset) {
+        const Ins& last = K->ins[i + skip - 1];
+        Ins y;
+        y.offset = in.offset;
+        y.arg = 0;
+        y.op = OP_YIELD_FROM_311;
+        y.kind = K_NONE;
+        y.nprefix = 0;
+        y.flags = 0;
+        y.cache = (ins_end(last) - in.offset) / 2 - 1;
+        out[n++] = y;
+        i += skip;
+        continue;
+      }
+    }
+    out[n++] = in;
+    i++;
+  }
+  K->ins = out;
+  K->n_ins = n;
+}
+
+// decode_exception_table (disasm.py:175-214)
+HD inline Vec<ExcEntry>* decode_exception_table(Dc* C, const Code* K) {
+  Vec<ExcEntry>* v = vnew<ExcEntry>(C);
+  const u8* data = C->A->bytes + K->o->exc_off;
+  u32 len = K->o->exc_len, pos = 0;
+  auto bad = [&](const char* what, u32 at) {
+    Text t;
+    if (fail_begin(C, UPY_ST_MALFORMED_EXCTABLE, 0, 0, &t)) {
+      m_puts(C, &t, what);
+      m_puts(C, &t, " at byte ");
+      m_i64(C, &t, at);
+      fail_end(C, &t);
+    }
+  };
+  auto varint = [&](bool first) -> u64 {
+    if (pos >= len) { bad("truncated varint", pos); return 0; }
+    u8 b = data[pos];
+    if (first && !(b & 0x80)) { bad("missing entry marker", pos); return 0; }
+    pos++;
+    u64 val = b & 0x3F;
+    while (b & 0x40) {
+      if (pos >= len) { bad("truncated varint", pos); return 0; }
+      b = data[pos];
+      if (b & 0x80) { bad("entry marker inside varint", pos); return 0; }
+      pos++;
+      val = (val << 6) | (b & 0x3F);
+    }
+    return val;
+  };
+  while (pos < len) {
+    u64 start = varint(true) * 2;
+    CKR(C, v);
+    u64 length = varint(false) * 2;
+    CKR(C, v);
+    u64 target = varint(false) * 2;
+    CKR(C, v);
+    u64 dl = varint(false);
+    CKR(C, v);
+    ExcEntry e;
+    e.start = (u32)start;
+    e.end = (u32)(start + length);
+    e.target = (u32)target;
+    e.depth = (u32)(dl >> 1);
+    e.lasti = dl & 1;
+    if (length == 0) {
+      Text t;
+      if (fail_begin(C, UPY_ST_MALFORMED_EXCTABLE, 0, 0, &t)) {
+        m_puts(C, &t, "empty range in entry at byte ");
+        m_i64(C, &t, pos);
+        fail_end(C, &t);
+      }
+      return v;
+    }
+    vpush(C, v, e);
+  }
+  return v;
+}
+
+// ------------------------------------------------------------ try regions
+HD inline u8 classify_handler(Dc* C, const Code* K, u32 handler) {  // structurer.py:91-103
+  i32 idx = index_of(C, K, handler);
+  CKR(C, RK_FINALLY);
+  const Ins* I = K->ins;
+  if (I[idx].op == OP_DUP_TOP) return RK_EXCEPT;
+  if (I[idx].op == OP_POP_TOP && idx + 2 < K->n_ins && I[idx + 1].op == OP_POP_TOP && I[idx + 2].op == OP_POP_TOP)
+    return RK_EXCEPT;
+  return RK_FINALLY;
+}
+HD inline bool is_as_cleanup(const Code* K, i32 idx) {  // structurer.py:154-160
+  if (idx + 3 > K->n_ins) return false;
+  const Ins* I = K->ins + idx;
+  return (I[0].op == OP_LOAD_CONST && I[1].op == OP_STORE_FAST && I[2].op == OP_DELETE_FAST) ||
+         (I[0].op == OP_LOAD_CONST && I[1].op == OP_STORE_NAME && I[2].op == OP_DELETE_NAME);
+}
+HD inline Vec<TryRegion>* match_try_regions(Dc* C, const Code* K, const Vec<ExcEntry>* exc) {
+  Vec<TryRegion>* out = vnew<TryRegion>(C);
+  const Ins* I = K->ins;
+  if (K->minor <= 10) {  // _regions_legacy (structurer.py:69-88)
+    for (i32 i = 0; i < K->n_ins; i++) {
+      if (I[i].op != OP_SETUP_FINALLY && I[i].op != OP_SETUP_WITH) continue;
+      TryRegion r;
+      r.start = ins_end(I[i]);
+      r.end = jump_target(K, I[i]);
+      r.handler = r.end;
+      r.kind = I[i].op == OP_SETUP_WITH ? RK_WITH : classify_handler(C, K, r.handler);
+      CKR(C, out);
+      r.setup_offset = I[i].offset;
+      vpush(C, out, r);
+    }
+    return out;
+  }
+  // _regions_311 (structurer.py:106-151)
+  for (u32 e = 0; exc && e < exc->n; e++) {
+    const ExcEntry& en = exc->d[e];
+    i32 ti = ins_index_of(K, en.target);
+    if (ti >= K->n_ins || I[ti].offset != en.target || I[ti].op != OP_PUSH_EXC_INFO) continue;
+    i32 idx = ti;
+    u8 kind = RK_FINALLY;
+    i32 j = idx + 1;
+    if (j < K->n_ins && I[j].op == OP_WITH_EXCEPT_START) {
+      kind = RK_WITH;
+    } else {
+      i32 k = j;
+      while (k < K->n_ins && k < j + 24) {
+        u8 op = I[k].op;
+        if (op == OP_CHECK_EXC_MATCH) { kind = RK_EXCEPT; break; }
+        if (op == OP_POP_TOP && k == j) { kind = RK_EXCEPT; break; }
+        if (op == OP_LOAD_GLOBAL || op == OP_LOAD_NAME || op == OP_LOAD_FAST || op == OP_LOAD_CONST ||
+            op == OP_LOAD_ATTR || op == OP_BUILD_TUPLE || op == OP_EXTENDED_ARG) {
+          k++;
+          continue;
+        }
+        break;
+      }
+      if (kind != RK_EXCEPT && is_as_cleanup(K, idx + 1)) kind = RK_AS_CLEANUP;
+    }
+    // merge fragments protecting the same handler (dict keyed by handler, insertion order)
+    bool merged = false;
+    for (u32 q = 0; q < out->n; q++) {
+      if (out->d[q].handler == en.target) {
+        if (en.start < out->d[q].start) out->d[q].start = en.start;
+        if (en.end > out->d[q].end) out->d[q].end = en.end;
+        merged = true;
+        break;
+      }
+    }
+    if (!merged) {
+      TryRegion r;
+      r.start = en.start;
+      r.end = en.end;
+      r.handler = en.target;
+      r.kind = kind;
+      r.setup_offset = -1;
+      vpush(C, out, r);
+    }
+  }
+  return out;
+}
+
+// ------------------------------------------------------------ basic blocks
+HD inline void link(Dc* C, Cfg* G, i32 src, u32 dst_off, u8 kind) {
+  i32 dst = block_at(G, dst_off);
+  if (dst < 0) {
+    py_error(C, UPY_ST_PY_KEY_ERROR, "block_at lookup");
+    return;
+  }
+  vpush(C, G->blocks[src].succ, dst);
+  vpush(C, G->blocks[src].succ_kind, kind);
+  vpush(C, G->blocks[dst].pred, src);
+}
+
+HD inline bool is_cond_for_cfg(u8 op) {  // cfg.py:122-127
+  switch (op) {
+    case OP_POP_JUMP_IF_FALSE: case OP_POP_JUMP_IF_TRUE: case OP_POP_JUMP_FORWARD_IF_FALSE:
+    case OP_POP_JUMP_FORWARD_IF_TRUE: case OP_POP_JUMP_BACKWARD_IF_FALSE: case OP_POP_JUMP_BACKWARD_IF_TRUE:
+    case OP_POP_JUMP_FORWARD_IF_NONE: case OP_POP_JUMP_FORWARD_IF_NOT_NONE:
+    case OP_POP_JUMP_BACKWARD_IF_NONE: case OP_POP_JUMP_BACKWARD_IF_NOT_NONE:
+    case OP_JUMP_IF_FALSE_OR_POP: case OP_JUMP_IF_TRUE_OR_POP: case OP_JUMP_IF_NOT_EXC_MATCH:
+    case OP_CALL_FINALLY:
+      return true;
+  }
+  return false;
+}
+HD inline bool is_setup_op(u8 op) {
+  return op == OP_SETUP_FINALLY || op == OP_SETUP_WITH || op == OP_SETUP_ASYNC_WITH;
+}
+
+HD inline void sort_u32(u32* a, i32 n) {  // heap sort (no recursion, no std)
+  auto sift = [&](i32 i, i32 m) {
+    while (true) {
+      i32 l = 2 * i + 1, r = l + 1, g = i;
+      if (l < m && a[l] > a[g]) g = l;
+      if (r < m && a[r] > a[g]) g = r;
+      if (g == i) return;
+      u32 t = a[i]; a[i] = a[g]; a[g] = t;
+      i = g;
+    }
+  };
+  for (i32 i = n / 2 - 1; i >= 0; i--) sift(i, n);
+  for (i32 m = n - 1; m > 0; m--) {
+    u32 t = a[0]; a[0] = a[m]; a[m] = t;
+    sift(0, m);
+  }
+}
+
+// build_basic_blocks (cfg.py:72-141)
+HD inline Cfg* build_basic_blocks(Dc* C, const Code* K, const Vec<ExcEntry>* entries) {
+  Cfg* G = anew<Cfg>(C);
+  CKR(C, G);
+  const Ins* I = K->ins;
+  i32 n = K->n_ins;
+  u32 end_of_code = ins_end(I[n - 1]);
+  G->end_of_code = end_of_code;
+  Vec<u32>* L = vnew<u32>(C, (u32)n + 8);
+  vpush(C, L, I[0].offset);
+  for (i32 i = 0; i < n; i++)
+    if (ins_is_jump(I[i])) vpush(C, L, jump_target(K, I[i]));
+  for (i32 i = 0; i < n; i++) {
+    u8 op = I[i].op;
+    bool ender = op == OP_RETURN_VALUE || op == OP_RAISE_VARARGS || op == OP_RERAISE || op == OP_END_FINALLY ||
+                 (ins_is_jump(I[i]) && !is_setup_op(op));
+    if (ender && ins_end(I[i]) < end_of_code) vpush(C, L, ins_end(I[i]));
+  }
+  for (u32 e = 0; entries && e < entries->n; e++) {
+    vpush(C, L, entries->d[e].target);
+    vpush(C, L, entries->d[e].start);
+    if (entries->d[e].end < end_of_code) vpush(C, L, entries->d[e].end);
+  }
+  CKR(C, G);
+  sort_u32(L->d, (i32)L->n);
+  u32 nu = 0;
+  for (u32 i = 0; i < L->n; i++)
+    if (nu == 0 || L->d[nu - 1] != L->d[i]) L->d[nu++] = L->d[i];
+  G->n_blocks = (i32)nu;
+  G->blocks = (Block*)zalloc(C, (u64)nu * sizeof(Block));
+  CKR(C, G);
+  i32 cursor = 0;
+  for (u32 b = 0; b < nu; b++) {
+    Block& B = G->blocks[b];
+    B.id = (i32)b;
+    B.start = L->d[b];
+    B.end = b + 1 < nu ? L->d[b + 1] : end_of_code;
+    while (cursor < n && I[cursor].offset < B.start) cursor++;
+    i32 lo = ins_index_of(K, B.start);
+    i32 hi = lo;
+    while (hi < n && I[hi].offset < B.end) hi++;
+    if (B.end <= B.start) hi = lo;
+    B.lo = lo;
+    B.hi = hi;
+    B.succ = vnew<i32>(C, 2);
+    B.succ_kind = vnew<u8>(C, 2);
+    B.pred = vnew<i32>(C, 2);
+    B.alive = true;
+  }
+  G->entry = block_at(G, I[0].offset);
+  for (u32 b = 0; b < nu; b++) {
+    CKR(C, G);
+    Block& B = G->blocks[b];
+    if (B.hi <= B.lo) continue;
+    const Ins& last = I[B.hi - 1];
+    u8 op = last.op;
+    bool falls = true;
+    if (op == OP_RETURN_VALUE || op == OP_RAISE_VARARGS || op == OP_RERAISE) {
+      falls = false;
+    } else if (op == OP_FOR_ITER) {
+      link(C, G, (i32)b, jump_target(K, last), EK_TAKEN);
+      link(C, G, (i32)b, ins_end(last), EK_NOT_TAKEN);
+      falls = false;
+    } else if (ins_is_jump(last) && !is_setup_op(op)) {
+      link(C, G, (i32)b, jump_target(K, last), EK_TAKEN);
+      if (is_cond_for_cfg(op)) link(C, G, (i32)b, ins_end(last), EK_NOT_TAKEN);
+      falls = false;
+    }
+    if (falls && B.end < end_of_code) link(C, G, (i32)b, B.end, EK_FALL);
+  }
+  for (u32 e = 0; entries && e < entries->n; e++) {
+    CKR(C, G);
+    const ExcEntry& en = entries->d[e];
+    i32 target = block_at(G, en.target);
+    for (u32 b = 0; b < nu; b++) {
+      Block& B = G->blocks[b];
+      if (B.start < en.end && B.end > en.start) {
+        bool has = false;
+        for (u32 q = 0; q < B.succ->n && !has; q++)
+          has = B.succ->d[q] == target && B.succ_kind->d[q] == EK_EXC;
+        if (!has && (i32)b != target) {
+          vpush(C, B.succ, target);
+          vpush(C, B.succ_kind, (u8)EK_EXC);
+          vpush(C, G->blocks[target].pred, (i32)b);
+        }
+      }
+    }
+  }
+  G->entries = (Vec<ExcEntry>*)entries;
+  return G;
+}
+
+// reachable_from (cfg.py:144-157) into a bitmap
+HD inline u8* reachable_from(Dc* C, const Cfg* G, i32 root, bool include_exc) {
+  u8* seen = (u8*)zalloc(C, (u64)G->n_blocks);
+  Vec<i32>* work = vnew<i32>(C, 16);
+  CKR(C, seen);
+  vpush(C, work, root);
+  while (work->n && !C->err) {
+    i32 b = work->d[--work->n];
+    if (seen[b]) continue;
+    seen[b] = 1;
+    const Block& B = G->blocks[b];
+    for (u32 q = 0; q < B.succ->n; q++) {
+      if (B.succ_kind->d[q] == EK_EXC && !include_exc) continue;
+      if (!seen[B.succ->d[q]]) vpush(C, work, B.succ->d[q]);
+    }
+  }
+  return seen;
+}
+
+// prune_unreachable (cfg.py:316-328)
+HD inline void prune_unreachable(Dc* C, Cfg* G) {
+  u8* keep = reachable_from(C, G, G->entry, true);
+  CK(C);
+  for (i32 b = 0; b < G->n_blocks; b++) {
+    Block& B = G->blocks[b];
+    if (!keep[b]) {
+      B.alive = false;
+      continue;
+    }
+    u32 w = 0;
+    for (u32 q = 0; q < B.succ->n; q++)
+      if (keep[B.succ->d[q]]) {
+        B.succ->d[w] = B.succ->d[q];
+        B.succ_kind->d[w] = B.succ_kind->d[q];
+        w++;
+      }
+    B.succ->n = w;
+    B.succ_kind->n = w;
+    w = 0;
+    for (u32 q = 0; q < B.pred->n; q++)
+      if (keep[B.pred->d[q]]) B.pred->d[w++] = B.pred->d[q];
+    B.pred->n = w;
+  }
+}
+
+HD inline bool has_normal_edge(const Block& P, i32 to) {
+  for (u32 q = 0; q < P.succ->n; q++)
+    if (P.succ->d[q] == to && P.succ_kind->d[q] != EK_EXC) return true;
+  return false;
+}
+
+// compute_dominators (cfg.py:160-220); idom[b] = -1 when b has no entry
+HD inline i32* compute_dominators(Dc* C, const Cfg* G, i32 root, const u8* universe) {
+  i32 nb = G->n_blocks;
+  i32* idom = (i32*)zalloc(C, (u64)nb * sizeof(i32));
+  i32* rpo_index = (i32*)zalloc(C, (u64)nb * sizeof(i32));
+  u8* seen = (u8*)zalloc(C, (u64)nb);
+  i32* order = (i32*)zalloc(C, (u64)nb * sizeof(i32));
+  i32* stk_b = (i32*)zalloc(C, (u64)nb * sizeof(i32));
+  u32* stk_q = (u32*)zalloc(C, (u64)nb * sizeof(u32));
+  CKR(C, idom);
+  for (i32 b = 0; b < nb; b++) idom[b] = -1;
+  // iterative DFS mirroring the recursive one (postorder)
+  i32 no = 0, sp = 0;
+  seen[root] = 1;
+  stk_b[sp] = root;
+  stk_q[sp] = 0;
+  sp++;
+  while (sp) {
+    i32 b = stk_b[sp - 1];
+    const Block& B = G->blocks[b];
+    u32& q = stk_q[sp - 1];
+    bool pushed = false;
+    while (q < B.succ->n) {
+      i32 s = B.succ->d[q];
+      u8 k = B.succ_kind->d[q];
+      q++;
+      if (k != EK_EXC && universe[s] && !seen[s]) {
+        seen[s] = 1;
+        stk_b[sp] = s;
+        stk_q[sp] = 0;
+        sp++;
+        pushed = true;
+        break;
+      }
+    }
+    if (!pushed) {
+      order[no++] = b;
+      sp--;
+    }
+  }
+  // rpo = reversed(order)
+  for (i32 i = 0; i < no; i++) rpo_index[order[no - 1 - i]] = i;
+  idom[root] = root;
+  bool changed = true;
+  while (changed && !C->err) {
+    changed = false;
+    for (i32 r = 0; r < no; r++) {
+      i32 b = order[no - 1 - r];
+      if (b == root) continue;
+      const Block& B = G->blocks[b];
+      i32 nw = -1;
+      for (u32 q = 0; q < B.pred->n; q++) {
+        i32 p = B.pred->d[q];
+        if (idom[p] < 0 || !universe[p] || !has_normal_edge(G->blocks[p], b)) continue;
+        if (nw < 0) {
+          nw = p;
+          continue;
+        }
+        i32 a = nw, c = p;
+        while (a != c) {
+          while (rpo_index[a] > rpo_index[c]) a = idom[a];
+          while (rpo_index[c] > rpo_index[a]) c = idom[c];
+        }
+        nw = a;
+      }
+      if (nw < 0) continue;
+      if (idom[b] != nw) {
+        idom[b] = nw;
+        changed = true;
+      }
+    }
+  }
+  return idom;
+}
+
+HD inline bool dominates(const i32* idom, i32 a, i32 b) {  // cfg.py:223-231
+  while (true) {
+    if (a == b) return true;
+    i32 parent = idom[b];
+    if (parent < 0 || parent == b) return a == b;
+    b = parent;
+  }
+}
+
+// analyze_loops (cfg.py:241-313); appends loops whose header is new to G->loops.
+// Returns false when irreducible.
+HD inline bool analyze_loops(Dc* C, Cfg* G, const i32* idom, const u8* universe) {
+  i32 nb = G->n_blocks;
+  // roots: universe blocks with no predecessor in the universe (any edge kind)
+  i32 root = -1;
+  i32 first_root = -1, min_u = -1;
+  for (i32 b = 0; b < nb; b++) {
+    if (!universe[b]) continue;
+    if (min_u < 0) min_u = b;
+    bool has = false;
+    const Block& B = G->blocks[b];
+    for (u32 q = 0; q < B.pred->n && !has; q++) has = universe[B.pred->d[q]] != 0;
+    if (!has && first_root < 0) first_root = b;
+  }
+  // Python iterates a set of small ints in ascending order when the table is large
+  // enough; roots is at most one element in practice, so take it.
+  if (first_root >= 0) root = first_root;
+  else root = universe[G->entry] ? G->entry : min_u;
+  if (root < 0) return true;
+  u8* visited = (u8*)zalloc(C, (u64)nb);
+  u8* onstack = (u8*)zalloc(C, (u64)nb);
+  i32* stk_b = (i32*)zalloc(C, (u64)nb * sizeof(i32));
+  u32* stk_q = (u32*)zalloc(C, (u64)nb * sizeof(u32));
+  Vec<i32>* ru = vnew<i32>(C, 8);
+  Vec<i32>* rv = vnew<i32>(C, 8);
+  CKR(C, true);
+  i32 sp = 0;
+  visited[root] = 1;
+  onstack[root] = 1;
+  stk_b[0] = root;
+  stk_q[0] = 0;
+  sp = 1;
+  while (sp && !C->err) {
+    i32 u = stk_b[sp - 1];
+    const Block& B = G->blocks[u];
+    u32& q = stk_q[sp - 1];
+    bool pushed = false;
+    while (q < B.succ->n) {
+      i32 v = B.succ->d[q];
+      u8 k = B.succ_kind->d[q];
+      q++;
+      if (k == EK_EXC || !universe[v]) continue;
+      if (!visited[v]) {
+        visited[v] = 1;
+        onstack[v] = 1;
+        stk_b[sp] = v;
+        stk_q[sp] = 0;
+        sp++;
+        pushed = true;
+        break;
+      } else if (onstack[v]) {
+        vpush(C, ru, u);
+        vpush(C, rv, v);
+      }
+    }
+    if (!pushed) {
+      onstack[u] = 0;
+      sp--;
+    }
+  }
+  bool reducible = true;
+  // back edges grouped by header in first-seen order
+  Vec<i32>* hdrs = vnew<i32>(C, 4);
+  Vec<Vec<i32>*>* tails = vnew<Vec<i32>*>(C, 4);
+  for (u32 e = 0; e < ru->n; e++) {
+    i32 u = ru->d[e], v = rv->d[e];
+    if (dominates(idom, v, u)) {
+      u32 h = 0;
+      while (h < hdrs->n && hdrs->d[h] != v) h++;
+      if (h == hdrs->n) {
+        vpush(C, hdrs, v);
+        vpush(C, tails, vnew<i32>(C, 2));
+      }
+      CKR(C, true);
+      vpush(C, tails->d[h], u);
+    } else {
+      reducible = false;
+    }
+  }
+  for (u32 h = 0; h < hdrs->n && !C->err; h++) {
+    i32 header = hdrs->d[h];
+    u8* body = (u8*)zalloc(C, (u64)nb);
+    Vec<i32>* work = vnew<i32>(C, 8);
+    CKR(C, reducible);
+    body[header] = 1;
+    for (u32 t = 0; t < tails->d[h]->n; t++) vpush(C, work, tails->d[h]->d[t]);
+    while (work->n && !C->err) {
+      i32 nn = work->d[--work->n];
+      if (body[nn]) continue;
+      body[nn] = 1;
+      const Block& N = G->blocks[nn];
+      for (u32 q = 0; q < N.pred->n; q++) {
+        i32 p = N.pred->d[q];
+        if (universe[p] && has_normal_edge(G->blocks[p], nn)) vpush(C, work, p);
+      }
+    }
+    if (G->loop_of_header[header] >= 0) continue;  // only new headers are added
+    Loop L;
+    L.header = header;
+    L.body = vnew<i32>(C, 8);
+    for (i32 b = 0; b < nb; b++)
+      if (body[b]) vpush(C, L.body, b);
+    L.back_tails = tails->d[h];
+    G->loop_of_header[header] = (i32)G->loops->n;
+    vpush(C, G->loops, L);
+  }
+  return reducible;
+}
+
+// analyze (pipeline.py:17-54)
+HD inline Cfg* analyze(Dc* C, Code* K) {
+  Vec<ExcEntry>* entries = vnew<ExcEntry>(C);
+  if (K->minor >= 11) {
+    rewrite_yield_from(C, K);
+    CKR(C, nullptr);
+    Vec<ExcEntry>* raw = decode_exception_table(C, K);
+    CKR(C, nullptr);
+    for (u32 e = 0; e < raw->n; e++) {
+      i32 ti = ins_index_of(K, raw->d[e].target);
+      if (ti < K->n_ins && K->ins[ti].offset == raw->d[e].target) vpush(C, entries, raw->d[e]);
+    }
+  } else {
+    Vec<TryRegion>* rs = match_try_regions(C, K, nullptr);
+    CKR(C, nullptr);
+    for (u32 r = 0; r < rs->n; r++) {
+      ExcEntry e;
+      e.start = rs->d[r].start;
+      e.end = rs->d[r].end;
+      e.target = rs->d[r].handler;
+      e.depth = 0;
+      e.lasti = false;
+      vpush(C, entries, e);
+    }
+  }
+  CKR(C, nullptr);
+  Cfg* G = build_basic_blocks(C, K, entries);
+  CKR(C, nullptr);
+  prune_unreachable(C, G);
+  CKR(C, nullptr);
+  G->loops = vnew<Loop>(C, 4);
+  G->loop_of_header = (i32*)zalloc(C, (u64)G->n_blocks * sizeof(i32));
+  CKR(C, nullptr);
+  for (i32 b = 0; b < G->n_blocks; b++) G->loop_of_header[b] = -1;
+  u8* uni = reachable_from(C, G, G->entry, false);
+  i32* idom = compute_dominators(C, G, G->entry, uni);
+  CKR(C, nullptr);
+  // universe of analyze_loops = set(idom)
+  u8* dom_set = (u8*)zalloc(C, (u64)G->n_blocks);
+  CKR(C, nullptr);
+  for (i32 b = 0; b < G->n_blocks; b++) dom_set[b] = idom[b] >= 0;
+  if (!analyze_loops(C, G, idom, dom_set)) {
+    CKR(C, nullptr);
+    fail_struct(C, G->entry, "irreducible control flow");
+    return nullptr;
+  }
+  CKR(C, nullptr);
+  u8* covered = dom_set;
+  for (u32 e = 0; e < entries->n; e++) {
+    i32 root = block_at(G, entries->d[e].target);
+    if (root < 0 || covered[root]) continue;
+    u8* reach = reachable_from(C, G, root, false);
+    u8* uni2 = (u8*)zalloc(C, (u64)G->n_blocks);
+    CKR(C, nullptr);
+    bool any = false;
+    for (i32 b = 0; b < G->n_blocks; b++) {
+      uni2[b] = reach[b] && !covered[b];
+      any |= uni2[b] != 0;
+    }
+    if (!any) continue;
+    uni2[root] = 1;
+    i32* sub = compute_dominators(C, G, root, uni2);
+    u8* sub_set = (u8*)zalloc(C, (u64)G->n_blocks);
+    CKR(C, nullptr);
+    for (i32 b = 0; b < G->n_blocks; b++) sub_set[b] = sub[b] >= 0;
+    if (!analyze_loops(C, G, sub, sub_set)) {
+      CKR(C, nullptr);
+      fail_struct(C, root, "irreducible control flow in handler");
+      return nullptr;
+    }
+    CKR(C, nullptr);
+    u8* nc = (u8*)zalloc(C, (u64)G->n_blocks);
+    CKR(C, nullptr);
+    for (i32 b = 0; b < G->n_blocks; b++) nc[b] = covered[b] | sub_set[b];
+    covered = nc;
+  }
+  return G;
+}

@@ -1,0 +1,381 @@
+// common.h -- per-thread decompile context: bump arena, growable vectors,
+// strings, error state and the frozen tables (opcodes, cmp_op, printable).
+//
+// Everything here compiles for sm_100a device code (one thread owns one root
+// code object and its arena slot) and, for the test-only host harness, as
+// plain C++.  Python-level failure semantics are modelled by a sticky status
+// in Dc: the first failure wins, every loop/recursive step checks `C->err`.
+#pragma once
+#include <stdint.h>
+#include <stddef.h>
+#include <string.h>
+#include "../../include/upy.h"
+#include "optables.h"
+#include "unicode_tables.h"
+
+#ifdef __CUDACC__
+#define HD __host__ __device__
+#define DI __device__ __forceinline__
+#else
+#define HD
+#define DI inline
+#endif
+
+typedef uint8_t u8;
+typedef uint16_t u16;
+typedef uint32_t u32;
+typedef uint64_t u64;
+typedef int32_t i32;
+typedef int64_t i64;
+
+// ------------------------------------------------------------------ tables
+#ifdef __CUDACC__
+__constant__ uint32_t UPY_OPTABLE_DEV[4][256] = UPY_OPTABLE_INIT;
+__constant__ uint32_t UPY_PRINTABLE_DEV[UPY_N_PRINTABLE_RANGES][2] = UPY_PRINTABLE_INIT;
+__constant__ int UPY_NCMP_DEV[4] = UPY_NCMP_INIT;
+__device__ const char* const UPY_OPNAMES_DEV[OP__COUNT] = UPY_OPNAMES_INIT;
+__device__ const char* const UPY_CMPOP_DEV[UPY_NCMP_ALL] = UPY_CMPOP_INIT;
+#endif
+static const uint32_t UPY_OPTABLE_HOST[4][256] = UPY_OPTABLE_INIT;
+static const uint32_t UPY_PRINTABLE_HOST[UPY_N_PRINTABLE_RANGES][2] = UPY_PRINTABLE_INIT;
+static const int UPY_NCMP_HOST[4] = UPY_NCMP_INIT;
+static const char* const UPY_OPNAMES_HOST[OP__COUNT] = UPY_OPNAMES_INIT;
+static const char* const UPY_CMPOP_HOST[UPY_NCMP_ALL] = UPY_CMPOP_INIT;
+
+#if defined(__CUDA_ARCH__)
+#define T_OPTABLE UPY_OPTABLE_DEV
+#define T_PRINTABLE UPY_PRINTABLE_DEV
+#define T_NCMP UPY_NCMP_DEV
+#define T_OPNAMES UPY_OPNAMES_DEV
+#define T_CMPOP UPY_CMPOP_DEV
+#else
+#define T_OPTABLE UPY_OPTABLE_HOST
+#define T_PRINTABLE UPY_PRINTABLE_HOST
+#define T_NCMP UPY_NCMP_HOST
+#define T_OPNAMES UPY_OPNAMES_HOST
+#define T_CMPOP UPY_CMPOP_HOST
+#endif
+
+HD inline u32 optab(int minor, u32 opcode) { return T_OPTABLE[minor - 8][opcode & 0xFF]; }
+HD inline const char* opname_of(int op) { return T_OPNAMES[op]; }
+
+HD inline size_t cstrlen(const char* s) {
+  size_t n = 0;
+  while (s[n]) n++;
+  return n;
+}
+
+// ------------------------------------------------------------------ strings
+// UTF-8 (surrogatepass) byte string; p == nullptr means Python None.
+struct Str {
+  const char* p;
+  u32 n;
+};
+HD inline Str S(const char* lit) { return Str{lit, (u32)cstrlen(lit)}; }
+HD inline Str Snone() { return Str{nullptr, 0}; }
+HD inline bool s_is_none(Str a) { return a.p == nullptr; }
+HD inline bool s_eq(Str a, Str b) {
+  if (a.p == nullptr || b.p == nullptr) return a.p == b.p;
+  if (a.n != b.n) return false;
+  if (a.p == b.p) return true;
+  for (u32 i = 0; i < a.n; i++)
+    if (a.p[i] != b.p[i]) return false;
+  return true;
+}
+HD inline bool s_eqc(Str a, const char* lit) {
+  if (a.p == nullptr) return false;
+  u32 i = 0;
+  for (; i < a.n; i++)
+    if (lit[i] == 0 || lit[i] != a.p[i]) return false;
+  return lit[i] == 0;
+}
+HD inline bool s_has(Str a, char ch) {
+  for (u32 i = 0; i < a.n; i++)
+    if (a.p[i] == ch) return true;
+  return false;
+}
+
+// ------------------------------------------------------------------ context
+struct NodeT;
+struct Dc;
+
+// Decoded instruction as the structurer sees it (disasm.py:28-52).
+struct Ins {
+  u32 offset;     // extent start
+  u32 arg;        // saturated arg
+  u8 op;          // canonical op id (optables.h)
+  u8 kind;        // UpyKind
+  u8 nprefix;
+  u8 flags;       // bit0 has_arg, bit1 arg saturated
+  u32 cache;      // cache units (3.11 yield-from collapse can exceed 255)
+};
+HD inline u32 ins_op_offset(const Ins& i) { return i.offset + 2 * i.nprefix; }
+HD inline u32 ins_end(const Ins& i) { return i.offset + 2 * (1 + i.nprefix + i.cache); }
+HD inline bool ins_is_jump(const Ins& i) {
+  return i.kind == K_JUMP_REL || i.kind == K_JUMP_ABS || i.kind == K_JUMP_BACK;
+}
+HD inline bool ins_has_arg(const Ins& i) { return i.flags & 1; }
+
+struct Dc {
+  // arena
+  u8* base;
+  u64 cap;
+  u64 used;
+  u8* sink;        // scratch returned after an overflow (zeroed), SINK_BYTES long
+  // status (first failure wins)
+  int err;
+  i64 aux0, aux1;
+  // message of the failure (device-formatted)
+  char* msg;
+  u32 msg_len, msg_cap;
+  // inputs
+  const upy_arena* A;
+  const upy_ins* ins_all;
+  const upy_decoded* dec_all;
+  // recursion guard
+  int depth;
+  int max_depth;
+};
+
+#define SINK_BYTES (64u * 1024u)
+
+HD inline void* zalloc(Dc* C, u64 bytes) {
+  bytes = (bytes + 15) & ~(u64)15;
+  if (C->used + bytes > C->cap) {
+    if (!C->err) {
+      C->err = UPY_ST_ARENA_OVERFLOW;
+      C->aux0 = (i64)C->used;
+      C->aux1 = (i64)bytes;
+    }
+    u64 z = bytes < SINK_BYTES ? bytes : SINK_BYTES;
+    memset(C->sink, 0, z);
+    return C->sink;
+  }
+  void* p = C->base + C->used;
+  C->used += bytes;
+  memset(p, 0, bytes);
+  return p;
+}
+template <class T>
+HD inline T* anew(Dc* C) {
+  return (T*)zalloc(C, sizeof(T));
+}
+
+// ------------------------------------------------------------------ vectors
+template <class T>
+struct Vec {
+  T* d;
+  u32 n, cap;
+};
+template <class T>
+HD inline Vec<T>* vnew(Dc* C, u32 cap = 0) {
+  Vec<T>* v = anew<Vec<T>>(C);
+  if (cap && !C->err) {
+    u64 b = (u64)cap * sizeof(T);
+    if (b > SINK_BYTES && C->used + b > C->cap) {
+      zalloc(C, b);  // records the overflow
+      return v;
+    }
+    v->d = (T*)zalloc(C, b);
+    v->cap = C->err ? 0 : cap;
+  }
+  return v;
+}
+template <class T>
+HD inline bool vgrow(Dc* C, Vec<T>* v, u32 need) {
+  if (need <= v->cap) return true;
+  if (C->err) return false;
+  u32 nc = v->cap ? v->cap * 2 : 4;
+  while (nc < need) nc *= 2;
+  T* nd = (T*)zalloc(C, (u64)nc * sizeof(T));
+  if (C->err) return false;
+  for (u32 i = 0; i < v->n; i++) nd[i] = v->d[i];
+  v->d = nd;
+  v->cap = nc;
+  return true;
+}
+template <class T>
+HD inline void vpush(Dc* C, Vec<T>* v, T x) {
+  if (v->n >= v->cap && !vgrow(C, v, v->n + 1)) return;
+  v->d[v->n++] = x;
+}
+template <class T>
+HD inline Vec<T>* vcopy(Dc* C, const Vec<T>* src, u32 lo = 0, u32 hi = 0xFFFFFFFFu) {
+  u32 n = src ? src->n : 0;
+  if (hi > n) hi = n;
+  if (lo > hi) lo = hi;
+  Vec<T>* v = vnew<T>(C, hi - lo);
+  if (C->err) return v;
+  for (u32 i = lo; i < hi; i++) v->d[i - lo] = src->d[i];
+  v->n = hi - lo;
+  return v;
+}
+template <class T>
+HD inline void vextend(Dc* C, Vec<T>* dst, const Vec<T>* src, u32 lo = 0, u32 hi = 0xFFFFFFFFu) {
+  if (!src) return;
+  if (hi > src->n) hi = src->n;
+  if (lo >= hi) return;
+  if (!vgrow(C, dst, dst->n + (hi - lo))) return;
+  for (u32 i = lo; i < hi; i++) dst->d[dst->n++] = src->d[i];
+}
+template <class T>
+HD inline T vlast(const Vec<T>* v) { return v->d[v->n - 1]; }
+
+// ------------------------------------------------------------------ text
+struct Text {
+  char* d;
+  u32 n, cap;
+};
+HD inline bool t_grow(Dc* C, Text* t, u32 need) {
+  if (need <= t->cap) return true;
+  if (C->err) return false;
+  u32 nc = t->cap ? t->cap * 2 : 256;
+  while (nc < need) nc *= 2;
+  char* nd = (char*)zalloc(C, nc);
+  if (C->err) return false;
+  memcpy(nd, t->d, t->n);
+  t->d = nd;
+  t->cap = nc;
+  return true;
+}
+HD inline void t_putn(Dc* C, Text* t, const char* p, u32 n) {
+  if (!n) return;
+  if (!t_grow(C, t, t->n + n)) return;
+  memcpy(t->d + t->n, p, n);
+  t->n += n;
+}
+HD inline void t_put(Dc* C, Text* t, char ch) {
+  if (t->n >= t->cap && !t_grow(C, t, t->n + 1)) return;
+  t->d[t->n++] = ch;
+}
+HD inline void t_puts(Dc* C, Text* t, const char* s) { t_putn(C, t, s, (u32)cstrlen(s)); }
+HD inline void t_str(Dc* C, Text* t, Str s) { t_putn(C, t, s.p, s.n); }
+HD inline void t_i64(Dc* C, Text* t, i64 v) {
+  char buf[24];
+  int k = 0;
+  u64 m = v < 0 ? (u64)(-(v + 1)) + 1 : (u64)v;
+  do {
+    buf[k++] = (char)('0' + (m % 10));
+    m /= 10;
+  } while (m);
+  if (v < 0) t_put(C, t, '-');
+  while (k) t_put(C, t, buf[--k]);
+}
+HD inline Str t_as_str(const Text* t) { return Str{t->d, t->n}; }
+
+// ------------------------------------------------------------------ errors
+// Failure with a device-formatted message: fail_begin() returns the message
+// buffer (or nullptr when a failure is already recorded).
+struct MsgBuf {
+  Dc* C;
+  Text t;
+};
+HD inline bool fail_begin(Dc* C, int status, i64 a0, i64 a1, Text* out) {
+  if (C->err) return false;
+  C->err = status;
+  C->aux0 = a0;
+  C->aux1 = a1;
+  out->d = C->msg;
+  out->n = 0;
+  out->cap = C->msg_cap;
+  return true;
+}
+HD inline void fail_end(Dc* C, Text* t) {
+  // message buffer is fixed (never grows: t_grow refuses once err is set)
+  C->msg_len = t->n;
+}
+// Message appenders that work after err is set (fixed buffer, truncating).
+HD inline void m_putn(Dc* C, Text* t, const char* p, u32 n) {
+  for (u32 i = 0; i < n && t->n < t->cap; i++) t->d[t->n++] = p[i];
+}
+HD inline void m_puts(Dc* C, Text* t, const char* s) { m_putn(C, t, s, (u32)cstrlen(s)); }
+HD inline void m_str(Dc* C, Text* t, Str s) { m_putn(C, t, s.p, s.n); }
+HD inline void m_i64(Dc* C, Text* t, i64 v) {
+  char buf[24];
+  int k = 0;
+  u64 m = v < 0 ? (u64)(-(v + 1)) + 1 : (u64)v;
+  do {
+    buf[k++] = (char)('0' + (m % 10));
+    m /= 10;
+  } while (m);
+  if (v < 0) m_putn(C, t, "-", 1);
+  while (k) {
+    char ch = buf[--k];
+    m_putn(C, t, &ch, 1);
+  }
+}
+
+// Plain-message failures.
+HD inline void fail_msg(Dc* C, int status, const char* m, i64 a0 = 0, i64 a1 = 0) {
+  Text t;
+  if (!fail_begin(C, status, a0, a1, &t)) return;
+  m_puts(C, &t, m);
+  fail_end(C, &t);
+}
+HD inline void py_error(Dc* C, int status, const char* what) { fail_msg(C, status, what); }
+
+// StackUnderflow(offset, opname)  errors.py:69-72
+HD inline void fail_underflow(Dc* C, const Ins* ins) {
+  Text t;
+  if (!fail_begin(C, UPY_ST_STACK_UNDERFLOW, ins->offset, 0, &t)) return;
+  m_puts(C, &t, "evaluation stack underflow at offset ");
+  m_i64(C, &t, ins->offset);
+  m_puts(C, &t, " (");
+  m_puts(C, &t, opname_of(ins->op));
+  m_puts(C, &t, ")");
+  fail_end(C, &t);
+}
+// UnsupportedOpcode(opname, offset)  errors.py:75-81
+HD inline void fail_unsupported(Dc* C, const char* opname, i64 offset) {
+  Text t;
+  if (!fail_begin(C, UPY_ST_UNSUPPORTED_OPCODE, offset, 0, &t)) return;
+  m_puts(C, &t, "no lifting rule for ");
+  m_puts(C, &t, opname);
+  m_puts(C, &t, " at offset ");
+  m_i64(C, &t, offset);
+  fail_end(C, &t);
+}
+// StructuringFailed(block_id, reason)  errors.py:92-96
+HD inline void fail_struct(Dc* C, i64 block_id, const char* reason) {
+  Text t;
+  if (!fail_begin(C, UPY_ST_STRUCTURING_FAILED, block_id, 0, &t)) return;
+  m_puts(C, &t, "cannot structure region at block ");
+  m_i64(C, &t, block_id);
+  m_puts(C, &t, ": ");
+  m_puts(C, &t, reason);
+  fail_end(C, &t);
+}
+// StackDepthMismatch(block_id, depths)  errors.py:84-89; depths an int or a 2-list
+HD inline void fail_depth(Dc* C, i64 block_id, i64 d0, i64 d1, bool is_list) {
+  Text t;
+  if (!fail_begin(C, UPY_ST_STACK_DEPTH_MISMATCH, block_id, 0, &t)) return;
+  m_puts(C, &t, "predecessors of block ");
+  m_i64(C, &t, block_id);
+  m_puts(C, &t, " disagree on stack depth: ");
+  if (is_list) {
+    m_puts(C, &t, "[");
+    m_i64(C, &t, d0);
+    m_puts(C, &t, ", ");
+    m_i64(C, &t, d1);
+    m_puts(C, &t, "]");
+  } else {
+    m_i64(C, &t, d0);
+  }
+  fail_end(C, &t);
+}
+
+// recursion guard (the reference runs under Python's default limit of 1000)
+struct DepthGuard {
+  Dc* C;
+  HD DepthGuard(Dc* c) : C(c) {
+    if (++C->depth > C->max_depth && !C->err) {
+      fail_msg(C, UPY_ST_DEPTH_LIMIT, "device recursion guard");
+    }
+  }
+  HD ~DepthGuard() { --C->depth; }
+};
+#define GUARD(C) DepthGuard _g_(C)
+#define CK(C) \
+  if ((C)->err) return
+#define CKR(C, v) \
+  if ((C)->err) return (v)

@@ -1,0 +1,322 @@
+// decode.h -- wordcode decoding (disasm.py:71-172) into upy_ins records.
+//
+// decode_scalar: one thread walks the object in reference order (used for
+//   3.11 objects, whose cache-unit skipping makes instruction starts a serial
+//   chain, and by the host harness).
+// decode_warp:   one warp per object for 3.8-3.10 (no caches: every unit is an
+//   instruction unit).  Lanes own 8 consecutive units (one 128-bit load each),
+//   EXTENDED_ARG runs are folded with a warp shuffle scan over (all-prefix,
+//   run length, run value) summaries, record slots come from a popc scan, and
+//   jump targets are validated inline: in <=3.10 an offset is an extent start
+//   iff it is in range and the previous unit is not EXTENDED_ARG.
+#pragma once
+#include "common.h"
+
+#define EXT_OP 144
+
+// error aux conventions (consumed by cfg.h load_instructions):
+//   UNKNOWN_OPCODE: aux0 opcode, aux1 offset
+//   TRUNCATED_CODE: aux0 reason (1 empty, 2 odd, 3 ext run, 4 cache, 5 none), aux1 position
+//   BAD_JUMP_TARGET: aux0 offset, aux1 target
+HD inline i64 jump_target_u64(int minor, u32 kind, u64 op_offset, u64 arg, bool* ok) {
+  *ok = true;
+  if (kind == K_JUMP_ABS) return (i64)(minor == 10 ? arg * 2 : arg);
+  if (kind == K_JUMP_BACK) return (i64)(op_offset + 2) - (i64)(2 * arg);
+  return (i64)(op_offset + 2 + (minor >= 10 ? arg * 2 : arg));
+}
+
+HD inline void decode_scalar(const u8* code, u32 len, int minor, upy_ins* rec, upy_decoded* res) {
+  res->status = UPY_ST_OK;
+  res->n_instrs = 0;
+  res->aux0 = res->aux1 = 0;
+  if (!len) {
+    res->status = UPY_ST_TRUNCATED_CODE;
+    res->aux0 = 1;
+    return;
+  }
+  if (len & 1) {
+    res->status = UPY_ST_TRUNCATED_CODE;
+    res->aux0 = 2;
+    return;
+  }
+  u32 i = 0, n = 0, nprefix = 0, extent = 0;
+  u64 ext = 0;
+  bool sat = false;
+  while (i < len) {
+    u32 op = code[i];
+    u32 e = optab(minor, op);
+    if (!e) {
+      res->status = UPY_ST_UNKNOWN_OPCODE;
+      res->aux0 = op;
+      res->aux1 = i;
+      return;
+    }
+    if (op == EXT_OP) {
+      if (nprefix >= 7) sat = true;
+      ext = (ext | code[i + 1]) << 8;
+      nprefix++;
+      i += 2;
+      if (i >= len) {
+        res->status = UPY_ST_TRUNCATED_CODE;
+        res->aux0 = 3;
+        res->aux1 = i;
+        return;
+      }
+      continue;
+    }
+    u64 arg = UPY_ENT_HASARG(e) ? (code[i + 1] | ext) : 0;
+    upy_ins& r = rec[n];
+    r.offset = extent;
+    r.opcode = (u8)op;
+    r.n_prefixes = (u8)(nprefix > 255 ? 255 : nprefix);
+    u32 cache = UPY_ENT_CACHE(e);
+    r.cache_units = (u8)cache;
+    bool big = sat || (arg >> 32);
+    r.arg = big ? 0xFFFFFFFFu : (u32)arg;
+    r.flags = (u8)(UPY_ENT_HASARG(e) | (big ? 2 : 0));
+    i += 2;
+    if (cache) {
+      u32 end = i + 2 * cache;
+      if (end > len) {
+        res->status = UPY_ST_TRUNCATED_CODE;
+        res->aux0 = 4;
+        res->aux1 = i;
+        return;
+      }
+      i = end;
+    }
+    n++;
+    ext = 0;
+    sat = false;
+    nprefix = 0;
+    extent = i;
+  }
+  if (!n) {
+    res->status = UPY_ST_TRUNCATED_CODE;
+    res->aux0 = 5;
+    return;
+  }
+  res->n_instrs = (i32)n;
+  // resolve_jump_targets: first jump (in order) whose target is not an extent start
+  for (u32 k = 0; k < n; k++) {
+    u32 e = optab(minor, rec[k].opcode);
+    u32 kind = UPY_ENT_KIND(e);
+    if (kind != K_JUMP_REL && kind != K_JUMP_ABS && kind != K_JUMP_BACK) continue;
+    u64 arg = rec[k].arg;
+    bool ok;
+    i64 t = jump_target_u64(minor, kind, rec[k].offset + 2ull * rec[k].n_prefixes, arg, &ok);
+    bool valid = false;
+    if (!(rec[k].flags & 2) && t >= 0 && t <= 0xFFFFFFFFll) {
+      u32 lo = 0, hi = n;
+      while (lo < hi) {
+        u32 mid = (lo + hi) >> 1;
+        if ((i64)rec[mid].offset < t) lo = mid + 1;
+        else hi = mid;
+      }
+      valid = lo < n && (i64)rec[lo].offset == t;
+    }
+    if (!valid) {
+      res->status = UPY_ST_BAD_JUMP_TARGET;
+      res->aux0 = rec[k].offset;
+      res->aux1 = t;
+      return;
+    }
+  }
+}
+
+#ifdef __CUDACC__
+// Summary of a span of units w.r.t. the pending EXTENDED_ARG run at its end.
+struct ExtRun {
+  u32 all;   // 1 if every unit of the span is EXTENDED_ARG (empty span: identity)
+  u32 len;   // trailing EXTENDED_ARG run length
+  u64 val;   // trailing run bytes concatenated (exact while len <= 7)
+};
+__device__ __forceinline__ ExtRun ext_combine(ExtRun a, ExtRun b) {  // a then b
+  if (!b.all) return b;
+  ExtRun r;
+  r.all = a.all;
+  r.len = a.len + b.len;
+  u32 sh = 8 * b.len;
+  r.val = sh >= 64 ? b.val : ((a.val << sh) | b.val);
+  return r;
+}
+__device__ __forceinline__ ExtRun shfl_up_run(ExtRun x, int d) {
+  ExtRun r;
+  r.all = __shfl_up_sync(0xffffffffu, x.all, d);
+  r.len = __shfl_up_sync(0xffffffffu, x.len, d);
+  r.val = __shfl_up_sync(0xffffffffu, x.val, d);
+  return r;
+}
+__device__ __forceinline__ ExtRun shfl_run(ExtRun x, int src) {
+  ExtRun r;
+  r.all = __shfl_sync(0xffffffffu, x.all, src);
+  r.len = __shfl_sync(0xffffffffu, x.len, src);
+  r.val = __shfl_sync(0xffffffffu, x.val, src);
+  return r;
+}
+
+// One warp decodes one <=3.10 object.  Must be called by all 32 lanes.
+__device__ __forceinline__ void decode_warp(const u8* __restrict__ code, u32 len, int minor,
+                                            upy_ins* __restrict__ rec, upy_decoded* res) {
+  const int lane = threadIdx.x & 31;
+  if (len == 0 || (len & 1)) {
+    if (lane == 0) {
+      res->status = UPY_ST_TRUNCATED_CODE;
+      res->n_instrs = 0;
+      res->aux0 = len == 0 ? 1 : 2;
+      res->aux1 = 0;
+    }
+    return;
+  }
+  const u32 units = len >> 1;
+  ExtRun carry = {0, 0, 0};     // state entering the chunk
+  u32 n_before = 0;              // instructions emitted in earlier chunks
+  i64 bad_ins = -1;              // first bad jump (instruction index) so far
+  i64 bad_off = 0, bad_tgt = 0;
+  for (u32 base = 0; base < units; base += 256) {
+    // 128-bit load: lane owns units [base + 8*lane, +8)
+    u32 u0 = base + 8 * lane;
+    uint4 w = make_uint4(0, 0, 0, 0);
+    u32 nu = 0;
+    if (u0 < units) {
+      nu = units - u0 < 8 ? units - u0 : 8;
+      if (nu == 8) {
+        w = *reinterpret_cast<const uint4*>(code + 2 * u0);
+      } else {
+        u32 tmp[4] = {0, 0, 0, 0};
+        for (u32 q = 0; q < 2 * nu; q++) tmp[q >> 2] |= (u32)code[2 * u0 + q] << (8 * (q & 3));
+        w = make_uint4(tmp[0], tmp[1], tmp[2], tmp[3]);
+      }
+    }
+    u32 words[4] = {w.x, w.y, w.z, w.w};
+    // per-unit opcode/arg bytes and table entries
+    u32 ops[8], argb[8], ent[8];
+    u32 ext_mask = 0, unknown_mask = 0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      u32 wd = words[q >> 1] >> (16 * (q & 1));
+      ops[q] = wd & 0xFF;
+      argb[q] = (wd >> 8) & 0xFF;
+      ent[q] = (u32)q < nu ? optab(minor, ops[q]) : 0;
+      if ((u32)q < nu) {
+        if (ops[q] == EXT_OP) ext_mask |= 1u << q;
+        if (!ent[q]) unknown_mask |= 1u << q;
+      }
+    }
+    // first unknown opcode of the warp chunk (reference order): stop the object
+    u32 has_unknown = __ballot_sync(0xffffffffu, unknown_mask != 0);
+    if (has_unknown) {
+      int first_lane = __ffs(has_unknown) - 1;
+      if (lane == first_lane) {
+        int q = __ffs(unknown_mask) - 1;
+        res->status = UPY_ST_UNKNOWN_OPCODE;
+        res->n_instrs = 0;
+        res->aux0 = ops[q];
+        res->aux1 = 2 * (u0 + q);
+      }
+      return;
+    }
+    // lane summary of its 8 units
+    ExtRun mine;
+    {
+      u32 valid_mask = nu >= 8 ? 0xFF : ((1u << nu) - 1);
+      mine.all = (nu > 0 && (ext_mask & valid_mask) == valid_mask) ? 1 : (nu == 0 ? 1 : 0);
+      // trailing run: from the top valid unit downward
+      u32 len_ = 0;
+      u64 val = 0;
+      for (int q = (int)nu - 1; q >= 0 && ((ext_mask >> q) & 1); q--) len_++;
+      for (u32 q = nu - len_; q < nu; q++) val = (val << 8) | argb[q];
+      mine.len = len_;
+      mine.val = val;
+    }
+    // inclusive scan over lanes, then exclusive = shifted
+    ExtRun inc = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      ExtRun o = shfl_up_run(inc, d);
+      if (lane >= d) inc = ext_combine(o, inc);
+    }
+    ExtRun excl = shfl_up_run(inc, 1);
+    if (lane == 0) excl = ExtRun{1, 0, 0};
+    excl = ext_combine(carry, excl);
+    // instruction slots: non-EXT units before this lane
+    u32 my_ins = (u32)__popc((~ext_mask) & (nu >= 8 ? 0xFF : ((1u << nu) - 1)));
+    u32 pre = my_ins;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      u32 o = __shfl_up_sync(0xffffffffu, pre, d);
+      if (lane >= d) pre += o;
+    }
+    u32 total = __shfl_sync(0xffffffffu, pre, 31);
+    u32 idx = n_before + pre - my_ins;
+    // walk my units with the incoming run
+    u32 run_len = excl.len;  // trailing EXTENDED_ARG run entering my span
+    u64 run_val = excl.val;
+    i64 my_bad = -1, my_bad_off = 0, my_bad_tgt = 0;
+    for (u32 q = 0; q < nu; q++) {
+      u32 u = u0 + q;
+      if ((ext_mask >> q) & 1) {
+        run_val = (run_val << 8) | argb[q];
+        run_len++;
+        continue;
+      }
+      u32 e = ent[q];
+      bool has_arg = UPY_ENT_HASARG(e);
+      u64 ext = run_len ? (run_len >= 8 ? 0 : (run_val << 8)) : 0;
+      bool sat = run_len >= 8;
+      u64 arg = has_arg ? (argb[q] | ext) : 0;
+      bool big = has_arg && (sat || (arg >> 32));
+      upy_ins r;
+      r.offset = 2 * (u - run_len);
+      r.arg = big ? 0xFFFFFFFFu : (u32)arg;
+      r.opcode = (u8)ops[q];
+      r.n_prefixes = (u8)(run_len > 255 ? 255 : run_len);
+      r.cache_units = 0;
+      r.flags = (u8)((has_arg ? 1 : 0) | (big ? 2 : 0));
+      rec[idx] = r;
+      u32 kind = UPY_ENT_KIND(e);
+      if (my_bad < 0 && (kind == K_JUMP_REL || kind == K_JUMP_ABS || kind == K_JUMP_BACK)) {
+        bool okk;
+        i64 t = jump_target_u64(minor, kind, 2ull * u, arg, &okk);
+        bool valid = !big && t >= 0 && t < (i64)len && !(t & 1) && (t == 0 || code[t - 2] != EXT_OP);
+        if (!valid) {
+          my_bad = idx;
+          my_bad_off = r.offset;
+          my_bad_tgt = t;
+        }
+      }
+      idx++;
+      run_len = 0;
+      run_val = 0;
+    }
+    // first bad jump of the chunk (lowest instruction index)
+    u32 badm = __ballot_sync(0xffffffffu, my_bad >= 0);
+    if (badm && bad_ins < 0) {
+      int bl = __ffs(badm) - 1;
+      bad_ins = __shfl_sync(0xffffffffu, my_bad, bl);
+      bad_off = __shfl_sync(0xffffffffu, my_bad_off, bl);
+      bad_tgt = __shfl_sync(0xffffffffu, my_bad_tgt, bl);
+    }
+    // carry into the next chunk: state after the whole chunk
+    carry = ext_combine(carry, shfl_run(inc, 31));
+    n_before += total;
+  }
+  if (lane == 0) {
+    if (carry.len) {  // code ends inside an EXTENDED_ARG run
+      res->status = UPY_ST_TRUNCATED_CODE;
+      res->n_instrs = 0;
+      res->aux0 = 3;
+      res->aux1 = len;
+    } else if (bad_ins >= 0) {
+      res->status = UPY_ST_BAD_JUMP_TARGET;
+      res->n_instrs = 0;
+      res->aux0 = bad_off;
+      res->aux1 = bad_tgt;
+    } else {
+      res->status = UPY_ST_OK;
+      res->n_instrs = (i32)n_before;
+      res->aux0 = res->aux1 = 0;
+    }
+  }
+}
+#endif

@@ -1,0 +1,275 @@
+// upy.cu -- sm_100a kernels and the C ABI of include/upy.h.
+//
+//   upy_decode_kernel      one warp per code object (roots and nested): HBM-bound
+//                          decode of co_code into 12-byte instruction records
+//                          (disasm.py:71-172).
+//   upy_decompile_kernel   persistent, one thread per root object at a time:
+//                          validate -> analyze -> structure -> recover -> emit
+//                          (pipeline.py:143-160) inside a per-thread arena slot,
+//                          then the text is appended to the flat output buffer.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include "pipeline.h"
+#include "decode.h"
+
+#define MSG_BYTES 4096u
+#define SLOT_HEADER (MSG_BYTES + SINK_BYTES)
+
+static __thread char g_last_error[512];
+static void set_err(const char* fmt, const char* a = "") {
+  snprintf(g_last_error, sizeof g_last_error, fmt, a);
+}
+
+__global__ void __launch_bounds__(256) upy_decode_kernel(upy_arena A, upy_ins* __restrict__ ins,
+                                                         upy_decoded* __restrict__ dec) {
+  const int lane = threadIdx.x & 31;
+  const i64 warp = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+  for (i64 o = warp; o < A.n_objs; o += nwarps) {
+    const upy_obj* ob = &A.objs[o];
+    const u8* code = A.bytes + ob->code_off;
+    upy_ins* rec = ins + (ob->code_off >> 1);
+    int minor = (int)ob->minor;
+    if (minor >= 8 && minor <= 10) {
+      decode_warp(code, ob->code_len, minor, rec, &dec[o]);
+    } else if (lane == 0) {
+      if (minor == 11) {
+        decode_scalar(code, ob->code_len, minor, rec, &dec[o]);
+      } else {
+        dec[o].status = UPY_ST_INTERNAL;
+        dec[o].n_instrs = 0;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+struct KParams {
+  upy_arena A;
+  const upy_ins* ins;
+  const upy_decoded* dec;
+  upy_out out;
+  u8* slots_base;
+  u64 slot_bytes;
+  u32* next_root;
+  int header;
+  int max_depth;
+  int indent_len, tool_len;
+  char indent[64];
+  char tool[64];
+};
+
+__global__ void __launch_bounds__(128) upy_decompile_kernel(KParams P) {
+  const u64 slot = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  u8* base = P.slots_base + slot * P.slot_bytes;
+  EmitOpts opt;
+  opt.header = P.header != 0;
+  opt.indent = Str{P.indent, (u32)P.indent_len};
+  opt.tool = Str{P.tool, (u32)P.tool_len};
+  while (true) {
+    u32 r = atomicAdd(P.next_root, 1u);
+    if (r >= (u64)P.A.n_roots) break;
+    u32 oi = (u32)P.A.roots[r];
+    Dc C;
+    C.msg = (char*)base;
+    C.msg_len = 0;
+    C.msg_cap = MSG_BYTES;
+    C.sink = base + MSG_BYTES;
+    C.base = base + SLOT_HEADER;
+    C.cap = P.slot_bytes - SLOT_HEADER;
+    C.used = 0;
+    C.err = 0;
+    C.aux0 = C.aux1 = 0;
+    C.A = &P.A;
+    C.ins_all = P.ins;
+    C.dec_all = P.dec;
+    C.depth = 0;
+    C.max_depth = P.max_depth;
+    Text out = {nullptr, 0, 0};
+    decompile_source(&C, oi, &opt, &out);
+    const char* src;
+    u32 len;
+    if (C.err) {
+      src = C.msg;
+      len = C.msg_len;
+    } else {
+      src = out.d;
+      len = out.n;
+    }
+    int status = C.err;
+    u64 off = atomicAdd((unsigned long long*)P.out.text_used, (unsigned long long)len);
+    if (off + len > P.out.text_cap) {
+      status = UPY_ST_OUTPUT_OVERFLOW;
+      len = 0;
+    } else {
+      u8* dst = P.out.text + off;
+      // 16-byte chunks where alignment allows
+      u32 q = 0;
+      if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0)
+        for (; q + 16 <= len; q += 16) *reinterpret_cast<uint4*>(dst + q) = *reinterpret_cast<const uint4*>(src + q);
+      for (; q < len; q++) dst[q] = (u8)src[q];
+    }
+    P.out.text_off[r] = off;
+    P.out.text_len[r] = len;
+    P.out.status[r] = status;
+    P.out.aux[2 * (u64)r] = C.aux0;
+    P.out.aux[2 * (u64)r + 1] = C.aux1;
+  }
+}
+
+// ------------------------------------------------------------ C ABI
+struct WsLayout {
+  u64 ins_off, dec_off, ctr_off, slots_off, total;
+  u64 slots, slot_bytes;
+};
+static u64 al(u64 x) { return (x + 255) & ~(u64)255; }
+
+static int sm_count() {
+  int dev = 0, n = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+static WsLayout layout(const upy_arena* a, const upy_options* o) {
+  WsLayout L;
+  u64 units = a->total_code_units + 1;
+  L.ins_off = 0;
+  L.dec_off = al(units * sizeof(upy_ins));
+  L.ctr_off = L.dec_off + al((u64)a->n_objs * sizeof(upy_decoded));
+  L.slots_off = L.ctr_off + 256;
+  u64 sb = o && o->arena_bytes ? o->arena_bytes : (u64)(256u << 10) + (u64)a->max_code_len * 512u;
+  sb = (sb + SLOT_HEADER + 255) & ~(u64)255;
+  L.slot_bytes = sb;
+  u64 slots;
+  if (o && o->slots > 0) {
+    slots = (u64)o->slots;
+  } else {
+    u64 cap_bytes = 24ull << 30;  // default arena budget
+    slots = cap_bytes / sb;
+    u64 full = (u64)sm_count() * 1024;
+    if (slots > full) slots = full;
+  }
+  if (slots > (u64)a->n_roots) slots = (u64)a->n_roots;
+  if (slots < 1) slots = 1;
+  int tpb = o && o->threads_per_block > 0 ? o->threads_per_block : 128;
+  slots = (slots + tpb - 1) / tpb * tpb;
+  L.slots = slots;
+  L.total = L.slots_off + slots * sb;
+  if (o && o->decode_only) L.total = L.slots_off;
+  return L;
+}
+
+extern "C" {
+
+size_t upy_abi_sizeof(int which) {
+  switch (which) {
+    case 0: return sizeof(upy_obj);
+    case 1: return sizeof(upy_const);
+    case 2: return sizeof(upy_str);
+    case 3: return sizeof(upy_arena);
+    case 4: return sizeof(upy_options);
+    case 5: return sizeof(upy_out);
+    case 6: return sizeof(upy_ins);
+    case 7: return sizeof(upy_decoded);
+  }
+  return 0;
+}
+int upy_abi_version(void) { return UPY_ABI_VERSION; }
+const char* upy_last_error(void) { return g_last_error; }
+
+int upy_query_workspace(const upy_arena* arena, const upy_options* opt, size_t* ws_bytes) {
+  if (!arena || !ws_bytes) {
+    set_err("upy_query_workspace: null argument");
+    return 1;
+  }
+  *ws_bytes = (size_t)layout(arena, opt).total;
+  return 0;
+}
+
+int upy_decode_batch(const upy_arena* arena, upy_ins* ins, upy_decoded* dec, void* stream) {
+  if (!arena || !ins || !dec) {
+    set_err("upy_decode_batch: null argument");
+    return 1;
+  }
+  if (arena->n_objs == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  int threads = 256;
+  i64 warps = arena->n_objs;
+  i64 blocks = (warps * 32 + threads - 1) / threads;
+  i64 max_blocks = (i64)sm_count() * 64;
+  if (blocks > max_blocks) blocks = max_blocks;
+  upy_decode_kernel<<<(unsigned)blocks, threads, 0, s>>>(*arena, ins, dec);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_err("decode launch: %s", cudaGetErrorString(e));
+    return 2;
+  }
+  return 0;
+}
+
+int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const upy_out* out, void* workspace,
+                        size_t ws_bytes, void* stream) {
+  if (!arena || !out || !workspace) {
+    set_err("upy_decompile_batch: null argument");
+    return 1;
+  }
+  WsLayout L = layout(arena, opt);
+  if (ws_bytes < L.total) {
+    set_err("upy_decompile_batch: workspace too small");
+    return 1;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  u8* ws = (u8*)workspace;
+  upy_ins* ins = (upy_ins*)(ws + L.ins_off);
+  upy_decoded* dec = (upy_decoded*)(ws + L.dec_off);
+  u32* ctr = (u32*)(ws + L.ctr_off);
+  int rc = upy_decode_batch(arena, ins, dec, stream);
+  if (rc) return rc;
+  if (opt && opt->decode_only) return 0;
+  if (arena->n_roots == 0) return 0;
+  static size_t stack_set = 0;
+  size_t want = 48 * 1024;
+  if (stack_set != want) {
+    cudaError_t e = cudaDeviceSetLimit(cudaLimitStackSize, want);
+    if (e != cudaSuccess) {
+      set_err("cudaDeviceSetLimit(stack): %s", cudaGetErrorString(e));
+      return 2;
+    }
+    stack_set = want;
+  }
+  cudaMemsetAsync(ctr, 0, 256, s);
+  KParams P;
+  memset(&P, 0, sizeof P);
+  P.A = *arena;
+  P.ins = ins;
+  P.dec = dec;
+  P.out = *out;
+  P.slots_base = ws + L.slots_off;
+  P.slot_bytes = L.slot_bytes;
+  P.next_root = ctr;
+  P.max_depth = 600;
+  if (opt) {
+    P.header = opt->header;
+    P.indent_len = opt->indent_len > 64 ? 64 : opt->indent_len;
+    memcpy(P.indent, opt->indent, P.indent_len);
+    P.tool_len = opt->tool_len > 64 ? 64 : opt->tool_len;
+    memcpy(P.tool, opt->tool, P.tool_len);
+  } else {
+    P.indent_len = 4;
+    memcpy(P.indent, "    ", 4);
+    P.tool_len = 6;
+    memcpy(P.tool, "unpyre", 6);
+  }
+  int tpb = opt && opt->threads_per_block > 0 ? opt->threads_per_block : 128;
+  unsigned blocks = (unsigned)(L.slots / tpb);
+  upy_decompile_kernel<<<blocks, tpb, 0, s>>>(P);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_err("decompile launch: %s", cudaGetErrorString(e));
+    return 2;
+  }
+  return 0;
+}
+
+}  // extern "C"

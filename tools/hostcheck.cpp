@@ -1,0 +1,63 @@
+// hostcheck.cpp -- TEST-ONLY host build of the device decompiler sources.
+//
+// Compiles the same headers the sm_100a kernels use (paper_2403_13839_b200/csrc)
+// with g++ so their logic can be diffed against the reference on CPU during
+// development (tools/dev_compare.py) and in the CPU test tier.  The product
+// never loads this library: the public API only calls libupy_cuda.so.
+#include <stdlib.h>
+#include <string.h>
+#include <vector>
+#include "../paper_2403_13839_b200/csrc/pipeline.h"
+#include "../paper_2403_13839_b200/csrc/decode.h"
+
+extern "C" int upyh_decompile(const upy_arena* A, int header, const char* indent, int indent_len, const char* tool,
+                              int tool_len, uint64_t arena_bytes, uint8_t* text, uint64_t text_cap,
+                              uint64_t* text_off, uint32_t* text_len, int32_t* status, int64_t* aux,
+                              upy_decoded* dec_out) {
+  std::vector<upy_ins> ins(A->total_code_units + 1);
+  std::vector<upy_decoded> dec(A->n_objs);
+  for (int64_t o = 0; o < A->n_objs; o++) {
+    const upy_obj* ob = &A->objs[o];
+    decode_scalar(A->bytes + ob->code_off, ob->code_len, (int)ob->minor, ins.data() + (ob->code_off >> 1), &dec[o]);
+    if (dec_out) dec_out[o] = dec[o];
+  }
+  std::vector<uint8_t> slot(arena_bytes);
+  std::vector<char> msg(4096);
+  std::vector<uint8_t> sink(SINK_BYTES);
+  EmitOpts opt;
+  opt.header = header != 0;
+  opt.indent = Str{indent, (u32)indent_len};
+  opt.tool = Str{tool, (u32)tool_len};
+  uint64_t used = 0;
+  for (int64_t r = 0; r < A->n_roots; r++) {
+    Dc C;
+    memset(&C, 0, sizeof C);
+    C.base = slot.data();
+    C.cap = arena_bytes;
+    C.sink = sink.data();
+    C.msg = msg.data();
+    C.msg_cap = 4096;
+    C.A = A;
+    C.ins_all = ins.data();
+    C.dec_all = dec.data();
+    C.max_depth = 600;
+    Text out = {nullptr, 0, 0};
+    decompile_source(&C, (u32)A->roots[r], &opt, &out);
+    const char* src = C.err ? C.msg : out.d;
+    uint32_t len = C.err ? C.msg_len : out.n;
+    int st = C.err;
+    if (used + len > text_cap) {
+      st = UPY_ST_OUTPUT_OVERFLOW;
+      len = 0;
+    } else if (len) {
+      memcpy(text + used, src, len);
+    }
+    text_off[r] = used;
+    text_len[r] = len;
+    status[r] = st;
+    aux[2 * r] = C.aux0;
+    aux[2 * r + 1] = C.aux1;
+    used += len;
+  }
+  return 0;
+}
