@@ -1,0 +1,183 @@
+"""Public host API: the reference's `decompile_source(code, style=None) -> str`
+surface (pipeline.py:143-160) as `decompile`, plus the batched
+`decompile_many(codes, style=None) -> list[str | UnpyreError]`.
+
+Host work is limited to packing CodeObjects into the arena image, one H2D copy,
+the C-ABI call (decode kernel + decompile kernel on the current CUDA stream),
+and reading back the flat text buffer.  Objects that hit a device capacity
+limit (per-thread arena, output buffer) are re-run on device with larger
+limits; nothing is ever computed on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi, _lib
+from .arena import Arena, pack
+from .errors import RETRYABLE, ST_OK, DeviceCapacityError, make_exception
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2403_13839_b200 requires a CUDA device (sm_100a); none is visible")
+    return torch
+
+
+@dataclass
+class BatchResult:
+    status: np.ndarray      # int32 [n_roots]
+    text_off: np.ndarray    # uint64
+    text_len: np.ndarray    # uint32
+    aux: np.ndarray         # int64 [n_roots, 2]
+    text: bytes             # flat UTF-8 buffer
+
+    def item(self, i):
+        s = self.text[int(self.text_off[i]):int(self.text_off[i]) + int(self.text_len[i])]
+        return int(self.status[i]), s.decode("utf-8", "surrogatepass")
+
+    def values(self):
+        out = []
+        for i in range(len(self.status)):
+            st, s = self.item(i)
+            out.append(s if st == ST_OK else make_exception(st, s, self.aux[i]))
+        return out
+
+
+class DeviceArena:
+    """An arena resident in HBM plus the workspace/output buffers to decompile it.
+
+    `run()` is stream-ordered and leaves every result on the device;
+    `fetch()` copies them back.  Used by the API and by bench.py (which times
+    `run()` on HBM-resident inputs and `upload()+run()+fetch()` end to end)."""
+
+    def __init__(self, arena: Arena, style=None, device=None, text_cap=None, arena_bytes=0, slots=0,
+                 threads_per_block=0, pinned=None):
+        torch = _torch()
+        self.torch = torch
+        self.lib = _lib.load()
+        self.arena = arena
+        self.device = torch.device(device or "cuda")
+        self.host = pinned if pinned is not None else torch.from_numpy(arena.blob).pin_memory()
+        self.dev = torch.empty(self.host.numel(), dtype=torch.uint8, device=self.device)
+        self.A = _abi.arena_struct(arena, self.dev.data_ptr())
+        self.opts = _abi.options(style, arena_bytes=arena_bytes, slots=slots,
+                                 threads_per_block=threads_per_block)
+        ws = C.c_size_t(0)
+        _lib.check(self.lib.upy_query_workspace(C.byref(self.A), C.byref(self.opts), C.byref(ws)),
+                   "upy_query_workspace")
+        self.ws_bytes = ws.value
+        self.ws = torch.empty(max(self.ws_bytes, 256), dtype=torch.uint8, device=self.device)
+        n = max(arena.n_roots, 1)
+        cap = text_cap or max(1 << 16, 8 * arena.code_bytes + 512 * arena.n_roots)
+        self.text = torch.empty(cap, dtype=torch.uint8, device=self.device)
+        # meta layout: [used u64 | pad][off u64 n][aux i64 2n][len u32 n][status i32 n]
+        self.out = _abi.UpyOut()
+        self.out.text = self.text.data_ptr()
+        self.out.text_cap = cap
+        self.meta = torch.zeros(64 + 32 * n, dtype=torch.uint8, device=self.device)
+        m = self.meta.data_ptr()
+        self.out.text_used = m
+        self.out.text_off = m + 64
+        self.out.aux = m + 64 + 8 * n
+        self.out.text_len = m + 64 + 24 * n
+        self.out.status = m + 64 + 28 * n
+        self.n = arena.n_roots
+
+    def upload(self, stream=None):
+        self.dev.copy_(self.host, non_blocking=True)
+
+    def run(self, stream=None):
+        torch = self.torch
+        s = stream or torch.cuda.current_stream(self.device)
+        self.meta[:8].zero_()
+        rc = self.lib.upy_decompile_batch(C.byref(self.A), C.byref(self.opts), C.byref(self.out),
+                                          C.c_void_p(self.ws.data_ptr()), C.c_size_t(self.ws_bytes),
+                                          C.c_void_p(s.cuda_stream))
+        _lib.check(rc, "upy_decompile_batch")
+
+    def fetch(self) -> BatchResult:
+        n = self.n
+        meta = self.meta.cpu().numpy()
+        used = int(meta[:8].view(np.uint64)[0])
+        used = min(used, self.out.text_cap)
+        off = meta[64:64 + 8 * n].view(np.uint64).copy()
+        aux = meta[64 + 8 * n:64 + 24 * n].view(np.int64).reshape(n, 2).copy()
+        ln = meta[64 + 24 * n:64 + 28 * n].view(np.uint32).copy()
+        st = meta[64 + 28 * n:64 + 32 * n].view(np.int32).copy()
+        text = self.text[:used].cpu().numpy().tobytes() if used else b""
+        return BatchResult(st, off, ln, aux, text)
+
+
+def run_arena(arena: Arena, style=None, device=None, retries=3) -> BatchResult:
+    """Decompile every root of a packed arena on the GPU (with on-device retries)."""
+    da = DeviceArena(arena, style, device)
+    da.upload()
+    da.run()
+    res = da.fetch()
+    bytes_per_slot = 0
+    text_scale = 1
+    for _ in range(retries):
+        redo = np.nonzero(np.isin(res.status, RETRYABLE))[0]
+        if not len(redo):
+            break
+        bytes_per_slot = (bytes_per_slot or da.ws_bytes // max(1, len(arena.section("roots")))) * 4
+        text_scale *= 4
+        sub = _subset(arena, redo)
+        db = DeviceArena(sub, style, device, text_cap=text_scale * max(1 << 16, 8 * sub.code_bytes),
+                         arena_bytes=max(bytes_per_slot, 64 << 20), slots=min(len(redo), 4096))
+        db.upload()
+        db.run()
+        r2 = db.fetch()
+        # splice retried results back
+        base = len(res.text)
+        res.text = res.text + r2.text
+        for j, i in enumerate(redo):
+            res.status[i] = r2.status[j]
+            res.text_off[i] = base + int(r2.text_off[j])
+            res.text_len[i] = r2.text_len[j]
+            res.aux[i] = r2.aux[j]
+    return res
+
+
+def _subset(arena: Arena, idx) -> Arena:
+    """Same objects, roots restricted to positions `idx` (a new roots section)."""
+    roots = arena.section("roots")[idx].copy()
+    blob = arena.blob.copy()
+    off = arena.offsets["roots"]
+    need = off + roots.nbytes
+    if need > len(blob):
+        blob = np.concatenate([blob, np.zeros(need - len(blob), np.uint8)])
+    blob[off:off + roots.nbytes] = roots.view(np.uint8)
+    counts = dict(arena.counts)
+    counts["roots"] = len(roots)
+    return Arena(blob, dict(arena.offsets), counts, arena.max_code_len, arena.total_code_units)
+
+
+def decompile_many(codes, style=None, device=None):
+    """Batched decompile_source: one entry per input, text or the exception
+    instance the reference would raise (the batch keeps going, like the CLI)."""
+    codes = list(codes)
+    if not codes:
+        return []
+    res = run_arena(pack(codes), style, device)
+    out = res.values()
+    for i, v in enumerate(out):
+        if isinstance(v, DeviceCapacityError):
+            raise v
+    return out
+
+
+def decompile(code, style=None, device=None) -> str:
+    """Drop-in for unpyre.decompile_source(code, style) (pipeline.py:143)."""
+    v = decompile_many([code], style, device)[0]
+    if isinstance(v, BaseException):
+        raise v
+    return v
+
+
+decompile_source = decompile

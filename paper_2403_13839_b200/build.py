@@ -1,0 +1,64 @@
+"""In-tree build of the sm_100a library (and the test-only host harness).
+
+    python -m paper_2403_13839_b200.build [--force]
+
+libupy_cuda.so is compiled with nvcc for sm_100a only.  The decompile kernel
+is one large, recursive, divergent function: full ptxas -O3 on it takes >10
+minutes for little gain on pointer-chasing code, so ptxas runs at -O2 (cicc
+stays at -O3).  See DESIGN.md "Build".
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libupy_cuda.so")
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared", "-Xcicc", "-O1", "-Xptxas", "-O1",
+              "-diag-suppress", "550"]
+
+
+def _deps():
+    out = [os.path.join(ROOT, "include", "upy.h")]
+    out += [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC))]
+    return out
+
+
+def up_to_date(target, deps):
+    if not os.path.exists(target):
+        return False
+    t = os.path.getmtime(target)
+    return all(os.path.getmtime(d) <= t for d in deps)
+
+
+def build_cuda(force=False, verbose=True):
+    if not force and up_to_date(LIB, _deps()):
+        return LIB
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB + ".tmp", os.path.join(CSRC, "upy.cu")]
+    if verbose:
+        print("[build]", " ".join(cmd), flush=True)
+    subprocess.check_call(cmd)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+def build_host(force=False):
+    from . import hostcheck
+
+    return hostcheck.build(force=force)
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    force = "--force" in argv
+    build_cuda(force)
+    build_host(force)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,83 @@
+"""Named parity cases: a spec dict -> CodeObject, and the golden sets built
+from them (tests/golden/*.jsonl are generated from these by the reference).
+"""
+from __future__ import annotations
+
+from . import corpus
+
+
+def build(spec):
+    g = spec["gen"]
+    m = spec.get("minor", 10)
+    kw = spec.get("kw", {})
+    if g == "fig1":
+        return corpus.fig1(m)[spec["index"]]
+    if g == "c3":
+        return corpus.c3(spec["seed"], m, **kw)
+    if g == "c4":
+        return corpus.c4(spec["seed"], m, **kw)
+    if g == "snippet":
+        from . import snippets
+
+        return snippets.SNIPPETS[spec["name"]](m)
+    if g == "fuzz":
+        from . import fuzz
+
+        return fuzz.program(spec["seed"], m, **kw)
+    raise KeyError(g)
+
+
+def _fig1():
+    out = []
+    for m in (10, 11):
+        for i in range(4):
+            out.append({"case": f"fig1-3.{m}-{i}", "gen": "fig1", "minor": m, "index": i})
+    out.append({"case": "fig1-3.10-0-header", "gen": "fig1", "minor": 10, "index": 0,
+                "style": {"indent": "    ", "header": True, "tool": "unpyre"}})
+    out.append({"case": "fig1-3.11-1-tabs", "gen": "fig1", "minor": 11, "index": 1,
+                "style": {"indent": "\t", "header": True, "tool": "b200"}})
+    return out
+
+
+def _c3(n=64):
+    return [{"case": f"c3-3.{m}-{s}", "gen": "c3", "minor": m, "seed": s} for m in (10, 11) for s in range(n)]
+
+
+def _c4(n=24):
+    out = []
+    for m in (10, 11):
+        for s in range(n):
+            units = (400, 1500, 4000)[s % 3]
+            out.append({"case": f"c4-3.{m}-{s}-{units}", "gen": "c4", "minor": m, "seed": s,
+                        "kw": {"target_units": units}})
+    return out
+
+
+def _snippets():
+    from . import snippets
+
+    return [{"case": f"snip-3.{m}-{name}", "gen": "snippet", "minor": m, "name": name}
+            for name, fn in snippets.SNIPPETS.items() for m in getattr(fn, "minors", (8, 9, 10, 11))]
+
+
+def _fuzz(n=400):
+    return [{"case": f"fuzz-3.{m}-{s}", "gen": "fuzz", "minor": m, "seed": s}
+            for m in (8, 9, 10, 11) for s in range(n)]
+
+
+class _Lazy(dict):
+    def __init__(self, **makers):
+        super().__init__()
+        self._makers = makers
+
+    def items(self):
+        return [(k, v()) for k, v in self._makers.items()]
+
+    def __getitem__(self, k):
+        return self._makers[k]()
+
+    def keys(self):
+        return self._makers.keys()
+
+
+GOLDEN_SETS = _Lazy(c1=_fig1, c3=_c3, c4=_c4, snippets=_snippets)
