@@ -84,7 +84,7 @@ typedef struct {
   int32_t slots;             /* concurrent per-thread arenas; 0 = auto */
   uint64_t arena_bytes;      /* bytes per slot arena; 0 = auto from max_code_len */
   int32_t decode_only;       /* 1: run only the decode kernel */
-  int32_t pad;
+  int32_t skip_decode;       /* 1: reuse the records of a previous decode_only call on the same workspace */
 } upy_options;
 
 /* Per-root results (device pointers, caller-allocated). */

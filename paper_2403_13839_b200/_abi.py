@@ -30,7 +30,7 @@ class UpyOptions(C.Structure):
         ("slots", C.c_int32),
         ("arena_bytes", C.c_uint64),
         ("decode_only", C.c_int32),
-        ("pad", C.c_int32),
+        ("skip_decode", C.c_int32),
     ]
 
 

@@ -91,10 +91,15 @@ class DeviceArena:
     def upload(self, stream=None):
         self.dev.copy_(self.host, non_blocking=True)
 
-    def run(self, stream=None):
+    def run(self, stream=None, mode="full"):
+        """mode: "full" (decode + decompile), "decode" (decode kernel only) or
+        "structure" (decompile kernel on the records of a previous "decode")."""
         torch = self.torch
         s = stream or torch.cuda.current_stream(self.device)
-        self.meta[:8].zero_()
+        self.opts.decode_only = 1 if mode == "decode" else 0
+        self.opts.skip_decode = 1 if mode == "structure" else 0
+        if mode != "decode":
+            self.meta[:8].zero_()
         rc = self.lib.upy_decompile_batch(C.byref(self.A), C.byref(self.opts), C.byref(self.out),
                                           C.c_void_p(self.ws.data_ptr()), C.c_size_t(self.ws_bytes),
                                           C.c_void_p(s.cuda_stream))

@@ -338,6 +338,53 @@ def unpack(arena: Arena, code_cls=CodeObject, const_cls=Const, version_cls=Versi
     return [obj(int(i)) for i in arena.section("roots")]
 
 
+def tile(arena: Arena, reps: int) -> Arena:
+    """Replicate every object `reps` times.  Each copy gets its own co_code
+    bytes (so the decoder reads reps x the bytecode) and its own object
+    records and roots; constant, string and name pools are shared read-only.
+    Used to build benchmark-scale corpora from a pool of distinct objects."""
+    objs = arena.section("objs")
+    by = arena.section("bytes")
+    roots = arena.section("roots")
+    code_end = int(max((int(o) + int(l) for o, l in zip(objs["code_off"], objs["code_len"])), default=0))
+    code_end = _align(code_end, 16)
+    rest_shift = (reps - 1) * code_end
+    n_obj = len(objs)
+    counts = dict(arena.counts)
+    counts["objs"] = n_obj * reps
+    counts["roots"] = len(roots) * reps
+    counts["bytes"] = int(arena.counts["bytes"]) + rest_shift
+    sizes = {"objs": OBJ_DTYPE.itemsize, "consts": CONST_DTYPE.itemsize, "strs": STR_DTYPE.itemsize,
+             "refs": 4, "limbs": 4, "bytes": 1, "roots": 4}
+    offsets = {}
+    total = 0
+    for s in SECTIONS:
+        offsets[s] = total
+        total = _align(total + counts[s] * sizes[s], ALIGN)
+    blob = np.zeros(total, dtype=np.uint8)
+    out = Arena(blob, offsets, counts, arena.max_code_len, (code_end * reps + 1) // 2)
+    o2 = out.section("objs").reshape(reps, n_obj)
+    o2[:] = objs[None, :]
+    o2["code_off"] += (np.arange(reps, dtype=np.uint64) * np.uint64(code_end))[:, None]
+    o2["exc_off"] += np.uint64(rest_shift)
+    o2["lnt_off"] += np.uint64(rest_shift)
+    c2 = out.section("consts")
+    c2[:] = arena.section("consts")
+    pay = (c2["kind"] == KIND_ID["str"]) | (c2["kind"] == KIND_ID["bytes"])
+    c2["off"][pay] += np.uint64(rest_shift)
+    s2 = out.section("strs")
+    s2[:] = arena.section("strs")
+    s2["off"] += np.uint64(rest_shift)
+    out.section("refs")[:] = arena.section("refs")
+    out.section("limbs")[:] = arena.section("limbs")
+    b2 = out.section("bytes")
+    b2[:code_end * reps].reshape(reps, code_end)[:] = by[:code_end][None, :]
+    b2[code_end * reps:] = by[code_end:]
+    r2 = out.section("roots").reshape(reps, len(roots))
+    r2[:] = roots[None, :] + (np.arange(reps, dtype=np.int32) * n_obj)[:, None]
+    return out
+
+
 def from_blob(blob, header):
     """Arena from a raw blob + the header dict written by the synthetic generator."""
     offsets = {s: int(header["off_" + s]) for s in SECTIONS}

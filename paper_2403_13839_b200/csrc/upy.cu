@@ -224,8 +224,10 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
   upy_ins* ins = (upy_ins*)(ws + L.ins_off);
   upy_decoded* dec = (upy_decoded*)(ws + L.dec_off);
   u32* ctr = (u32*)(ws + L.ctr_off);
-  int rc = upy_decode_batch(arena, ins, dec, stream);
-  if (rc) return rc;
+  if (!(opt && opt->skip_decode)) {
+    int rc = upy_decode_batch(arena, ins, dec, stream);
+    if (rc) return rc;
+  }
   if (opt && opt->decode_only) return 0;
   if (arena->n_roots == 0) return 0;
   static size_t stack_set = 0;

@@ -222,17 +222,18 @@ def c3(seed, minor=10, n_stmts=33):
 def c4(seed, minor=10, target_units=10000, max_depth=8):
     """Long nested-control-flow function of roughly target_units instructions."""
     g = _Gen(minor, Rng(splitmix64(0xC4 ^ seed)))
-    budget = [target_units]
+
+    def full():
+        return g.units() >= target_units
 
     def block(depth, n):
         for _ in range(n):
-            if budget[0] <= 0:
+            if full():
                 break
             stmt(depth)
 
     def stmt(depth):
         a, r = g.a, g.r
-        before = g.units()
         kind = r.below(10) if depth < max_depth else 0
         if kind <= 3:
             g.simple()
@@ -267,9 +268,8 @@ def c4(seed, minor=10, target_units=10000, max_depth=8):
                 a("JUMP_IF_NOT_EXC_MATCH", rr); a("POP_TOP"); a("POP_TOP"); a("POP_TOP")
                 block(depth + 1, 1 + r.below(3)); a("POP_EXCEPT"); a("JUMP_FORWARD", end)
                 a.label(rr); a("RERAISE", 0); a.label(end)
-        budget[0] -= g.units() - before
 
-    while budget[0] > 0:
+    while not full():
         stmt(0)
     g.finish()
     return g.a.build(f"c4_{seed}", argcount=2, stacksize=32)
