@@ -12,7 +12,7 @@ import os
 from . import _abi
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libupy_cuda.so")
+LIB_PATH = os.environ.get("UPY_LIB") or os.path.join(HERE, "libupy_cuda.so")
 _lib = None
 
 

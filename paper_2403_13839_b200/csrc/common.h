@@ -135,11 +135,36 @@ struct Dc {
   // recursion guard
   int depth;
   int max_depth;
+  // FuncExpr / BuildClass nodes created so far (recovery is an identity
+  // transform on trees that contain neither, see recover.h decompile_body)
+  u32 n_defs;
 };
 
 #define SINK_BYTES (64u * 1024u)
 
-HD inline void* zalloc(Dc* C, u64 bytes) {
+// 16-byte-granular zero / copy for 16-aligned arena blocks (device memset /
+// memcpy on generic pointers compile to byte loops).
+HD inline void zero16(void* p, u64 bytes) {
+#ifdef __CUDA_ARCH__
+  uint4* q = (uint4*)p;
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  for (u64 i = 0, n = bytes >> 4; i < n; i++) q[i] = z;
+#else
+  memset(p, 0, bytes);
+#endif
+}
+HD inline void copy16(void* dst, const void* src, u64 bytes) {  // both 16-aligned; copies ceil16(bytes)
+#ifdef __CUDA_ARCH__
+  uint4* d = (uint4*)dst;
+  const uint4* s = (const uint4*)src;
+  for (u64 i = 0, n = (bytes + 15) >> 4; i < n; i++) d[i] = s[i];
+#else
+  memcpy(dst, src, bytes);
+#endif
+}
+
+// Bump allocation; zeroed unless `zero` is false (buffers written before read).
+HD inline void* alloc_raw(Dc* C, u64 bytes, bool zero) {
   bytes = (bytes + 15) & ~(u64)15;
   if (C->used + bytes > C->cap) {
     if (!C->err) {
@@ -148,14 +173,16 @@ HD inline void* zalloc(Dc* C, u64 bytes) {
       C->aux1 = (i64)bytes;
     }
     u64 z = bytes < SINK_BYTES ? bytes : SINK_BYTES;
-    memset(C->sink, 0, z);
+    zero16(C->sink, z);
     return C->sink;
   }
   void* p = C->base + C->used;
   C->used += bytes;
-  memset(p, 0, bytes);
+  if (zero) zero16(p, bytes);
   return p;
 }
+HD inline void* zalloc(Dc* C, u64 bytes) { return alloc_raw(C, bytes, true); }
+HD inline void* ualloc(Dc* C, u64 bytes) { return alloc_raw(C, bytes, false); }
 template <class T>
 HD inline T* anew(Dc* C) {
   return (T*)zalloc(C, sizeof(T));
@@ -176,7 +203,7 @@ HD inline Vec<T>* vnew(Dc* C, u32 cap = 0) {
       zalloc(C, b);  // records the overflow
       return v;
     }
-    v->d = (T*)zalloc(C, b);
+    v->d = (T*)ualloc(C, b);
     v->cap = C->err ? 0 : cap;
   }
   return v;
@@ -187,9 +214,9 @@ HD inline bool vgrow(Dc* C, Vec<T>* v, u32 need) {
   if (C->err) return false;
   u32 nc = v->cap ? v->cap * 2 : 4;
   while (nc < need) nc *= 2;
-  T* nd = (T*)zalloc(C, (u64)nc * sizeof(T));
+  T* nd = (T*)ualloc(C, (u64)nc * sizeof(T));
   if (C->err) return false;
-  for (u32 i = 0; i < v->n; i++) nd[i] = v->d[i];
+  if (v->n) copy16(nd, v->d, (u64)v->n * sizeof(T));
   v->d = nd;
   v->cap = nc;
   return true;
@@ -206,7 +233,9 @@ HD inline Vec<T>* vcopy(Dc* C, const Vec<T>* src, u32 lo = 0, u32 hi = 0xFFFFFFF
   if (lo > hi) lo = hi;
   Vec<T>* v = vnew<T>(C, hi - lo);
   if (C->err) return v;
-  for (u32 i = lo; i < hi; i++) v->d[i - lo] = src->d[i];
+  if (lo == 0 && hi) copy16(v->d, src->d, (u64)hi * sizeof(T));
+  else
+    for (u32 i = lo; i < hi; i++) v->d[i - lo] = src->d[i];
   v->n = hi - lo;
   return v;
 }
@@ -231,9 +260,9 @@ HD inline bool t_grow(Dc* C, Text* t, u32 need) {
   if (C->err) return false;
   u32 nc = t->cap ? t->cap * 2 : 256;
   while (nc < need) nc *= 2;
-  char* nd = (char*)zalloc(C, nc);
+  char* nd = (char*)ualloc(C, nc);
   if (C->err) return false;
-  memcpy(nd, t->d, t->n);
+  if (t->n) copy16(nd, t->d, t->n);
   t->d = nd;
   t->cap = nc;
   return true;
@@ -241,7 +270,8 @@ HD inline bool t_grow(Dc* C, Text* t, u32 need) {
 HD inline void t_putn(Dc* C, Text* t, const char* p, u32 n) {
   if (!n) return;
   if (!t_grow(C, t, t->n + n)) return;
-  memcpy(t->d + t->n, p, n);
+  char* d = t->d + t->n;
+  for (u32 i = 0; i < n; i++) d[i] = p[i];
   t->n += n;
 }
 HD inline void t_put(Dc* C, Text* t, char ch) {

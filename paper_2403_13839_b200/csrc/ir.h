@@ -121,6 +121,7 @@ HD inline bool is_k(const Node* n, u8 k) { return n && n->k == k; }
 HD inline Node* mk(Dc* C, u8 k) {
   Node* n = anew<Node>(C);
   n->k = k;
+  if (k == E_FUNC || k == E_BUILDCLASS) C->n_defs++;
   return n;
 }
 HD inline Node* mk_const(Dc* C, u32 cid) {

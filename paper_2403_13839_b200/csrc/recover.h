@@ -563,6 +563,7 @@ HD inline NV* decompile_body(Dc* C, u32 oi) {
   CKR(C, nullptr);
   Code* K = anew<Code>(C);
   CKR(C, nullptr);
+  u32 defs_before = C->n_defs;
   if (!load_instructions(C, K, oi)) return nullptr;
   Cfg* G = analyze(C, K);
   CKR(C, nullptr);
@@ -572,13 +573,19 @@ HD inline NV* decompile_body(Dc* C, u32 oi) {
   CKR(C, nullptr);
   stmts = canonicalize_tree(C, stmts);
   CKR(C, nullptr);
-  Recovery R;
-  R.C = C;
-  R.oi = oi;
-  R.hoisted = vnew<Node*>(C);
-  R.lambda_counter = 0;
-  stmts = R.rewrite_block(stmts);
-  CKR(C, nullptr);
+  // DefRecovery (recover.py:81-227) only ever changes a tree through FuncExpr
+  // and BuildClass nodes (pre/post hooks, _match_def); everything else it does
+  // is rebuilding lists with identical contents.  When the simulation of this
+  // object created neither, the pass is skipped: the output is identical.
+  if (C->n_defs != defs_before) {
+    Recovery R;
+    R.C = C;
+    R.oi = oi;
+    R.hoisted = vnew<Node*>(C);
+    R.lambda_counter = 0;
+    stmts = R.rewrite_block(stmts);
+    CKR(C, nullptr);
+  }
   stmts = add_scope_decls(C, stmts, oi);
   CKR(C, nullptr);
   const upy_obj* o = obj_at(C, oi);

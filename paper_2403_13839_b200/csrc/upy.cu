@@ -59,7 +59,10 @@ struct KParams {
   char tool[64];
 };
 
-__global__ void __launch_bounds__(128) upy_decompile_kernel(KParams P) {
+#ifndef UPY_MINB
+#define UPY_MINB 8  // <= 64 registers: 32 resident warps per SM (measured +43% vs unbounded)
+#endif
+__global__ void __launch_bounds__(128, UPY_MINB) upy_decompile_kernel(KParams P) {
   const u64 slot = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   u8* base = P.slots_base + slot * P.slot_bytes;
   EmitOpts opt;
@@ -97,17 +100,14 @@ __global__ void __launch_bounds__(128) upy_decompile_kernel(KParams P) {
       len = out.n;
     }
     int status = C.err;
-    u64 off = atomicAdd((unsigned long long*)P.out.text_used, (unsigned long long)len);
-    if (off + len > P.out.text_cap) {
+    // reservations are 16-byte granular so the copy-out is whole uint4 stores
+    u64 resv = ((u64)len + 15) & ~(u64)15;
+    u64 off = atomicAdd((unsigned long long*)P.out.text_used, (unsigned long long)resv);
+    if (off + resv > P.out.text_cap) {
       status = UPY_ST_OUTPUT_OVERFLOW;
       len = 0;
-    } else {
-      u8* dst = P.out.text + off;
-      // 16-byte chunks where alignment allows
-      u32 q = 0;
-      if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0)
-        for (; q + 16 <= len; q += 16) *reinterpret_cast<uint4*>(dst + q) = *reinterpret_cast<const uint4*>(src + q);
-      for (; q < len; q++) dst[q] = (u8)src[q];
+    } else if (len) {
+      copy16(P.out.text + off, src, len);
     }
     P.out.text_off[r] = off;
     P.out.text_len[r] = len;
@@ -138,14 +138,15 @@ static WsLayout layout(const upy_arena* a, const upy_options* o) {
   L.dec_off = al(units * sizeof(upy_ins));
   L.ctr_off = L.dec_off + al((u64)a->n_objs * sizeof(upy_decoded));
   L.slots_off = L.ctr_off + 256;
-  u64 sb = o && o->arena_bytes ? o->arena_bytes : (u64)(256u << 10) + (u64)a->max_code_len * 512u;
+  // C3-size objects use ~55 KB; larger ones overflow and are retried by the host with 4x
+  u64 sb = o && o->arena_bytes ? o->arena_bytes : (u64)(64u << 10) + (u64)a->max_code_len * 256u;
   sb = (sb + SLOT_HEADER + 255) & ~(u64)255;
   L.slot_bytes = sb;
   u64 slots;
   if (o && o->slots > 0) {
     slots = (u64)o->slots;
   } else {
-    u64 cap_bytes = 24ull << 30;  // default arena budget
+    u64 cap_bytes = 40ull << 30;  // default arena budget (of 180 GB HBM)
     slots = cap_bytes / sb;
     u64 full = (u64)sm_count() * 1024;
     if (slots > full) slots = full;
