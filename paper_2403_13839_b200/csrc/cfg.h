@@ -70,7 +70,7 @@ HD inline i32 index_of(Dc* C, const Code* K, u32 off) {
 // ------------------------------------------------------------ instructions
 // Materialize the object's instruction list from the decode kernel's records
 // and surface the decode status (decode_instructions, disasm.py:71-172).
-HD inline bool load_instructions(Dc* C, Code* K, u32 oi) {
+HD NOINL bool load_instructions(Dc* C, Code* K, u32 oi) {
   K->oi = oi;
   K->o = obj_at(C, oi);
   K->minor = (int)K->o->minor;
@@ -133,7 +133,7 @@ HD inline bool load_instructions(Dc* C, Code* K, u32 oi) {
 }
 
 // rewrite_yield_from (pipeline.py:57-87)
-HD inline void rewrite_yield_from(Dc* C, Code* K) {
+HD NOINL void rewrite_yield_from(Dc* C, Code* K) {
   bool any = false;
   for (i32 i = 0; i < K->n_ins; i++)
     if (K->ins[i].op == OP_SEND) any = true;
@@ -173,7 +173,7 @@ HD inline void rewrite_yield_from(Dc* C, Code* K) {
 }
 
 // decode_exception_table (disasm.py:175-214)
-HD inline Vec<ExcEntry>* decode_exception_table(Dc* C, const Code* K) {
+HD NOINL Vec<ExcEntry>* decode_exception_table(Dc* C, const Code* K) {
   Vec<ExcEntry>* v = vnew<ExcEntry>(C);
   const u8* data = C->A->bytes + K->o->exc_off;
   u32 len = K->o->exc_len, pos = 0;
@@ -246,7 +246,7 @@ HD inline bool is_as_cleanup(const Code* K, i32 idx) {  // structurer.py:154-160
   return (I[0].op == OP_LOAD_CONST && I[1].op == OP_STORE_FAST && I[2].op == OP_DELETE_FAST) ||
          (I[0].op == OP_LOAD_CONST && I[1].op == OP_STORE_NAME && I[2].op == OP_DELETE_NAME);
 }
-HD inline Vec<TryRegion>* match_try_regions(Dc* C, const Code* K, const Vec<ExcEntry>* exc) {
+HD NOINL Vec<TryRegion>* match_try_regions(Dc* C, const Code* K, const Vec<ExcEntry>* exc) {
   Vec<TryRegion>* out = vnew<TryRegion>(C);
   const Ins* I = K->ins;
   if (K->minor <= 10) {  // _regions_legacy (structurer.py:69-88)
@@ -358,7 +358,7 @@ HD inline void sort_u32(u32* a, i32 n) {  // heap sort (no recursion, no std)
 }
 
 // build_basic_blocks (cfg.py:72-141)
-HD inline Cfg* build_basic_blocks(Dc* C, const Code* K, const Vec<ExcEntry>* entries) {
+HD NOINL Cfg* build_basic_blocks(Dc* C, const Code* K, const Vec<ExcEntry>* entries) {
   Cfg* G = anew<Cfg>(C);
   CKR(C, G);
   const Ins* I = K->ins;
@@ -501,7 +501,7 @@ HD inline bool has_normal_edge(const Block& P, i32 to) {
 }
 
 // compute_dominators (cfg.py:160-220); idom[b] = -1 when b has no entry
-HD inline i32* compute_dominators(Dc* C, const Cfg* G, i32 root, const u8* universe) {
+HD NOINL i32* compute_dominators(Dc* C, const Cfg* G, i32 root, const u8* universe) {
   i32 nb = G->n_blocks;
   i32* idom = (i32*)zalloc(C, (u64)nb * sizeof(i32));
   i32* rpo_index = (i32*)zalloc(C, (u64)nb * sizeof(i32));
@@ -586,7 +586,7 @@ HD inline bool dominates(const i32* idom, i32 a, i32 b) {  // cfg.py:223-231
 
 // analyze_loops (cfg.py:241-313); appends loops whose header is new to G->loops.
 // Returns false when irreducible.
-HD inline bool analyze_loops(Dc* C, Cfg* G, const i32* idom, const u8* universe) {
+HD NOINL bool analyze_loops(Dc* C, Cfg* G, const i32* idom, const u8* universe) {
   i32 nb = G->n_blocks;
   // roots: universe blocks with no predecessor in the universe (any edge kind)
   i32 root = -1;
@@ -695,7 +695,7 @@ HD inline bool analyze_loops(Dc* C, Cfg* G, const i32* idom, const u8* universe)
 }
 
 // analyze (pipeline.py:17-54)
-HD inline Cfg* analyze(Dc* C, Code* K) {
+HD NOINL Cfg* analyze(Dc* C, Code* K) {
   Vec<ExcEntry>* entries = vnew<ExcEntry>(C);
   if (K->minor >= 11) {
     rewrite_yield_from(C, K);

@@ -16,9 +16,11 @@
 #ifdef __CUDACC__
 #define HD __host__ __device__
 #define DI __device__ __forceinline__
+#define NOINL __noinline__
 #else
 #define HD
 #define DI inline
+#define NOINL __attribute__((noinline))
 #endif
 
 typedef uint8_t u8;

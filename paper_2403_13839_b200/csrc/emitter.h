@@ -111,7 +111,7 @@ struct Emitter {
     t_float_repr(C, t, im);
     t_put(C, t, 'j');
   }
-  HD void render_constant(Text* t, u32 cid) {  // emitter.py:53-80
+  HD NOINL void render_constant(Text* t, u32 cid) {  // emitter.py:53-80
     GUARD(C);
     CK(C);
     if (cid == CID_INVALID) {
@@ -273,7 +273,7 @@ HD inline void Emitter::r_const_value(Text* t, u32 cid) {
   t_puts(C, t, "None");
 }
 
-HD inline void Emitter::r_node(Text* t, const Node* n) {
+HD NOINL void Emitter::r_node(Text* t, const Node* n) {
   GUARD(C);
   CK(C);
   if (!n) {
@@ -514,7 +514,7 @@ HD inline int Emitter::prec_of(const Node* e, bool* ok) {
   return 0;
 }
 
-HD inline void Emitter::expr(Text* t, Node* e, int parent, bool right_side) {
+HD NOINL void Emitter::expr(Text* t, Node* e, int parent, bool right_side) {
   GUARD(C);
   CK(C);
   bool ok;
@@ -544,7 +544,7 @@ HD inline void Emitter::expr(Text* t, Node* e, int parent, bool right_side) {
   if (paren) t_put(C, t, ')');
 }
 
-HD inline void Emitter::expr_body(Text* t, Node* e) {
+HD NOINL void Emitter::expr_body(Text* t, Node* e) {
   switch (e->k) {
     case E_CONST: render_constant(t, e->cid); return;
     case E_NAME: name_text(t, e->s); return;
@@ -809,7 +809,7 @@ HD inline void Emitter::expr_body(Text* t, Node* e) {
   }
 }
 
-HD inline void Emitter::format_part(Text* t, Node* fv) {  // emitter.py:510-519
+HD NOINL void Emitter::format_part(Text* t, Node* fv) {  // emitter.py:510-519
   if (!is_k(fv, E_FMTVAL)) {
     // not a FormattedValue: the reference calls _format_part on it anyway
     py_error(C, UPY_ST_PY_ATTRIBUTE_ERROR, "object has no attribute 'value'");
@@ -913,7 +913,7 @@ HD inline void Emitter::target(Text* t, Node* e, bool nested) {  // emitter.py:3
   expr(t, e);
 }
 
-HD inline void Emitter::params(Text* t, Node* p) {  // emitter.py:285-308
+HD NOINL void Emitter::params(Text* t, Node* p) {  // emitter.py:285-308
   bool first = true;
   auto sep = [&]() {
     if (!first) t_puts(C, t, ", ");
@@ -960,7 +960,7 @@ HD inline void Emitter::params(Text* t, Node* p) {  // emitter.py:285-308
 }
 
 // ------------------------------------------------------------ statements
-HD inline void Emitter::emit_if(Node* s, const char* kw) {
+HD NOINL void Emitter::emit_if(Node* s, const char* kw) {
   line_start();
   t_puts(C, out, kw);
   t_put(C, out, ' ');
@@ -977,7 +977,7 @@ HD inline void Emitter::emit_if(Node* s, const char* kw) {
   block(s->l2);
 }
 
-HD inline void Emitter::stmt(Node* s) {  // emitter.py:136-283
+HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
   GUARD(C);
   CK(C);
   switch (s ? s->k : 0) {

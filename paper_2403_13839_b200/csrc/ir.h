@@ -247,7 +247,7 @@ HD inline bool kwdict_eq(Dc* C, const NV* a, const NV* b) {
   return ua == ub;
 }
 
-HD inline bool node_eq(Dc* C, const Node* x, const Node* y) {
+HD NOINL bool node_eq(Dc* C, const Node* x, const Node* y) {
   if (x == y) return true;
   if (!x || !y) return false;
   if (x->k != y->k) return false;

@@ -120,7 +120,7 @@ HD inline u64 dbits(double d) {
   return u;
 }
 
-HD inline bool const_key_eq(Dc* C, u32 a, u32 b) {
+HD NOINL bool const_key_eq(Dc* C, u32 a, u32 b) {
   GUARD(C);
   CKR(C, false);
   if (a == b) return true;
@@ -178,7 +178,7 @@ HD inline bool strtab_eq(Dc* C, u32 offa, u32 na, u32 offb, u32 nb) {
 }
 
 // CodeObject._key() (code_model.py:147-164): excludes filename/linetable/exctable/qualname
-HD inline bool code_key_eq(Dc* C, u32 ia, u32 ib) {
+HD NOINL bool code_key_eq(Dc* C, u32 ia, u32 ib) {
   if (ia == ib) return true;
   const upy_obj* a = obj_at(C, ia);
   const upy_obj* b = obj_at(C, ib);

@@ -86,7 +86,7 @@ HD inline void bn_pow10(Big* a, u32 k) {
 // Shortest round-trip digits (Burger & Dybvig free-format, with closest-digit
 // fix-up), matching CPython's dtoa mode 0.  digits[] gets ASCII, returns count;
 // *decpt = position of the decimal point (value = 0.DIGITS * 10^decpt).
-HD inline int shortest_digits(double v, char* digits, int* decpt) {
+HD NOINL int shortest_digits(double v, char* digits, int* decpt) {
   u64 bits;
   memcpy(&bits, &v, 8);
   u64 frac = bits & ((1ull << 52) - 1);
@@ -302,7 +302,7 @@ HD inline void t_complex_repr(Dc* C, Text* t, double re, double im) {
 
 // ------------------------------------------------------------ int repr
 // repr of a sign/magnitude bigint from the arena (ValueError above 4300 digits)
-HD inline bool t_int_repr(Dc* C, Text* t, int sign, const u32* limbs, u32 n) {
+HD NOINL bool t_int_repr(Dc* C, Text* t, int sign, const u32* limbs, u32 n) {
   while (n > 0 && limbs[n - 1] == 0) n--;
   if (n == 0) {
     t_put(C, t, '0');
@@ -400,7 +400,7 @@ HD inline void t_hex(Dc* C, Text* t, u32 v, int width) {
   const char* hx = "0123456789abcdef";
   for (int q = width - 1; q >= 0; q--) t_put(C, t, hx[(v >> (4 * q)) & 0xF]);
 }
-HD inline void t_str_repr(Dc* C, Text* t, Str s) {  // unicode_repr (CPython 3.12)
+HD NOINL void t_str_repr(Dc* C, Text* t, Str s) {  // unicode_repr (CPython 3.12)
   bool sq = false, dq = false;
   for (u32 i = 0; i < s.n; i++) {
     if (s.p[i] == '\'') sq = true;

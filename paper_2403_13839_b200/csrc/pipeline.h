@@ -28,7 +28,7 @@ struct Validator {
     add_begin(where);
     t_puts(C, &rep, msg);
   }
-  HD void one(u32 oi, Str path) {
+  HD NOINL void one(u32 oi, Str path) {
     GUARD(C);
     CK(C);
     const upy_obj* o = obj_at(C, oi);
@@ -116,7 +116,7 @@ struct Validator {
 };
 
 // function_tree / module_tree (pipeline.py:121-140)
-HD inline NV* root_tree(Dc* C, u32 oi) {
+HD NOINL NV* root_tree(Dc* C, u32 oi) {
   NV* body = decompile_body(C, oi);
   CKR(C, nullptr);
   if (s_eqc(obj_name(C, oi), "<module>")) {
@@ -144,7 +144,7 @@ HD inline NV* root_tree(Dc* C, u32 oi) {
 }
 
 // decompile_source (pipeline.py:143-160) + emit_module (emitter.py:535-547)
-HD inline void decompile_source(Dc* C, u32 oi, const EmitOpts* opt, Text* out) {
+HD NOINL void decompile_source(Dc* C, u32 oi, const EmitOpts* opt, Text* out) {
   Validator V;
   V.C = C;
   V.rep = {nullptr, 0, 0};

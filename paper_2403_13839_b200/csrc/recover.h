@@ -102,7 +102,7 @@ HD inline NV* Recovery::map_list(NV* v) {
 }
 
 // map_expr (recover.py:25-50): pre may replace a subtree, fields in dataclass order, post last
-HD inline Node* Recovery::map_expr(Node* e) {
+HD NOINL Node* Recovery::map_expr(Node* e) {
   if (!is_expr(e)) return e;
   GUARD(C);
   CKR(C, e);
@@ -192,7 +192,7 @@ HD inline Node* Recovery::hoist(Node* fe) {  // recover.py:221-227
   vpush(C, hoisted, d);
   return mk_name(C, name, SC_FAST);
 }
-HD inline Node* Recovery::make_funcdef(Str name, Node* fe) {  // recover.py:150-159
+HD NOINL Node* Recovery::make_funcdef(Str name, Node* fe) {  // recover.py:150-159
   GUARD(C);
   CKR(C, nullptr);
   if (fe->cid == CID_INVALID) {
@@ -242,7 +242,7 @@ HD inline NV* clean_class_body(Dc* C, NV* body) {
   return out;
 }
 
-HD inline Node* Recovery::make_classdef(Str name, Node* call) {  // recover.py:161-172
+HD NOINL Node* Recovery::make_classdef(Str name, Node* call) {  // recover.py:161-172
   NV* args = call->l1;
   if (args->n < 2 || !is_k(args->d[0], E_FUNC)) return nullptr;
   u32 cls_code = args->d[0]->cid;
@@ -330,7 +330,7 @@ HD inline bool match_comp_body(Dc* C, NV* body, Node** accum, NV** gens_out) {
   return false;
 }
 
-HD inline Node* Recovery::make_comp(int kind, u32 code, Node* iter_arg) {  // recover.py:206-219
+HD NOINL Node* Recovery::make_comp(int kind, u32 code, Node* iter_arg) {  // recover.py:206-219
   NV* body = decompile_body(C, code);
   CKR(C, nullptr);
   Node* accum = nullptr;
@@ -350,7 +350,7 @@ HD inline Node* Recovery::make_comp(int kind, u32 code, Node* iter_arg) {  // re
   return c;
 }
 
-HD inline Node* Recovery::match_def(Node* target, Node* value) {  // recover.py:123-148
+HD NOINL Node* Recovery::match_def(Node* target, Node* value) {  // recover.py:123-148
   NV* decorators = vnew<Node*>(C);
   Node* inner = value;
   while (is_k(inner, E_CALL) && inner->l1->n == 1 && inner->l2->n == 0 && !is_k(inner->a, E_BUILDCLASS)) {
@@ -384,7 +384,7 @@ HD inline Node* Recovery::match_def(Node* target, Node* value) {  // recover.py:
 }
 
 // _stmt_exprs (recover.py:63-78), dataclass field order per statement kind
-HD inline void Recovery::stmt_exprs(Node* s) {
+HD NOINL void Recovery::stmt_exprs(Node* s) {
   auto mx = [&](Node** f) {
     if (is_expr(*f)) *f = map_expr(*f);
   };
@@ -438,7 +438,7 @@ HD inline void Recovery::stmt_exprs(Node* s) {
   }
 }
 
-HD inline NV* Recovery::rewrite_stmt(Node* s) {  // recover.py:99-121
+HD NOINL NV* Recovery::rewrite_stmt(Node* s) {  // recover.py:99-121
   GUARD(C);
   CKR(C, nullptr);
   if (is_k(s, S_ASSIGN) && s->l1->n == 1 && is_k(s->l1->d[0], E_NAME)) {
@@ -526,7 +526,7 @@ struct ScopeScan {
     }
   }
 };
-HD inline NV* add_scope_decls(Dc* C, NV* body, u32 oi) {
+HD NOINL NV* add_scope_decls(Dc* C, NV* body, u32 oi) {
   ScopeScan sc;
   sc.C = C;
   sc.o = obj_at(C, oi);
@@ -558,7 +558,7 @@ HD inline bool is_return_none(Dc* C, Node* s) {  // pipeline.py:113-118
 }
 
 // decompile_body (pipeline.py:90-110)
-HD inline NV* decompile_body(Dc* C, u32 oi) {
+HD NOINL NV* decompile_body(Dc* C, u32 oi) {
   GUARD(C);
   CKR(C, nullptr);
   Code* K = anew<Code>(C);

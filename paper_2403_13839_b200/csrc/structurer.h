@@ -120,7 +120,7 @@ HD inline NV* strip_as_cleanup(Dc* C, NV* body, Str name) {  // structurer.py:10
 }
 
 // strip_finally_copies (structurer.py:1089-1112)
-HD inline NV* strip_finally_copies(Dc* C, NV* stmts, NV* final) {
+HD NOINL NV* strip_finally_copies(Dc* C, NV* stmts, NV* final) {
   GUARD(C);
   CKR(C, stmts);
   if (!final->n) return stmts;
@@ -187,7 +187,7 @@ HD inline Node* while_guard_merge(Dc* C, Node* cond, Node* shape) {
   }
   return nullptr;
 }
-HD inline Node* canon_one(Dc* C, Node* s) {  // structurer.py:1166-1197
+HD NOINL Node* canon_one(Dc* C, Node* s) {  // structurer.py:1166-1197
   GUARD(C);
   CKR(C, s);
   if (is_k(s, S_IF) && s->l1->n == 1 && is_k(s->l1->d[0], S_WHILESHAPE) && s->l2->n == 0) {
@@ -343,7 +343,7 @@ struct Structurer {
 #define NO_POS ((i64)-0x7FFFFFFFFFFFFFFFll)
 
 // walk (structurer.py:226-278)
-HD inline NV* Structurer::walk(Segs segs, NV* stack, const WCtx* ctx, WalkExit* ex) {
+HD NOINL NV* Structurer::walk(Segs segs, NV* stack, const WCtx* ctx, WalkExit* ex) {
   GUARD(C);
   NV* out = vnew<Node*>(C);
   *ex = wx(WX_ENDED);
@@ -411,7 +411,7 @@ HD inline NV* Structurer::walk(Segs segs, NV* stack, const WCtx* ctx, WalkExit* 
 }
 
 // _consume_block (structurer.py:280-310)
-HD inline WalkExit Structurer::consume_block(const Block* b, BlockResult& res, NV* out, NV* stack,
+HD NOINL WalkExit Structurer::consume_block(const Block* b, BlockResult& res, NV* out, NV* stack,
                                              const WCtx* ctx) {
   if (res.term < 0) {
     vextend(C, out, res.stmts);
@@ -453,7 +453,7 @@ HD inline WalkExit Structurer::resolve_jump(i64 target, NV* stack, NV* out, cons
 }
 
 // ------------------------------------------------------------ loops
-HD inline i64 Structurer::structure_loop(i32 li, const Block* header, NV* out, NV** stack, const WCtx* ctx) {
+HD NOINL i64 Structurer::structure_loop(i32 li, const Block* header, NV* out, NV** stack, const WCtx* ctx) {
   GUARD(C);
   CKR(C, NO_POS);
   const Loop& L = G->loops->d[li];
@@ -504,7 +504,7 @@ HD inline i64 Structurer::structure_loop(i32 li, const Block* header, NV* out, N
   return C->err ? NO_POS : r;
 }
 
-HD inline i64 Structurer::structure_for(i32 li, const Block* header, BlockResult& hres, NV* out, NV** stack,
+HD NOINL i64 Structurer::structure_for(i32 li, const Block* header, BlockResult& hres, NV* out, NV** stack,
                                         const WCtx* ctx) {
   const Ins& term = K->ins[hres.term];
   i64 after = jump_target(K, term);
@@ -559,7 +559,7 @@ HD inline bool is_pop_jump(u8 op) {
   return false;
 }
 
-HD inline i64 Structurer::structure_while_true(i32 li, const Block* header, NV* out, NV** stack,
+HD NOINL i64 Structurer::structure_while_true(i32 li, const Block* header, NV* out, NV** stack,
                                                const WCtx* ctx, i64 lo, i64 hi) {
   const Loop& L = G->loops->d[li];
   i64 lx = lexical_exit_max(lo, hi);
@@ -643,7 +643,7 @@ HD inline bool is_assertion_raise(const Node* s) {  // structurer.py:1031-1037
   return false;
 }
 
-HD inline WalkExit Structurer::structure_conditional(const Block* block, Node* marker, BlockResult& res,
+HD NOINL WalkExit Structurer::structure_conditional(const Block* block, Node* marker, BlockResult& res,
                                                      NV* out, NV* stack, const WCtx* ctx) {
   GUARD(C);
   CKR(C, wx(WX_ENDED));
@@ -795,7 +795,7 @@ HD inline WalkExit Structurer::structure_conditional(const Block* block, Node* m
 }
 
 // _collect_chain (structurer.py:619-655)
-HD inline void Structurer::collect_chain(Node** fall_cond, i64* target, i64* fall_pos, NV** fall_state) {
+HD NOINL void Structurer::collect_chain(Node** fall_cond, i64* target, i64* fall_pos, NV** fall_state) {
   while (!C->err) {
     i32 nb = *fall_pos >= 0 && *fall_pos <= 0xFFFFFFFFll ? block_at(G, (u32)*fall_pos) : -1;
     if (nb < 0) break;
@@ -822,7 +822,7 @@ HD inline void Structurer::collect_chain(Node** fall_cond, i64* target, i64* fal
 }
 
 // _structure_orpop (structurer.py:657-719)
-HD inline WalkExit Structurer::structure_orpop(const Block* block, Node* marker, BlockResult& res, NV* out,
+HD NOINL WalkExit Structurer::structure_orpop(const Block* block, Node* marker, BlockResult& res, NV* out,
                                                NV* stack, const WCtx* ctx) {
   u8 op = (marker->f & 1) ? 1 : 0;  // or : and
   i64 join = marker->i;
@@ -885,7 +885,7 @@ HD inline bool Structurer::is_chain_fixup(i64 off, bool returning) {  // structu
 }
 
 // ------------------------------------------------------------ regions
-HD inline i64 Structurer::structure_region(i32 r, NV* out, NV** stack, const WCtx* ctx) {
+HD NOINL i64 Structurer::structure_region(i32 r, NV* out, NV** stack, const WCtx* ctx) {
   GUARD(C);
   CKR(C, NO_POS);
   vpush(C, active_regions, r);
@@ -916,7 +916,7 @@ HD inline NV* Structurer::exc_entry_stack(NV* stack) {
   return st;
 }
 
-HD inline i64 Structurer::structure_with(const TryRegion& R, NV* out, NV** stack, const WCtx* ctx) {
+HD NOINL i64 Structurer::structure_with(const TryRegion& R, NV* out, NV** stack, const WCtx* ctx) {
   NV* st = *stack;
   Node* ctx_expr = nullptr;
   bool found = false;
@@ -988,7 +988,7 @@ HD inline i64 Structurer::after_handler_code(const TryRegion& R) {  // structure
   return end_offset;
 }
 
-HD inline i64 Structurer::structure_finally(const TryRegion& R, NV* out, NV** stack, const WCtx* ctx) {
+HD NOINL i64 Structurer::structure_finally(const TryRegion& R, NV* out, NV** stack, const WCtx* ctx) {
   if (K->minor == 8) return structure_finally_38(R, out, stack, ctx);
   WalkExit fx;
   NV* final = walk(seg1(R.handler, end_offset), exc_entry_stack(vnew<Node*>(C)), ctx_no_joins(ctx), &fx);
@@ -1022,7 +1022,7 @@ HD inline i64 Structurer::structure_finally(const TryRegion& R, NV* out, NV** st
   return after_handler_code(R);
 }
 
-HD inline i64 Structurer::structure_finally_38(const TryRegion& R, NV* out, NV** stack, const WCtx* ctx) {
+HD NOINL i64 Structurer::structure_finally_38(const TryRegion& R, NV* out, NV** stack, const WCtx* ctx) {
   NV* sent = nv_copy(C, *stack);
   vpush(C, sent, mk(C, E_FINSENT));
   WalkExit fx;
@@ -1052,7 +1052,7 @@ HD inline i64 Structurer::structure_finally_38(const TryRegion& R, NV* out, NV**
   return idx < K->n_ins ? (i64)ins_end(K->ins[idx]) : (i64)end_offset;
 }
 
-HD inline i64 Structurer::structure_except(const TryRegion& R, NV* out, NV** stack, const WCtx* ctx) {
+HD NOINL i64 Structurer::structure_except(const TryRegion& R, NV* out, NV** stack, const WCtx* ctx) {
   const WCtx* bctx = ctx_with_join(ctx, R.handler);
   WalkExit bx;
   NV* body = walk(seg1(R.start, R.end), *stack, bctx, &bx);
@@ -1090,7 +1090,7 @@ HD inline i64 Structurer::structure_except(const TryRegion& R, NV* out, NV** sta
   return join;
 }
 
-HD inline NV* Structurer::parse_handlers(const TryRegion& R, const WCtx* ctx, i64* join_out) {
+HD NOINL NV* Structurer::parse_handlers(const TryRegion& R, const WCtx* ctx, i64* join_out) {
   NV* handlers = vnew<Node*>(C);
   i64 best = -1;
   bool any = false;
@@ -1144,7 +1144,7 @@ HD inline NV* Structurer::parse_handlers(const TryRegion& R, const WCtx* ctx, i6
   return handlers;
 }
 
-HD inline NV* Structurer::walk_arm(i64 arm_start, NV* arm_stack, const WCtx* ctx, i64 limit, Str* name,
+HD NOINL NV* Structurer::walk_arm(i64 arm_start, NV* arm_stack, const WCtx* ctx, i64 limit, Str* name,
                                    i64* join) {
   i64 end = limit >= 0 ? limit : (i64)end_offset;
   WalkExit ex;
@@ -1166,7 +1166,7 @@ HD inline NV* Structurer::walk_arm(i64 arm_start, NV* arm_stack, const WCtx* ctx
   return body;
 }
 
-HD inline Structurer* make_structurer(Dc* C, Code* K, Cfg* G) {
+HD NOINL Structurer* make_structurer(Dc* C, Code* K, Cfg* G) {
   Structurer* S_ = anew<Structurer>(C);
   CKR(C, S_);
   S_->C = C;

@@ -279,7 +279,7 @@ struct Sim {
   }
 
   // _store (symexec.py:295-399); returns the number of following stores consumed
-  HD int store(const Ins* ins, NV* st, NV* out, i32 idx, i32 hi, Node* target) {
+  HD NOINL int store(const Ins* ins, NV* st, NV* out, i32 idx, i32 hi, Node* target) {
     Node* v = pop(st, ins);
     CKR(C, 0);
     if (is_k(v, E_UNPACKSLOT)) {
@@ -510,7 +510,7 @@ struct Sim {
 
 #define BR_PUSH(x) push(st, (x))
 
-HD inline int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out) {
+HD NOINL int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out) {
   const Ins& in = *ins;
   switch (in.op) {
     // ------------------------------------------------ loads (symexec.py:239-268)
@@ -1360,7 +1360,7 @@ HD inline Node* mk_condjump(Dc* C, Node* cond, bool jump_when, u32 target, bool 
 }
 
 // simulate_block (symexec.py:138-210)
-HD inline BlockResult Sim::simulate(const Block* b, const NV* entry) {
+HD NOINL BlockResult Sim::simulate(const Block* b, const NV* entry) {
   BlockResult R = {nullptr, nullptr, nullptr, -1};
   NV* st = nv_copy(C, entry);
   NV* out = vnew<Node*>(C);

@@ -69,11 +69,15 @@ __global__ void __launch_bounds__(128, UPY_MINB) upy_decompile_kernel(KParams P)
   opt.header = P.header != 0;
   opt.indent = Str{P.indent, (u32)P.indent_len};
   opt.tool = Str{P.tool, (u32)P.tool_len};
+  // The per-thread context (arena cursor, sticky status, depth guard) is read
+  // after nearly every call; keeping it in shared memory instead of the local
+  // stack takes those accesses off the L1/L2/DRAM path.
+  __shared__ Dc dcs[128];
+  Dc& C = dcs[threadIdx.x];
   while (true) {
     u32 r = atomicAdd(P.next_root, 1u);
     if (r >= (u64)P.A.n_roots) break;
     u32 oi = (u32)P.A.roots[r];
-    Dc C;
     C.msg = (char*)base;
     C.msg_len = 0;
     C.msg_cap = MSG_BYTES;
@@ -88,6 +92,7 @@ __global__ void __launch_bounds__(128, UPY_MINB) upy_decompile_kernel(KParams P)
     C.dec_all = P.dec;
     C.depth = 0;
     C.max_depth = P.max_depth;
+    C.n_defs = 0;
     Text out = {nullptr, 0, 0};
     decompile_source(&C, oi, &opt, &out);
     const char* src;
@@ -153,7 +158,7 @@ static WsLayout layout(const upy_arena* a, const upy_options* o) {
   }
   if (slots > (u64)a->n_roots) slots = (u64)a->n_roots;
   if (slots < 1) slots = 1;
-  int tpb = o && o->threads_per_block > 0 ? o->threads_per_block : 128;
+  int tpb = o && o->threads_per_block > 0 && o->threads_per_block < 128 ? o->threads_per_block : 128;
   slots = (slots + tpb - 1) / tpb * tpb;
   L.slots = slots;
   L.total = L.slots_off + slots * sb;
@@ -264,7 +269,7 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
     P.tool_len = 6;
     memcpy(P.tool, "unpyre", 6);
   }
-  int tpb = opt && opt->threads_per_block > 0 ? opt->threads_per_block : 128;
+  int tpb = opt && opt->threads_per_block > 0 && opt->threads_per_block < 128 ? opt->threads_per_block : 128;
   unsigned blocks = (unsigned)(L.slots / tpb);
   upy_decompile_kernel<<<blocks, tpb, 0, s>>>(P);
   cudaError_t e = cudaGetLastError();
