@@ -33,15 +33,29 @@ def _deps():
     return out
 
 
-def up_to_date(target, deps):
-    if not os.path.exists(target):
+def _digest(deps, flags):
+    import hashlib
+
+    h = hashlib.sha256(" ".join(flags).encode())
+    for d in deps:
+        with open(d, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()
+
+
+def up_to_date(target, deps, flags=()):
+    """Content-addressed: a stamp next to the library records the digest of
+    the sources and flags it was built from (mtimes do not survive copies)."""
+    stamp = target + ".stamp"
+    if not os.path.exists(target) or not os.path.exists(stamp):
         return False
-    t = os.path.getmtime(target)
-    return all(os.path.getmtime(d) <= t for d in deps)
+    with open(stamp) as f:
+        return f.read().strip() == _digest(deps, flags)
 
 
 def build_cuda(force=False, verbose=True):
-    if not force and up_to_date(LIB, _deps()):
+    deps = _deps()
+    if not force and up_to_date(LIB, deps, NVCC_FLAGS):
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     cmd = [nvcc, *NVCC_FLAGS, "-o", LIB + ".tmp", os.path.join(CSRC, "upy.cu")]
@@ -49,6 +63,8 @@ def build_cuda(force=False, verbose=True):
         print("[build]", " ".join(cmd), flush=True)
     subprocess.check_call(cmd)
     os.replace(LIB + ".tmp", LIB)
+    with open(LIB + ".stamp", "w") as f:
+        f.write(_digest(deps, NVCC_FLAGS))
     return LIB
 
 

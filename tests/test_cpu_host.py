@@ -1,0 +1,113 @@
+"""CPU tier: packer round trips, ABI surface of the built libraries, sharding
+logic under a 2-process gloo group."""
+import ctypes
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from paper_2403_13839_b200 import _abi, arena, shard
+from paper_2403_13839_b200.model import CodeObject, Const, VersionTag
+from paper_2403_13839_b200.synth import corpus, snippets
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _all_objects():
+    objs = corpus.fig1(10) + corpus.fig1(11) + [corpus.c3(3), corpus.c4(1, 10, 600)]
+    objs += [fn(m) for fn in snippets.SNIPPETS.values() for m in fn.minors]
+    return objs
+
+
+def test_pack_unpack_roundtrip():
+    objs = _all_objects()
+    back = arena.unpack(arena.pack(objs))
+    assert len(back) == len(objs)
+    for a, b in zip(objs, back):
+        assert a._key() == b._key()
+        assert a.filename == b.filename and a.qualname == b.qualname and a.exceptiontable == b.exceptiontable
+
+
+def test_pack_layout_alignment():
+    a = arena.pack(_all_objects())
+    objs = a.section("objs")
+    assert all(int(o) % 16 == 0 for o in objs["code_off"])
+    for s in arena.SECTIONS:
+        assert a.offsets[s] % 256 == 0
+
+
+def test_tile_shares_pools_and_copies_code():
+    a = arena.pack([corpus.c3(i) for i in range(5)])
+    t = arena.tile(a, 3)
+    assert t.n_roots == 15 and t.code_bytes == 3 * a.code_bytes
+    back = arena.unpack(t)
+    for k in range(3):
+        for i in range(5):
+            assert back[5 * k + i]._key() == back[i]._key()
+
+
+def test_bigint_and_float_consts_roundtrip():
+    c = Const("tuple", (Const("int", -(2 ** 200) + 7), Const("float", -0.0), Const("complex", complex(1, -2)),
+                        Const("str", "\udc80x"), Const("bytes", b"\x00\xff"), Const("frozenset", (Const("int", 0),))))
+    co = CodeObject(VersionTag(3, 10), 0, 0, 0, 0, 1, 0, b"d\x00S\x00", (c,), (), (), (), (), "f", "<s>", 1)
+    back = arena.unpack(arena.pack([co]))[0]
+    assert back.consts[0] == c
+
+
+def _lib_path(name):
+    return os.path.join(ROOT, "paper_2403_13839_b200", name)
+
+
+@pytest.mark.skipif(not os.path.exists(_lib_path("libupy_cuda.so")), reason="CUDA library not built")
+def test_cuda_library_exports_every_declared_symbol():
+    import re
+
+    lib = ctypes.CDLL(_lib_path("libupy_cuda.so"))
+    with open(os.path.join(ROOT, "include", "upy.h")) as f:
+        declared = set(re.findall(r"\b(upy_[a-z_]+)\s*\(", f.read()))
+    assert declared == set(_abi.EXPORTS)
+    for sym in declared:
+        assert hasattr(lib, sym), sym
+    _abi.check_layout(lib)
+    lib.upy_abi_version.restype = ctypes.c_int
+    assert lib.upy_abi_version() == 1
+
+
+def test_shard_bounds_partition_and_balance():
+    w = np.random.default_rng(0).integers(1, 1000, size=1001)
+    for world in (1, 2, 3, 8):
+        b = shard.shard_bounds(w, world)
+        assert b[0][0] == 0 and b[-1][1] == len(w)
+        assert all(b[i][1] == b[i + 1][0] for i in range(world - 1))
+        loads = [w[lo:hi].sum() for lo, hi in b]
+        assert max(loads) - min(loads) <= 2 * w.max()
+
+
+GLOO_WORKER = r"""
+import os, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch, torch.distributed as dist
+from paper_2403_13839_b200 import shard
+dist.init_process_group("gloo")
+r, w = dist.get_rank(), dist.get_world_size()
+weights = np.arange(1, 101)
+lo, hi = shard.shard_bounds(weights, w)[r]
+mx = shard.max_over_ranks([float(r + 1), float(hi - lo)])
+tot = shard.sum_over_ranks([hi - lo])
+assert mx[0] == w, mx
+assert tot[0] == 100, tot
+print("ok", r, lo, hi, mx, tot)
+dist.destroy_process_group()
+"""
+
+
+def test_gloo_world_size_2(tmp_path):
+    script = tmp_path / "w.py"
+    script.write_text(GLOO_WORKER)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", str(script), ROOT]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.count("ok ") == 2
