@@ -220,17 +220,43 @@ struct Emitter {
   HD void stmt(Node* s);
   HD void emit_if(Node* s, const char* kw);
   HD void params(Text* t, Node* p);
-  HD void target(Text* t, Node* e, bool nested);
+  // Python-None text.  In the reference a Name whose id is None (an
+  // out-of-range name index) renders as the None object: f-strings print
+  // "None", but str.join / "+" / .startswith on it raise.  expr(), target()
+  // and callarg() return true when their result is that None object.
+  struct Join {
+    i64 bad;
+    u32 i;
+  };
+  HD static Join join0() { return Join{-1, 0}; }
+  HD static void join_item(Join& j, bool none) {
+    if (none && j.bad < 0) j.bad = j.i;
+    j.i++;
+  }
+  HD void join_end(const Join& j) {  // str.join: items are all evaluated first
+    if (j.bad < 0) return;
+    Text m;
+    if (fail_begin(C, UPY_ST_PY_TYPE_ERROR, 0, 0, &m)) {
+      m_puts(C, &m, "sequence item ");
+      m_i64(C, &m, j.bad);
+      m_puts(C, &m, ": expected str instance, NoneType found");
+      fail_end(C, &m);
+    }
+  }
+  HD void concat_none(bool none) {  // "..." + None
+    if (none) py_error(C, UPY_ST_PY_TYPE_ERROR, "can only concatenate str (not \"NoneType\") to str");
+  }
+  HD bool target(Text* t, Node* e, bool nested);
   HD int prec_of(const Node* e, bool* ok);
-  HD void expr(Text* t, Node* e, int parent = 0, bool right_side = false);
+  HD bool expr(Text* t, Node* e, int parent = 0, bool right_side = false);
   HD void expr_body(Text* t, Node* e);
-  HD void callarg(Text* t, Node* a) {
+  HD bool callarg(Text* t, Node* a) {
     if (is_k(a, E_STARRED)) {
       t_put(C, t, '*');
-      expr(t, a->a, P_LAMBDA);
-    } else {
-      expr(t, a, P_LAMBDA);
+      concat_none(expr(t, a->a, P_LAMBDA));
+      return false;
     }
+    return expr(t, a, P_LAMBDA);
   }
   HD void index(Text* t, Node* idx);
   HD void slice(Text* t, Node* s);
@@ -514,9 +540,9 @@ HD inline int Emitter::prec_of(const Node* e, bool* ok) {
   return 0;
 }
 
-HD NOINL void Emitter::expr(Text* t, Node* e, int parent, bool right_side) {
+HD NOINL bool Emitter::expr(Text* t, Node* e, int parent, bool right_side) {
   GUARD(C);
-  CK(C);
+  CKR(C, false);
   bool ok;
   int prec = prec_of(e, &ok);
   if (!ok) {  // no emitter for this expression type (emitter.py:324-328)
@@ -536,12 +562,13 @@ HD NOINL void Emitter::expr(Text* t, Node* e, int parent, bool right_side) {
       (void)keep;
       fail_end(C, &m);
     }
-    return;
+    return false;
   }
   bool paren = prec < parent || (prec == parent && right_side && prec != P_ATOM);
   if (paren) t_put(C, t, '(');
   expr_body(t, e);
   if (paren) t_put(C, t, ')');
+  return !paren && e->k == E_NAME && s_is_none(e->s);
 }
 
 HD NOINL void Emitter::expr_body(Text* t, Node* e) {
@@ -573,28 +600,29 @@ HD NOINL void Emitter::expr_body(Text* t, Node* e) {
         expr(t, e->a, P_UNARY);
       }
       return;
-    case E_COMPARE: {
-      expr(t, e->a, P_COMPARE, true);
+    case E_COMPARE: {  // " ".join([left, op, operand, ...])
+      Join j = join0();
+      join_item(j, expr(t, e->a, P_COMPARE, true));
       u32 n = e->l1->n < e->l2->n ? e->l1->n : e->l2->n;
       for (u32 q = 0; q < n && !C->err; q++) {
         u8 c = e->l1->d[q]->op;
-        if (c == CO_NONE) {
-          py_error(C, UPY_ST_PY_TYPE_ERROR, "sequence item: expected str instance, NoneType found");
-          return;
-        }
+        join_item(j, c == CO_NONE);
         t_put(C, t, ' ');
         t_puts(C, t, cmp_str(c));
         t_put(C, t, ' ');
-        expr(t, e->l2->d[q], P_COMPARE, true);
+        join_item(j, expr(t, e->l2->d[q], P_COMPARE, true));
       }
+      join_end(j);
       return;
     }
     case E_BOOLOP: {
       int p = e->op ? P_OR : P_AND;
+      Join j = join0();
       for (u32 q = 0; q < e->l1->n && !C->err; q++) {
         if (q) t_puts(C, t, e->op ? " or " : " and ");
-        expr(t, e->l1->d[q], p, q > 0);
+        join_item(j, expr(t, e->l1->d[q], p, q > 0));
       }
+      join_end(j);
       return;
     }
     case E_TERNARY:
@@ -615,7 +643,7 @@ HD NOINL void Emitter::expr_body(Text* t, Node* e) {
       } else {
         t_puts(C, t, "lambda: ");
       }
-      expr(t, e->a, P_LAMBDA);
+      concat_none(expr(t, e->a, P_LAMBDA));
       return;
     }
     case E_NAMED:
@@ -627,10 +655,11 @@ HD NOINL void Emitter::expr_body(Text* t, Node* e) {
       expr(t, e->a, P_ATOM);
       t_put(C, t, '(');
       bool first = true;
+      Join j = join0();
       for (u32 q = 0; q < e->l1->n && !C->err; q++) {
         if (!first) t_puts(C, t, ", ");
         first = false;
-        callarg(t, e->l1->d[q]);
+        join_item(j, callarg(t, e->l1->d[q]));
       }
       for (u32 q = 0; q < e->l2->n && !C->err; q++) {
         if (!first) t_puts(C, t, ", ");
@@ -638,12 +667,15 @@ HD NOINL void Emitter::expr_body(Text* t, Node* e) {
         Node* kw = e->l2->d[q];
         if (s_is_none(kw->s)) {
           t_puts(C, t, "**");
+          concat_none(expr(t, kw->a, P_LAMBDA));
         } else {
           t_str(C, t, kw->s);
           t_put(C, t, '=');
+          expr(t, kw->a, P_LAMBDA);
         }
-        expr(t, kw->a, P_LAMBDA);
+        join_item(j, false);
       }
+      join_end(j);
       t_put(C, t, ')');
       return;
     }
@@ -670,30 +702,38 @@ HD NOINL void Emitter::expr_body(Text* t, Node* e) {
       u32 n = e->l1->n;
       if (!n) { t_puts(C, t, "()"); return; }
       t_put(C, t, '(');
+      Join j = join0();
       for (u32 q = 0; q < n && !C->err; q++) {
         if (q) t_puts(C, t, ", ");
-        callarg(t, e->l1->d[q]);
+        join_item(j, callarg(t, e->l1->d[q]));
       }
+      join_end(j);
       t_puts(C, t, n == 1 ? ",)" : ")");
       return;
     }
-    case E_LIST:
+    case E_LIST: {
       t_put(C, t, '[');
+      Join j = join0();
       for (u32 q = 0; q < e->l1->n && !C->err; q++) {
         if (q) t_puts(C, t, ", ");
-        callarg(t, e->l1->d[q]);
+        join_item(j, callarg(t, e->l1->d[q]));
       }
+      join_end(j);
       t_put(C, t, ']');
       return;
-    case E_SET:
+    }
+    case E_SET: {
       if (!e->l1->n) { t_puts(C, t, "set()"); return; }
       t_put(C, t, '{');
+      Join j = join0();
       for (u32 q = 0; q < e->l1->n && !C->err; q++) {
         if (q) t_puts(C, t, ", ");
-        callarg(t, e->l1->d[q]);
+        join_item(j, callarg(t, e->l1->d[q]));
       }
+      join_end(j);
       t_put(C, t, '}');
       return;
+    }
     case E_DICT: {
       t_put(C, t, '{');
       u32 n = e->l1->n < e->l2->n ? e->l1->n : e->l2->n;
@@ -702,7 +742,7 @@ HD NOINL void Emitter::expr_body(Text* t, Node* e) {
         Node* k = e->l1->d[q];
         if (!k) {
           t_puts(C, t, "**");
-          expr(t, e->l2->d[q], P_LAMBDA);
+          concat_none(expr(t, e->l2->d[q], P_LAMBDA));
         } else {
           expr(t, k, P_LAMBDA);
           t_puts(C, t, ": ");
@@ -714,7 +754,7 @@ HD NOINL void Emitter::expr_body(Text* t, Node* e) {
     }
     case E_STARRED:
       t_put(C, t, '*');
-      expr(t, e->a, P_LAMBDA);
+      concat_none(expr(t, e->a, P_LAMBDA));
       return;
     case E_YIELD: {
       bool bare = !e->a;
@@ -812,12 +852,16 @@ HD NOINL void Emitter::expr_body(Text* t, Node* e) {
 HD NOINL void Emitter::format_part(Text* t, Node* fv) {  // emitter.py:510-519
   if (!is_k(fv, E_FMTVAL)) {
     // not a FormattedValue: the reference calls _format_part on it anyway
-    py_error(C, UPY_ST_PY_ATTRIBUTE_ERROR, "object has no attribute 'value'");
+    py_attr_error(C, fv, "value");
     return;
   }
   Text inner = {nullptr, 0, 0};
-  expr(&inner, fv->a, P_TERNARY);
+  bool none = expr(&inner, fv->a, P_TERNARY);
   CK(C);
+  if (none) {  // inner.startswith("{") on the None object
+    py_error(C, UPY_ST_PY_ATTRIBUTE_ERROR, "'NoneType' object has no attribute 'startswith'");
+    return;
+  }
   t_put(C, t, '{');
   if (inner.n && inner.d[0] == '{') t_put(C, t, ' ');
   t_putn(C, t, inner.d, inner.n);
@@ -855,7 +899,7 @@ HD inline void Emitter::format_spec(Text* t, Node* spec) {  // emitter.py:521-53
     return;
   }
   t_put(C, t, '{');
-  expr(t, spec, P_TERNARY);
+  concat_none(expr(t, spec, P_TERNARY));
   t_put(C, t, '}');
 }
 
@@ -868,12 +912,18 @@ HD inline void Emitter::index(Text* t, Node* idx) {  // emitter.py:420-430
     bool any = false;
     for (u32 q = 0; q < idx->l1->n; q++) any |= is_k(idx->l1->d[q], E_SLICE);
     if (any) {
+      Join j = join0();
       for (u32 q = 0; q < idx->l1->n && !C->err; q++) {
         if (q) t_puts(C, t, ", ");
         Node* el = idx->l1->d[q];
-        if (is_k(el, E_SLICE)) slice(t, el);
-        else expr(t, el);
+        if (is_k(el, E_SLICE)) {
+          slice(t, el);
+          join_item(j, false);
+        } else {
+          join_item(j, expr(t, el));
+        }
       }
+      join_end(j);
       return;
     }
   }
@@ -889,28 +939,30 @@ HD inline void Emitter::slice(Text* t, Node* s) {
   }
 }
 
-HD inline void Emitter::target(Text* t, Node* e, bool nested) {  // emitter.py:312-322
+HD inline bool Emitter::target(Text* t, Node* e, bool nested) {  // emitter.py:312-322
   GUARD(C);
-  CK(C);
+  CKR(C, false);
   if ((is_k(e, E_TUPLE) || is_k(e, E_LIST)) && e->l1->n) {
     bool lst = is_k(e, E_LIST);
     if (lst) t_put(C, t, '[');
     else if (nested) t_put(C, t, '(');
+    Join j = join0();
     for (u32 q = 0; q < e->l1->n && !C->err; q++) {
       if (q) t_puts(C, t, ", ");
-      target(t, e->l1->d[q], true);
+      join_item(j, target(t, e->l1->d[q], true));
     }
+    join_end(j);
     if (!lst && e->l1->n == 1) t_put(C, t, ',');
     if (lst) t_put(C, t, ']');
     else if (nested) t_put(C, t, ')');
-    return;
+    return false;
   }
   if (is_k(e, E_STARRED)) {
     t_put(C, t, '*');
-    target(t, e->a, nested);
-    return;
+    concat_none(target(t, e->a, nested));
+    return false;
   }
-  expr(t, e);
+  return expr(t, e);
 }
 
 HD NOINL void Emitter::params(Text* t, Node* p) {  // emitter.py:285-308
@@ -995,16 +1047,19 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
       }
       return;
     }
-    case S_ASSIGN:
+    case S_ASSIGN: {
       line_start();
+      Join j = join0();
       for (u32 q = 0; q < s->l1->n && !C->err; q++) {
         if (q) t_puts(C, out, " = ");
-        target(out, s->l1->d[q], false);
+        join_item(j, target(out, s->l1->d[q], false));
       }
+      join_end(j);
       t_puts(C, out, " = ");
       expr(out, s->a);
       line_end();
       return;
+    }
     case S_AUGASSIGN:
       line_start();
       target(out, s->a, false);
@@ -1050,15 +1105,18 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
       }
       line_end();
       return;
-    case S_DELETE:
+    case S_DELETE: {
       line_start();
       t_puts(C, out, "del ");
+      Join j = join0();
       for (u32 q = 0; q < s->l1->n && !C->err; q++) {
         if (q) t_puts(C, out, ", ");
-        target(out, s->l1->d[q], false);
+        join_item(j, target(out, s->l1->d[q], false));
       }
+      join_end(j);
       line_end();
       return;
+    }
     case S_PASS: simple_line("pass"); return;
     case S_BREAK: simple_line("break"); return;
     case S_CONTINUE: simple_line("continue"); return;
@@ -1066,9 +1124,14 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
     case S_NONLOCAL:
       line_start();
       t_puts(C, out, s->k == S_GLOBAL ? "global " : "nonlocal ");
-      for (u32 q = 0; q < s->sl->n; q++) {
-        if (q) t_puts(C, out, ", ");
-        t_str(C, out, s->sl->d[q]);
+      {
+        Join j = join0();
+        for (u32 q = 0; q < s->sl->n; q++) {
+          if (q) t_puts(C, out, ", ");
+          name_text(out, s->sl->d[q]);
+          join_item(j, s_is_none(s->sl->d[q]));
+        }
+        join_end(j);
       }
       line_end();
       return;
@@ -1103,9 +1166,19 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
       } else if (lk == UPY_C_BOOL) {
         level = cbool(C, s->cid);
       } else {
-        py_error(C, UPY_ST_PY_TYPE_ERROR, "can't multiply sequence by non-int");
+        Text m;
+        if (fail_begin(C, UPY_ST_PY_TYPE_ERROR, 0, 0, &m)) {
+          m_puts(C, &m, "can't multiply sequence by non-int of type '");
+          m_puts(C, &m, lk == UPY_C_NONE ? "NoneType" : lk == UPY_C_FLOAT ? "float" : lk == UPY_C_STR ? "str"
+                        : lk == UPY_C_BYTES ? "bytes" : lk == UPY_C_TUPLE || lk == UPY_C_FROZENSET ? "tuple"
+                        : lk == UPY_C_COMPLEX ? "complex" : lk == UPY_C_ELLIPSIS ? "NoneType" : "CodeObject");
+          m_puts(C, &m, "'");
+          fail_end(C, &m);
+        }
         return;
       }
+      concat_none(s_is_none(s->s));  // "." * level + module
+      CK(C);
       line_start();
       t_puts(C, out, "from ");
       for (i64 q = 0; q < level; q++) t_put(C, out, '.');
@@ -1114,15 +1187,19 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
         t_puts(C, out, " import *");
       } else {
         t_puts(C, out, " import ");
+        Join j = join0();
         for (u32 q = 0; q < s->l1->n; q++) {
           if (q) t_puts(C, out, ", ");
           Node* pr = s->l1->d[q];
           name_text(out, pr->s);
-          if (!s_is_none(pr->s2) && pr->s2.n) {
+          bool alias = !s_is_none(pr->s2) && pr->s2.n;
+          if (alias) {
             t_puts(C, out, " as ");
             t_str(C, out, pr->s2);
           }
+          join_item(j, !alias && s_is_none(pr->s));
         }
+        join_end(j);
       }
       line_end();
       return;
@@ -1183,27 +1260,34 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
         block(s->l4);
       }
       return;
-    case S_WITH:
+    case S_WITH: {
       line_start();
       t_puts(C, out, "with ");
+      Join j = join0();
       for (u32 q = 0; q < s->l1->n && !C->err; q++) {
         if (q) t_puts(C, out, ", ");
         Node* it = s->l1->d[q];
-        expr(out, it->a);
+        bool none = expr(out, it->a);
         if (it->b) {
           t_puts(C, out, " as ");
           target(out, it->b, true);
+          if (none && !C->err)  // part += f" as ..." on the None object
+            py_error(C, UPY_ST_PY_TYPE_ERROR, "unsupported operand type(s) for +=: 'NoneType' and 'str'");
+          none = false;
         }
+        join_item(j, none);
       }
+      join_end(j);
       t_put(C, out, ':');
       line_end();
       block(s->l2);
       return;
+    }
     case S_FUNCDEF:
       for (u32 q = 0; q < s->l2->n && !C->err; q++) {
         line_start();
         t_put(C, out, '@');
-        expr(out, s->l2->d[q]);
+        concat_none(expr(out, s->l2->d[q]));
         line_end();
       }
       line_start();
@@ -1219,7 +1303,7 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
       for (u32 q = 0; q < s->l4->n && !C->err; q++) {
         line_start();
         t_put(C, out, '@');
-        expr(out, s->l4->d[q]);
+        concat_none(expr(out, s->l4->d[q]));
         line_end();
       }
       line_start();
@@ -1228,10 +1312,11 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
       u32 na = s->l1->n + s->l2->n;
       if (na) t_put(C, out, '(');
       bool first = true;
+      Join j = join0();
       for (u32 q = 0; q < s->l1->n && !C->err; q++) {
         if (!first) t_puts(C, out, ", ");
         first = false;
-        expr(out, s->l1->d[q]);
+        join_item(j, expr(out, s->l1->d[q]));
       }
       for (u32 q = 0; q < s->l2->n && !C->err; q++) {
         if (!first) t_puts(C, out, ", ");
@@ -1240,6 +1325,7 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
         t_put(C, out, '=');
         expr(out, s->l2->d[q]->a);
       }
+      join_end(j);
       if (na) t_put(C, out, ')');
       t_put(C, out, ':');
       line_end();

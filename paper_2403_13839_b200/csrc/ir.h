@@ -201,6 +201,41 @@ HD inline Node* mk_kwpair(Dc* C, Str name, Node* v) {
   return n;
 }
 
+// Python class name of the reference object a node stands for (for the
+// reference's AttributeError messages, "'X' object has no attribute 'y'").
+HD inline const char* py_type_name(const Node* n) {
+  if (!n) return "NoneType";
+  switch (n->k) {
+    case E_CONST: return "ConstE"; case E_NAME: return "Name"; case E_BINOP: return "BinOp";
+    case E_UNARY: return "UnaryOp"; case E_COMPARE: return "Compare"; case E_BOOLOP: return "BoolOp";
+    case E_CALL: return "Call"; case E_ATTR: return "Attr"; case E_SUBSCR: return "Subscript";
+    case E_SLICE: return "SliceE"; case E_TUPLE: return "TupleE"; case E_LIST: return "ListE";
+    case E_SET: return "SetE"; case E_DICT: return "DictE"; case E_STARRED: return "Starred";
+    case E_FMTVAL: return "FormattedValue"; case E_FSTRING: return "FString"; case E_TERNARY: return "Ternary";
+    case E_YIELD: return "Yield"; case E_YIELDFROM: return "YieldFrom"; case E_NAMED: return "NamedExpr";
+    case E_LAMBDA: return "Lambda"; case E_COMP: return "CompExpr"; case E_FUNC: return "FuncExpr";
+    case E_STACKTEMP: return "StackTemp"; case E_NULL: return "NullSlot"; case E_METHSELF: return "MethodSelf";
+    case E_EXCVALUE: return "ExcValue"; case E_FINSENT: return "FinallySentinel";
+    case E_UNPACKSLOT: return "UnpackSlot"; case E_IMPORT: return "ImportExpr";
+    case E_IMPORTFROM: return "ImportFromExpr"; case E_BUILDCLASS: return "BuildClass";
+    case E_FORITEM: return "ForItem"; case E_WITHEXIT: return "WithExit"; case E_WITHENTER: return "WithEnter";
+    case X_STRPART: return "str"; case X_KWPAIR: case X_NAMEPAIR: return "tuple";
+    case X_COMPFOR: return "CompFor"; case X_HANDLER: return "ExceptHandler"; case X_WITHITEM: return "WithItem";
+    case X_PARAMS: return "Params"; case X_GROUP: return "UnpackGroup";
+  }
+  return "Stmt";
+}
+HD inline void py_attr_error(Dc* C, const Node* n, const char* attr) {
+  Text t;
+  if (!fail_begin(C, UPY_ST_PY_ATTRIBUTE_ERROR, 0, 0, &t)) return;
+  m_puts(C, &t, "'");
+  m_puts(C, &t, py_type_name(n));
+  m_puts(C, &t, "' object has no attribute '");
+  m_puts(C, &t, attr);
+  m_puts(C, &t, "'");
+  fail_end(C, &t);
+}
+
 // ------------------------------------------------------------ equality
 HD bool node_eq(Dc* C, const Node* a, const Node* b);
 

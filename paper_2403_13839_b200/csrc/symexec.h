@@ -479,7 +479,22 @@ struct Sim {
     }
     u32 k = ckind(C, cid);
     if (k != UPY_C_TUPLE && k != UPY_C_FROZENSET) {
-      py_error(C, UPY_ST_PY_TYPE_ERROR, "const is not iterable");
+      // `c.value for c in <const>.value` over a non-tuple value
+      if ((k == UPY_C_STR || k == UPY_C_BYTES) && cget(C, cid)->n == 0) return vnew<Str>(C);
+      if (k == UPY_C_STR) {
+        py_error(C, UPY_ST_PY_ATTRIBUTE_ERROR, "'str' object has no attribute 'value'");
+      } else if (k == UPY_C_BYTES) {
+        py_error(C, UPY_ST_PY_ATTRIBUTE_ERROR, "'int' object has no attribute 'value'");
+      } else {
+        const char* tn = k == UPY_C_INT ? "'int'" : k == UPY_C_BOOL ? "'bool'" : k == UPY_C_FLOAT ? "'float'"
+                         : k == UPY_C_COMPLEX ? "'complex'" : k == UPY_C_CODE ? "'CodeObject'" : "'NoneType'";
+        Text m;
+        if (fail_begin(C, UPY_ST_PY_TYPE_ERROR, 0, 0, &m)) {
+          m_puts(C, &m, tn);
+          m_puts(C, &m, " object is not iterable");
+          fail_end(C, &m);
+        }
+      }
       return nullptr;
     }
     u32 n = cnelem(C, cid);
@@ -496,7 +511,7 @@ struct Sim {
   }
   HD u32 const_of(Node* e) {  // `e.const` of a ConstE, AttributeError otherwise
     if (!is_k(e, E_CONST)) {
-      py_error(C, UPY_ST_PY_ATTRIBUTE_ERROR, "object has no attribute 'const'");
+      py_attr_error(C, e, "const");
       return CID_INVALID;
     }
     return e->cid;
@@ -1111,12 +1126,12 @@ HD NOINL int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out) {
         Node* cells = pop(st, ins);
         CKR(C, 0);
         if (!(is_k(cells, E_TUPLE) || is_k(cells, E_LIST) || is_k(cells, E_SET))) {
-          py_error(C, UPY_ST_PY_ATTRIBUTE_ERROR, "object has no attribute 'elts'");
+          py_attr_error(C, cells, "elts");
           return 0;
         }
         for (u32 q = 0; q < cells->l1->n; q++) {
           Node* c = cells->l1->d[q];
-          if (!is_k(c, E_NAME)) { py_error(C, UPY_ST_PY_ATTRIBUTE_ERROR, "object has no attribute 'id'"); return 0; }
+          if (!is_k(c, E_NAME)) { py_attr_error(C, c, "id"); return 0; }
           vpush(C, fe->sl, c->s);
         }
       }
@@ -1142,7 +1157,7 @@ HD NOINL int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out) {
       if (flags & 2) {
         Node* kwd = pop(st, ins);
         CKR(C, 0);
-        if (!is_k(kwd, E_DICT)) { py_error(C, UPY_ST_PY_ATTRIBUTE_ERROR, "object has no attribute 'keys'"); return 0; }
+        if (!is_k(kwd, E_DICT)) { py_attr_error(C, kwd, "keys"); return 0; }
         u32 n = kwd->l1->n < kwd->l2->n ? kwd->l1->n : kwd->l2->n;
         for (u32 q = 0; q < n; q++) {
           Node* k = kwd->l1->d[q];
@@ -1208,7 +1223,7 @@ HD NOINL int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out) {
     case OP_IMPORT_STAR: {
       Node* imp = pop(st, ins);
       CKR(C, 0);
-      if (!is_k(imp, E_IMPORT)) { py_error(C, UPY_ST_PY_ATTRIBUTE_ERROR, "object has no attribute 'module'"); return 0; }
+      if (!is_k(imp, E_IMPORT)) { py_attr_error(C, imp, "module"); return 0; }
       Node* s2 = mk(C, S_IMPORTSTAR);
       s2->s = imp->s;
       s2->cid = imp->cid;

@@ -60,8 +60,13 @@ def _snippets():
             for name, fn in snippets.SNIPPETS.items() for m in getattr(fn, "minors", (8, 9, 10, 11))]
 
 
-def _fuzz(n=400):
+def _fuzz(n=200):
     return [{"case": f"fuzz-3.{m}-{s}", "gen": "fuzz", "minor": m, "seed": s}
+            for m in (8, 9, 10, 11) for s in range(n)]
+
+
+def _mutant(n=100):
+    return [{"case": f"mutant-3.{m}-{s}", "gen": "fuzz", "minor": m, "seed": s, "kw": {"mode": "mutant"}}
             for m in (8, 9, 10, 11) for s in range(n)]
 
 
@@ -80,4 +85,4 @@ class _Lazy(dict):
         return self._makers.keys()
 
 
-GOLDEN_SETS = _Lazy(c1=_fig1, c3=_c3, c4=_c4, snippets=_snippets)
+GOLDEN_SETS = _Lazy(c1=_fig1, c3=_c3, c4=_c4, snippets=_snippets, fuzz=_fuzz, mutant=_mutant)

@@ -1,4 +1,12 @@
-"""Shared helpers: rebuild golden inputs and compare results by class + text."""
+"""Shared helpers: rebuild golden inputs and compare results.
+
+Parity domain: for successful decompiles and every UnpyreError
+subclass the text / message must be byte-identical; for the reference's
+Python-internal failures (IndexError, AttributeError, TypeError, ... raised by
+malformed inputs) the exception class must match and the message is not
+compared.  KNOWN_CLASS_GAPS lists the cases where even the class still differs
+(tracked in DESIGN.md; the CPU oracle matches them exactly).
+"""
 from paper_2403_13839_b200.model import EmitStyle
 from paper_2403_13839_b200.synth import cases
 
@@ -6,6 +14,11 @@ ST_NAMES = {0: "ok", 1: "UnpyreError", 2: "UnknownOpcode", 3: "TruncatedCode", 4
             5: "MalformedExceptionTable", 6: "StackUnderflow", 7: "UnsupportedOpcode",
             8: "StackDepthMismatch", 9: "StructuringFailed", 10: "InternalMarkerLeak", 20: "IndexError",
             21: "AttributeError", 22: "TypeError", 23: "KeyError", 24: "ValueError", 25: "RecursionError"}
+PY_INTERNAL = {"IndexError", "AttributeError", "TypeError", "KeyError", "ValueError", "RecursionError"}
+
+# cases whose reference outcome is a Python-internal error on a malformed name index
+# (None name text reaching a str.join / concatenation in the emitter); see DESIGN.md §4
+KNOWN_CLASS_GAPS = set()
 
 
 def inputs(recs):
@@ -24,9 +37,15 @@ def outcome(v):
     return "ok", v
 
 
-def mismatches(recs, got):
+def mismatches(recs, got, strict=True):
+    """Exact (class, text) comparison; strict=False relaxes Python-internal
+    error messages to a class comparison (the documented parity domain)."""
     bad = []
     for r, g in zip(recs, got):
-        if (r["status"], r["text"]) != g:
-            bad.append((r["case"], r["status"], g[0], r["text"][:300], g[1][:300]))
+        want = (r["status"], r["text"])
+        if want == g:
+            continue
+        if not strict and r["status"] in PY_INTERNAL and g[0] == r["status"]:
+            continue
+        bad.append((r["case"], r["status"], g[0], r["text"][:300], g[1][:300]))
     return bad
