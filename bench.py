@@ -33,6 +33,7 @@ WORKLOADS = {
     "c3": ("c3_310", 1_000_000, "C3: synthetic 1M code objects x ~200 units (3.10), straight-line"),
     "c3_311": ("c3_311", 1_000_000, "C3 (3.11 variant): synthetic 1M code objects x ~200 units + caches"),
     "c4": ("c4_310", 65_536, "C4: synthetic 64K code objects x ~10K units (3.10), nested if/for/while/try"),
+    "c4_311": ("c4_311", 65_536, "C4 (3.11 variant): synthetic 64K code objects x ~10K units, exception tables"),
 }
 
 

@@ -11,6 +11,7 @@ POOLS = {
     "c3_311": {"gen": "c3", "minor": 11, "size": 1024},
     # C4: ~10K-unit nested control flow (3.10)
     "c4_310": {"gen": "c4", "minor": 10, "size": 64, "units": 10000},
+    "c4_311": {"gen": "c4", "minor": 11, "size": 32, "units": 10000},
 }
 
 

@@ -61,10 +61,11 @@ def build_cuda(force=False, verbose=True):
     cmd = [nvcc, *NVCC_FLAGS, "-o", LIB + ".tmp", os.path.join(CSRC, "upy.cu")]
     if verbose:
         print("[build]", " ".join(cmd), flush=True)
+    digest = _digest(deps, NVCC_FLAGS)  # of the sources as they were when compilation started
     subprocess.check_call(cmd)
     os.replace(LIB + ".tmp", LIB)
     with open(LIB + ".stamp", "w") as f:
-        f.write(_digest(deps, NVCC_FLAGS))
+        f.write(digest)
     return LIB
 
 

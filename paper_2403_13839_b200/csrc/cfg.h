@@ -365,26 +365,29 @@ HD NOINL Cfg* build_basic_blocks(Dc* C, const Code* K, const Vec<ExcEntry>* entr
   i32 n = K->n_ins;
   u32 end_of_code = ins_end(I[n - 1]);
   G->end_of_code = end_of_code;
-  Vec<u32>* L = vnew<u32>(C, (u32)n + 8);
-  vpush(C, L, I[0].offset);
+  // leaders on the scratch stack (released when analyze() returns)
+  u32 ne = entries ? entries->n : 0;
+  u32* Ld = sarr<u32>(C, 1 + 2 * (u64)n + 3 * (u64)ne, false);
+  CKR(C, G);
+  u32 nl = 0;
+  Ld[nl++] = I[0].offset;
   for (i32 i = 0; i < n; i++)
-    if (ins_is_jump(I[i])) vpush(C, L, jump_target(K, I[i]));
+    if (ins_is_jump(I[i])) Ld[nl++] = jump_target(K, I[i]);
   for (i32 i = 0; i < n; i++) {
     u8 op = I[i].op;
     bool ender = op == OP_RETURN_VALUE || op == OP_RAISE_VARARGS || op == OP_RERAISE || op == OP_END_FINALLY ||
                  (ins_is_jump(I[i]) && !is_setup_op(op));
-    if (ender && ins_end(I[i]) < end_of_code) vpush(C, L, ins_end(I[i]));
+    if (ender && ins_end(I[i]) < end_of_code) Ld[nl++] = ins_end(I[i]);
   }
-  for (u32 e = 0; entries && e < entries->n; e++) {
-    vpush(C, L, entries->d[e].target);
-    vpush(C, L, entries->d[e].start);
-    if (entries->d[e].end < end_of_code) vpush(C, L, entries->d[e].end);
+  for (u32 e = 0; e < ne; e++) {
+    Ld[nl++] = entries->d[e].target;
+    Ld[nl++] = entries->d[e].start;
+    if (entries->d[e].end < end_of_code) Ld[nl++] = entries->d[e].end;
   }
-  CKR(C, G);
-  sort_u32(L->d, (i32)L->n);
+  sort_u32(Ld, (i32)nl);
   u32 nu = 0;
-  for (u32 i = 0; i < L->n; i++)
-    if (nu == 0 || L->d[nu - 1] != L->d[i]) L->d[nu++] = L->d[i];
+  for (u32 i = 0; i < nl; i++)
+    if (nu == 0 || Ld[nu - 1] != Ld[i]) Ld[nu++] = Ld[i];
   G->n_blocks = (i32)nu;
   G->blocks = (Block*)zalloc(C, (u64)nu * sizeof(Block));
   CKR(C, G);
@@ -392,8 +395,8 @@ HD NOINL Cfg* build_basic_blocks(Dc* C, const Code* K, const Vec<ExcEntry>* entr
   for (u32 b = 0; b < nu; b++) {
     Block& B = G->blocks[b];
     B.id = (i32)b;
-    B.start = L->d[b];
-    B.end = b + 1 < nu ? L->d[b + 1] : end_of_code;
+    B.start = Ld[b];
+    B.end = b + 1 < nu ? Ld[b + 1] : end_of_code;
     while (cursor < n && I[cursor].offset < B.start) cursor++;
     i32 lo = ins_index_of(K, B.start);
     i32 hi = lo;
@@ -449,20 +452,27 @@ HD NOINL Cfg* build_basic_blocks(Dc* C, const Code* K, const Vec<ExcEntry>* entr
   return G;
 }
 
-// reachable_from (cfg.py:144-157) into a bitmap
+HD inline u32 total_edges(const Cfg* G) {
+  u32 e = 0;
+  for (i32 b = 0; b < G->n_blocks; b++) e += G->blocks[b].succ->n;
+  return e;
+}
+
+// reachable_from (cfg.py:144-157) into a scratch bitmap
 HD inline u8* reachable_from(Dc* C, const Cfg* G, i32 root, bool include_exc) {
-  u8* seen = (u8*)zalloc(C, (u64)G->n_blocks);
-  Vec<i32>* work = vnew<i32>(C, 16);
+  u8* seen = sarr<u8>(C, (u64)G->n_blocks);
+  i32* work = sarr<i32>(C, (u64)total_edges(G) + 1, false);
   CKR(C, seen);
-  vpush(C, work, root);
-  while (work->n && !C->err) {
-    i32 b = work->d[--work->n];
+  u32 sp = 0;
+  work[sp++] = root;
+  while (sp) {
+    i32 b = work[--sp];
     if (seen[b]) continue;
     seen[b] = 1;
     const Block& B = G->blocks[b];
     for (u32 q = 0; q < B.succ->n; q++) {
       if (B.succ_kind->d[q] == EK_EXC && !include_exc) continue;
-      if (!seen[B.succ->d[q]]) vpush(C, work, B.succ->d[q]);
+      if (!seen[B.succ->d[q]]) work[sp++] = B.succ->d[q];
     }
   }
   return seen;
@@ -500,15 +510,15 @@ HD inline bool has_normal_edge(const Block& P, i32 to) {
   return false;
 }
 
-// compute_dominators (cfg.py:160-220); idom[b] = -1 when b has no entry
+// compute_dominators (cfg.py:160-220); idom[b] = -1 when b has no entry.  Scratch.
 HD NOINL i32* compute_dominators(Dc* C, const Cfg* G, i32 root, const u8* universe) {
   i32 nb = G->n_blocks;
-  i32* idom = (i32*)zalloc(C, (u64)nb * sizeof(i32));
-  i32* rpo_index = (i32*)zalloc(C, (u64)nb * sizeof(i32));
-  u8* seen = (u8*)zalloc(C, (u64)nb);
-  i32* order = (i32*)zalloc(C, (u64)nb * sizeof(i32));
-  i32* stk_b = (i32*)zalloc(C, (u64)nb * sizeof(i32));
-  u32* stk_q = (u32*)zalloc(C, (u64)nb * sizeof(u32));
+  i32* idom = sarr<i32>(C, (u64)nb, false);
+  i32* rpo_index = sarr<i32>(C, (u64)nb, false);
+  u8* seen = sarr<u8>(C, (u64)nb);
+  i32* order = sarr<i32>(C, (u64)nb, false);
+  i32* stk_b = sarr<i32>(C, (u64)nb, false);
+  u32* stk_q = sarr<u32>(C, (u64)nb, false);
   CKR(C, idom);
   for (i32 b = 0; b < nb; b++) idom[b] = -1;
   // iterative DFS mirroring the recursive one (postorder)
@@ -584,8 +594,8 @@ HD inline bool dominates(const i32* idom, i32 a, i32 b) {  // cfg.py:223-231
   }
 }
 
-// analyze_loops (cfg.py:241-313); appends loops whose header is new to G->loops.
-// Returns false when irreducible.
+// analyze_loops (cfg.py:241-313); appends loops whose header is new to G->loops
+// (persistent), everything else on the scratch stack.  Returns false when irreducible.
 HD NOINL bool analyze_loops(Dc* C, Cfg* G, const i32* idom, const u8* universe) {
   i32 nb = G->n_blocks;
   // roots: universe blocks with no predecessor in the universe (any edge kind)
@@ -599,18 +609,20 @@ HD NOINL bool analyze_loops(Dc* C, Cfg* G, const i32* idom, const u8* universe) 
     for (u32 q = 0; q < B.pred->n && !has; q++) has = universe[B.pred->d[q]] != 0;
     if (!has && first_root < 0) first_root = b;
   }
-  // Python iterates a set of small ints in ascending order when the table is large
-  // enough; roots is at most one element in practice, so take it.
+  // roots has at most one element (every other universe block was reached from
+  // the dominator root through a predecessor in the universe), so its order is moot
   if (first_root >= 0) root = first_root;
   else root = universe[G->entry] ? G->entry : min_u;
   if (root < 0) return true;
-  u8* visited = (u8*)zalloc(C, (u64)nb);
-  u8* onstack = (u8*)zalloc(C, (u64)nb);
-  i32* stk_b = (i32*)zalloc(C, (u64)nb * sizeof(i32));
-  u32* stk_q = (u32*)zalloc(C, (u64)nb * sizeof(u32));
-  Vec<i32>* ru = vnew<i32>(C, 8);
-  Vec<i32>* rv = vnew<i32>(C, 8);
+  u32 E = total_edges(G) + 1;
+  u8* visited = sarr<u8>(C, (u64)nb);
+  u8* onstack = sarr<u8>(C, (u64)nb);
+  i32* stk_b = sarr<i32>(C, (u64)nb, false);
+  u32* stk_q = sarr<u32>(C, (u64)nb, false);
+  i32* ru = sarr<i32>(C, E, false);
+  i32* rv = sarr<i32>(C, E, false);
   CKR(C, true);
+  u32 nr = 0;
   i32 sp = 0;
   visited[root] = 1;
   onstack[root] = 1;
@@ -636,8 +648,9 @@ HD NOINL bool analyze_loops(Dc* C, Cfg* G, const i32* idom, const u8* universe) 
         pushed = true;
         break;
       } else if (onstack[v]) {
-        vpush(C, ru, u);
-        vpush(C, rv, v);
+        ru[nr] = u;
+        rv[nr] = v;
+        nr++;
       }
     }
     if (!pushed) {
@@ -646,129 +659,142 @@ HD NOINL bool analyze_loops(Dc* C, Cfg* G, const i32* idom, const u8* universe) 
     }
   }
   bool reducible = true;
-  // back edges grouped by header in first-seen order
-  Vec<i32>* hdrs = vnew<i32>(C, 4);
-  Vec<Vec<i32>*>* tails = vnew<Vec<i32>*>(C, 4);
-  for (u32 e = 0; e < ru->n; e++) {
-    i32 u = ru->d[e], v = rv->d[e];
+  // back edges grouped by header in first-seen order; tails are persistent
+  i32* hdrs = sarr<i32>(C, (u64)nb + 1, false);
+  Vec<i32>** tails = sarr<Vec<i32>*>(C, (u64)nb + 1, false);
+  CKR(C, true);
+  u32 nh = 0;
+  for (u32 e = 0; e < nr; e++) {
+    i32 u = ru[e], v = rv[e];
     if (dominates(idom, v, u)) {
       u32 h = 0;
-      while (h < hdrs->n && hdrs->d[h] != v) h++;
-      if (h == hdrs->n) {
-        vpush(C, hdrs, v);
-        vpush(C, tails, vnew<i32>(C, 2));
+      while (h < nh && hdrs[h] != v) h++;
+      if (h == nh) {
+        hdrs[nh] = v;
+        tails[nh] = vnew<i32>(C, 2);
+        nh++;
       }
       CKR(C, true);
-      vpush(C, tails->d[h], u);
+      vpush(C, tails[h], u);
     } else {
       reducible = false;
     }
   }
-  for (u32 h = 0; h < hdrs->n && !C->err; h++) {
-    i32 header = hdrs->d[h];
-    u8* body = (u8*)zalloc(C, (u64)nb);
-    Vec<i32>* work = vnew<i32>(C, 8);
-    CKR(C, reducible);
+  u8* body = sarr<u8>(C, (u64)nb, false);
+  i32* work = sarr<i32>(C, E + nb, false);
+  CKR(C, reducible);
+  for (u32 h = 0; h < nh && !C->err; h++) {
+    i32 header = hdrs[h];
+    for (i32 b = 0; b < nb; b++) body[b] = 0;
+    u32 wn = 0;
     body[header] = 1;
-    for (u32 t = 0; t < tails->d[h]->n; t++) vpush(C, work, tails->d[h]->d[t]);
-    while (work->n && !C->err) {
-      i32 nn = work->d[--work->n];
+    for (u32 t = 0; t < tails[h]->n; t++) work[wn++] = tails[h]->d[t];
+    while (wn) {
+      i32 nn = work[--wn];
       if (body[nn]) continue;
       body[nn] = 1;
       const Block& N = G->blocks[nn];
       for (u32 q = 0; q < N.pred->n; q++) {
         i32 p = N.pred->d[q];
-        if (universe[p] && has_normal_edge(G->blocks[p], nn)) vpush(C, work, p);
+        if (universe[p] && has_normal_edge(G->blocks[p], nn)) work[wn++] = p;
       }
     }
     if (G->loop_of_header[header] >= 0) continue;  // only new headers are added
     Loop L;
     L.header = header;
-    L.body = vnew<i32>(C, 8);
+    u32 cnt = 0;
+    for (i32 b = 0; b < nb; b++) cnt += body[b];
+    L.body = vnew<i32>(C, cnt);
     for (i32 b = 0; b < nb; b++)
       if (body[b]) vpush(C, L.body, b);
-    L.back_tails = tails->d[h];
+    L.back_tails = tails[h];
     G->loop_of_header[header] = (i32)G->loops->n;
     vpush(C, G->loops, L);
   }
   return reducible;
 }
 
-// analyze (pipeline.py:17-54)
+// analyze (pipeline.py:17-54).  All analysis temporaries live on the scratch
+// stack and are released before returning (the Cfg, loops and entries persist).
 HD NOINL Cfg* analyze(Dc* C, Code* K) {
-  Vec<ExcEntry>* entries = vnew<ExcEntry>(C);
-  if (K->minor >= 11) {
-    rewrite_yield_from(C, K);
-    CKR(C, nullptr);
-    Vec<ExcEntry>* raw = decode_exception_table(C, K);
-    CKR(C, nullptr);
-    for (u32 e = 0; e < raw->n; e++) {
-      i32 ti = ins_index_of(K, raw->d[e].target);
-      if (ti < K->n_ins && K->ins[ti].offset == raw->d[e].target) vpush(C, entries, raw->d[e]);
+  u64 mark = C->top;
+  Cfg* G = nullptr;
+  do {
+    Vec<ExcEntry>* entries = vnew<ExcEntry>(C);
+    if (K->minor >= 11) {
+      rewrite_yield_from(C, K);
+      if (C->err) break;
+      Vec<ExcEntry>* raw = decode_exception_table(C, K);
+      if (C->err) break;
+      for (u32 e = 0; e < raw->n; e++) {
+        i32 ti = ins_index_of(K, raw->d[e].target);
+        if (ti < K->n_ins && K->ins[ti].offset == raw->d[e].target) vpush(C, entries, raw->d[e]);
+      }
+    } else {
+      Vec<TryRegion>* rs = match_try_regions(C, K, nullptr);
+      if (C->err) break;
+      for (u32 r = 0; r < rs->n; r++) {
+        ExcEntry e;
+        e.start = rs->d[r].start;
+        e.end = rs->d[r].end;
+        e.target = rs->d[r].handler;
+        e.depth = 0;
+        e.lasti = false;
+        vpush(C, entries, e);
+      }
     }
-  } else {
-    Vec<TryRegion>* rs = match_try_regions(C, K, nullptr);
-    CKR(C, nullptr);
-    for (u32 r = 0; r < rs->n; r++) {
-      ExcEntry e;
-      e.start = rs->d[r].start;
-      e.end = rs->d[r].end;
-      e.target = rs->d[r].handler;
-      e.depth = 0;
-      e.lasti = false;
-      vpush(C, entries, e);
+    if (C->err) break;
+    G = build_basic_blocks(C, K, entries);
+    if (C->err) break;
+    prune_unreachable(C, G);
+    if (C->err) break;
+    i32 nb = G->n_blocks;
+    G->loops = vnew<Loop>(C, 4);
+    G->loop_of_header = (i32*)ualloc(C, (u64)nb * sizeof(i32));
+    if (C->err) break;
+    for (i32 b = 0; b < nb; b++) G->loop_of_header[b] = -1;
+    u8* uni = reachable_from(C, G, G->entry, false);
+    i32* idom = compute_dominators(C, G, G->entry, uni);
+    u8* covered = sarr<u8>(C, (u64)nb);  // universe of analyze_loops = set(idom), then grows
+    if (C->err) break;
+    for (i32 b = 0; b < nb; b++) covered[b] = idom[b] >= 0;
+    if (!analyze_loops(C, G, idom, covered)) {
+      if (C->err) break;
+      fail_struct(C, G->entry, "irreducible control flow");
+      break;
     }
-  }
-  CKR(C, nullptr);
-  Cfg* G = build_basic_blocks(C, K, entries);
-  CKR(C, nullptr);
-  prune_unreachable(C, G);
-  CKR(C, nullptr);
-  G->loops = vnew<Loop>(C, 4);
-  G->loop_of_header = (i32*)zalloc(C, (u64)G->n_blocks * sizeof(i32));
-  CKR(C, nullptr);
-  for (i32 b = 0; b < G->n_blocks; b++) G->loop_of_header[b] = -1;
-  u8* uni = reachable_from(C, G, G->entry, false);
-  i32* idom = compute_dominators(C, G, G->entry, uni);
-  CKR(C, nullptr);
-  // universe of analyze_loops = set(idom)
-  u8* dom_set = (u8*)zalloc(C, (u64)G->n_blocks);
-  CKR(C, nullptr);
-  for (i32 b = 0; b < G->n_blocks; b++) dom_set[b] = idom[b] >= 0;
-  if (!analyze_loops(C, G, idom, dom_set)) {
-    CKR(C, nullptr);
-    fail_struct(C, G->entry, "irreducible control flow");
-    return nullptr;
-  }
-  CKR(C, nullptr);
-  u8* covered = dom_set;
-  for (u32 e = 0; e < entries->n; e++) {
-    i32 root = block_at(G, entries->d[e].target);
-    if (root < 0 || covered[root]) continue;
-    u8* reach = reachable_from(C, G, root, false);
-    u8* uni2 = (u8*)zalloc(C, (u64)G->n_blocks);
-    CKR(C, nullptr);
-    bool any = false;
-    for (i32 b = 0; b < G->n_blocks; b++) {
-      uni2[b] = reach[b] && !covered[b];
-      any |= uni2[b] != 0;
+    if (C->err) break;
+    for (u32 e = 0; e < entries->n && !C->err; e++) {
+      i32 root = block_at(G, entries->d[e].target);
+      if (root < 0 || covered[root]) continue;
+      u64 inner = C->top;  // per-handler temporaries
+      u8* reach = reachable_from(C, G, root, false);
+      u8* uni2 = sarr<u8>(C, (u64)nb, false);
+      if (C->err) break;
+      bool any = false;
+      for (i32 b = 0; b < nb; b++) {
+        uni2[b] = reach[b] && !covered[b];
+        any |= uni2[b] != 0;
+      }
+      if (!any) {
+        C->top = inner;
+        continue;
+      }
+      uni2[root] = 1;
+      i32* sub = compute_dominators(C, G, root, uni2);
+      u8* sub_set = sarr<u8>(C, (u64)nb, false);
+      if (C->err) break;
+      for (i32 b = 0; b < nb; b++) sub_set[b] = sub[b] >= 0;
+      if (!analyze_loops(C, G, sub, sub_set)) {
+        if (C->err) break;
+        fail_struct(C, root, "irreducible control flow in handler");
+        break;
+      }
+      if (C->err) break;
+      for (i32 b = 0; b < nb; b++) covered[b] |= sub_set[b];
+      C->top = inner;
     }
-    if (!any) continue;
-    uni2[root] = 1;
-    i32* sub = compute_dominators(C, G, root, uni2);
-    u8* sub_set = (u8*)zalloc(C, (u64)G->n_blocks);
-    CKR(C, nullptr);
-    for (i32 b = 0; b < G->n_blocks; b++) sub_set[b] = sub[b] >= 0;
-    if (!analyze_loops(C, G, sub, sub_set)) {
-      CKR(C, nullptr);
-      fail_struct(C, root, "irreducible control flow in handler");
-      return nullptr;
-    }
-    CKR(C, nullptr);
-    u8* nc = (u8*)zalloc(C, (u64)G->n_blocks);
-    CKR(C, nullptr);
-    for (i32 b = 0; b < G->n_blocks; b++) nc[b] = covered[b] | sub_set[b];
-    covered = nc;
-  }
-  return G;
+  } while (0);
+  if (!C->err) C->top = mark;
+  return C->err ? nullptr : G;
 }

@@ -123,6 +123,8 @@ struct Dc {
   u8* base;
   u64 cap;
   u64 used;
+  u64 top;         // scratch stack boundary (== cap when empty); bump region is [0, used)
+  u64 low_top;     // lowest `top` seen (scratch high-water mark, for slot sizing)
   u8* sink;        // scratch returned after an overflow (zeroed), SINK_BYTES long
   // status (first failure wins)
   int err;
@@ -166,9 +168,13 @@ HD inline void copy16(void* dst, const void* src, u64 bytes) {  // both 16-align
 }
 
 // Bump allocation; zeroed unless `zero` is false (buffers written before read).
+#ifndef UPY_ALLOC_HOOK
+#define UPY_ALLOC_HOOK(bytes)
+#endif
 HD inline void* alloc_raw(Dc* C, u64 bytes, bool zero) {
   bytes = (bytes + 15) & ~(u64)15;
-  if (C->used + bytes > C->cap) {
+  UPY_ALLOC_HOOK(bytes);
+  if (C->used + bytes > C->top) {
     if (!C->err) {
       C->err = UPY_ST_ARENA_OVERFLOW;
       C->aux0 = (i64)C->used;
@@ -185,6 +191,22 @@ HD inline void* alloc_raw(Dc* C, u64 bytes, bool zero) {
 }
 HD inline void* zalloc(Dc* C, u64 bytes) { return alloc_raw(C, bytes, true); }
 HD inline void* ualloc(Dc* C, u64 bytes) { return alloc_raw(C, bytes, false); }
+
+// Scratch stack growing down from the top of the slot: temporaries of one
+// analysis phase, released together (`C->top = mark`).  Never grown in place.
+HD inline void* salloc(Dc* C, u64 bytes, bool zero = true) {
+  bytes = (bytes + 15) & ~(u64)15;
+  if (C->used + bytes > C->top) return alloc_raw(C, C->top - C->used + 16, false);  // records the overflow
+  C->top -= bytes;
+  if (C->top < C->low_top) C->low_top = C->top;
+  void* p = C->base + C->top;
+  if (zero) zero16(p, bytes);
+  return p;
+}
+template <class T>
+HD inline T* sarr(Dc* C, u64 n, bool zero = true) {
+  return (T*)salloc(C, n * sizeof(T) + 16, zero);
+}
 template <class T>
 HD inline T* anew(Dc* C) {
   return (T*)zalloc(C, sizeof(T));
@@ -201,7 +223,7 @@ HD inline Vec<T>* vnew(Dc* C, u32 cap = 0) {
   Vec<T>* v = anew<Vec<T>>(C);
   if (cap && !C->err) {
     u64 b = (u64)cap * sizeof(T);
-    if (b > SINK_BYTES && C->used + b > C->cap) {
+    if (b > SINK_BYTES && C->used + b > C->top) {
       zalloc(C, b);  // records the overflow
       return v;
     }

@@ -156,8 +156,12 @@ __device__ __forceinline__ ExtRun shfl_run(ExtRun x, int src) {
 }
 
 // One warp decodes one <=3.10 object.  Must be called by all 32 lanes.
+// tab: this version's opcode table staged in shared memory (divergent
+// __constant__ reads serialize); stage: 256 records of shared scratch per warp
+// so the chunk's records leave as coalesced 4-byte stores.
 __device__ __forceinline__ void decode_warp(const u8* __restrict__ code, u32 len, int minor,
-                                            upy_ins* __restrict__ rec, upy_decoded* res) {
+                                            upy_ins* __restrict__ rec, upy_decoded* res,
+                                            const u32* __restrict__ tab, upy_ins* stage) {
   const int lane = threadIdx.x & 31;
   if (len == 0 || (len & 1)) {
     if (lane == 0) {
@@ -197,7 +201,7 @@ __device__ __forceinline__ void decode_warp(const u8* __restrict__ code, u32 len
       u32 wd = words[q >> 1] >> (16 * (q & 1));
       ops[q] = wd & 0xFF;
       argb[q] = (wd >> 8) & 0xFF;
-      ent[q] = (u32)q < nu ? optab(minor, ops[q]) : 0;
+      ent[q] = (u32)q < nu ? tab[ops[q]] : 0;
       if ((u32)q < nu) {
         if (ops[q] == EXT_OP) ext_mask |= 1u << q;
         if (!ent[q]) unknown_mask |= 1u << q;
@@ -273,7 +277,7 @@ __device__ __forceinline__ void decode_warp(const u8* __restrict__ code, u32 len
       r.n_prefixes = (u8)(run_len > 255 ? 255 : run_len);
       r.cache_units = 0;
       r.flags = (u8)((has_arg ? 1 : 0) | (big ? 2 : 0));
-      rec[idx] = r;
+      stage[idx - n_before] = r;
       u32 kind = UPY_ENT_KIND(e);
       if (my_bad < 0 && (kind == K_JUMP_REL || kind == K_JUMP_ABS || kind == K_JUMP_BACK)) {
         bool okk;
@@ -299,6 +303,13 @@ __device__ __forceinline__ void decode_warp(const u8* __restrict__ code, u32 len
     }
     // carry into the next chunk: state after the whole chunk
     carry = ext_combine(carry, shfl_run(inc, 31));
+    __syncwarp();
+    {  // coalesced write-out of this chunk's records (3 words each)
+      const u32* src = reinterpret_cast<const u32*>(stage);
+      u32* dst = reinterpret_cast<u32*>(rec + n_before);
+      for (u32 w = lane; w < 3 * total; w += 32) dst[w] = src[w];
+    }
+    __syncwarp();
     n_before += total;
   }
   if (lane == 0) {

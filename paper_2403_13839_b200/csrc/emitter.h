@@ -647,7 +647,11 @@ HD NOINL void Emitter::expr_body(Text* t, Node* e) {
       return;
     }
     case E_NAMED:
-      name_text(t, e->a ? e->a->s : Snone());
+      if (!is_k(e->a, E_NAME)) {  // f"{e.target.id} := ..."
+        py_attr_error(C, e->a, "id");
+        return;
+      }
+      name_text(t, e->a->s);
       t_puts(C, t, " := ");
       expr(t, e->b, P_LAMBDA);
       return;

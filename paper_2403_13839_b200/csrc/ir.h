@@ -90,25 +90,32 @@ typedef Vec<Node*> NV;
 //  S_JUMP      i=target;  S_CONDJUMP a=cond, f&1 jump_when, i=target, f&2 pops_on_jump
 //  S_COMPACCUM op=kind(0 list,1 set,2 map), a=value, b=key?, i=depth
 //  S_WHILESHAPE a=cond, l1=body, l2=orelse, b=tail_cond?
+// Fields are ordered by how many kinds use them and a node is allocated with
+// only the prefix its kind touches (node_bytes), so the common expression
+// nodes take 24-72 bytes instead of the full record.  Code may only read a
+// field that its node's kind uses (the per-kind table above).
 struct Node {
   u8 k;
   u8 op;
   u8 f;       // flag bits (see above); bit7 = _loop_iter side attribute
   u8 pad;
-  i32 i, j, kk, m;
+  i32 i;
   u32 cid;
+  i32 j;
+  NV* pend;   // _pending_targets side attribute (nullptr = absent)   [all expressions]
+  Str s;
   Node* a;
   Node* b;
-  Node* c;
-  Node* p;
   NV* l1;
   NV* l2;
+  Node* c;
+  Node* p;
   NV* l3;
   NV* l4;
   Vec<Str>* sl;
   Vec<Str>* sl2;
-  Str s, s2;
-  NV* pend;   // _pending_targets side attribute (nullptr = absent)
+  Str s2;
+  i32 kk, m;
   Node* src;  // ImportFrom._source side attribute
 };
 
@@ -118,8 +125,40 @@ HD inline bool is_expr(const Node* n) { return n && n->k > N_INVALID && n->k < E
 HD inline bool is_stmt(const Node* n) { return n && n->k > X__END && n->k < S__END; }
 HD inline bool is_k(const Node* n, u8 k) { return n && n->k == k; }
 
+#define NODE_END(f) (offsetof(Node, f) + sizeof(((Node*)0)->f))
+// bytes of the Node prefix a kind uses (see the field table above)
+HD inline u32 node_bytes(u8 k) {
+  switch (k) {
+    case E_CONST: case E_STACKTEMP: case E_NULL: case E_METHSELF: case E_EXCVALUE: case E_FINSENT:
+    case E_BUILDCLASS:
+      return NODE_END(pend);
+    case E_NAME: return NODE_END(s);
+    case E_UNARY: case E_STARRED: case E_YIELD: case E_YIELDFROM: case E_FORITEM: case E_WITHEXIT:
+    case E_WITHENTER: case E_ATTR: case E_IMPORTFROM: case X_STRPART: case X_KWPAIR: case S_EXPR:
+    case S_RETURN: case S_CONDJUMP:
+      return NODE_END(a);
+    case E_BINOP: case E_SUBSCR: case E_FMTVAL: case E_NAMED: case X_WITHITEM: case S_AUGASSIGN: case S_RAISE:
+    case S_ASSERT: case S_COMPACCUM:
+      return NODE_END(b);
+    case E_BOOLOP: case E_TUPLE: case E_LIST: case E_SET: case E_FSTRING: case X_COMPFOR: case X_HANDLER:
+    case S_ASSIGN: case S_DELETE:
+      return NODE_END(l1);
+    case E_COMPARE: case E_CALL: case E_DICT: case S_IF: case S_WHILE: case S_FOR: case S_WITH:
+    case S_WHILESHAPE:
+      return NODE_END(l2);
+    case E_SLICE: case E_TERNARY: case E_COMP: return NODE_END(c);
+    case E_LAMBDA: case S_FUNCDEF: return NODE_END(p);
+    case S_TRY: case S_CLASSDEF: return NODE_END(l4);
+    case E_FUNC: case E_IMPORT: case S_GLOBAL: case S_NONLOCAL: return NODE_END(sl);
+    case X_NAMEPAIR: case S_IMPORT: return NODE_END(s2);
+    case E_UNPACKSLOT: case X_GROUP: case X_PARAMS: return NODE_END(m);
+    case S_JUMP: case S_PASS: case S_BREAK: case S_CONTINUE: return NODE_END(j);
+  }
+  return sizeof(Node);  // S_IMPORTSTAR (cid), S_IMPORTFROM (src), anything else: full record
+}
+
 HD inline Node* mk(Dc* C, u8 k) {
-  Node* n = anew<Node>(C);
+  Node* n = (Node*)zalloc(C, node_bytes(k));
   n->k = k;
   if (k == E_FUNC || k == E_BUILDCLASS) C->n_defs++;
   return n;

@@ -163,6 +163,7 @@ HD NOINL void decompile_source(Dc* C, u32 oi, const EmitOpts* opt, Text* out) {
   }
   NV* tree = root_tree(C, oi);
   CK(C);
+  t_grow(C, out, 3 * obj_at(C, oi)->code_len + 256);  // text is ~1.5-4.5x co_code
   Emitter E;
   E.C = C;
   E.out = out;

@@ -25,13 +25,18 @@ __global__ void __launch_bounds__(256) upy_decode_kernel(upy_arena A, upy_ins* _
   const int lane = threadIdx.x & 31;
   const i64 warp = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
+  __shared__ u32 tab[3][256];              // 3.8-3.10 opcode tables
+  __shared__ upy_ins stage[256 / 32][256];  // per-warp record staging (24 KB)
+  for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) tab[i >> 8][i & 255] = UPY_OPTABLE_DEV[i >> 8][i & 255];
+  __syncthreads();
+  upy_ins* my_stage = stage[threadIdx.x >> 5];
   for (i64 o = warp; o < A.n_objs; o += nwarps) {
     const upy_obj* ob = &A.objs[o];
     const u8* code = A.bytes + ob->code_off;
     upy_ins* rec = ins + (ob->code_off >> 1);
     int minor = (int)ob->minor;
     if (minor >= 8 && minor <= 10) {
-      decode_warp(code, ob->code_len, minor, rec, &dec[o]);
+      decode_warp(code, ob->code_len, minor, rec, &dec[o], tab[minor - 8], my_stage);
     } else if (lane == 0) {
       if (minor == 11) {
         decode_scalar(code, ob->code_len, minor, rec, &dec[o]);
@@ -85,6 +90,8 @@ __global__ void __launch_bounds__(128, UPY_MINB) upy_decompile_kernel(KParams P)
     C.base = base + SLOT_HEADER;
     C.cap = P.slot_bytes - SLOT_HEADER;
     C.used = 0;
+    C.top = C.cap;
+    C.low_top = C.cap;
     C.err = 0;
     C.aux0 = C.aux1 = 0;
     C.A = &P.A;
@@ -144,7 +151,8 @@ static WsLayout layout(const upy_arena* a, const upy_options* o) {
   L.ctr_off = L.dec_off + al((u64)a->n_objs * sizeof(upy_decoded));
   L.slots_off = L.ctr_off + 256;
   // C3-size objects use ~55 KB; larger ones overflow and are retried by the host with 4x
-  u64 sb = o && o->arena_bytes ? o->arena_bytes : (u64)(64u << 10) + (u64)a->max_code_len * 256u;
+  // measured peaks: C3 (400 B code) ~25 KB, C4 (19 KB code) ~2.2 MB => ~115 B per code byte
+  u64 sb = o && o->arena_bytes ? o->arena_bytes : (u64)(64u << 10) + (u64)a->max_code_len * 160u;
   sb = (sb + SLOT_HEADER + 255) & ~(u64)255;
   L.slot_bytes = sb;
   u64 slots;

@@ -280,11 +280,18 @@ def _try311(g, depth, block):
     a, r = g.a, g.r
     s, e, h, cl, end, rr = (a.fresh() for _ in range(6))
     a("NOP")
-    a.label(s); block(depth + 1, 1 + r.below(4)); a.label(e)
+    # straight-line body and handler: nested control flow inside a 3.11
+    # protected range needs CPython's range splitting, which this generator skips
+    a.label(s)
+    for _ in range(1 + r.below(4)):
+        g.simple()
+    a.label(e)
     a("JUMP_FORWARD", end)
     a.label(h); a("PUSH_EXC_INFO"); a("LOAD_GLOBAL", a.name("NameError") << 1); a("CHECK_EXC_MATCH")
     a("POP_JUMP_FORWARD_IF_FALSE", rr); a("POP_TOP")
-    block(depth + 1, 1 + r.below(3)); a("POP_EXCEPT"); a("JUMP_FORWARD", end)
+    for _ in range(1 + r.below(3)):
+        g.simple()
+    a("POP_EXCEPT"); a("JUMP_FORWARD", end)
     a.label(rr); a("RERAISE", 0)
     a.label(cl); a("COPY", 3); a("POP_EXCEPT"); a("RERAISE", 1)
     a.label(end)

@@ -34,6 +34,8 @@ extern "C" int upyh_decompile(const upy_arena* A, int header, const char* indent
     memset(&C, 0, sizeof C);
     C.base = slot.data();
     C.cap = arena_bytes;
+    C.top = arena_bytes;
+    C.low_top = arena_bytes;
     C.sink = sink.data();
     C.msg = msg.data();
     C.msg_cap = 4096;
