@@ -434,7 +434,16 @@ HD NOINL Cfg* build_basic_blocks(Dc* C, const Code* K, const Vec<ExcEntry>* entr
     CKR(C, G);
     const ExcEntry& en = entries->d[e];
     i32 target = block_at(G, en.target);
-    for (u32 b = 0; b < nu; b++) {
+    // blocks overlapping [start, end): block ends are the next block's start, so
+    // they form one contiguous id range starting at the block holding en.start
+    u32 first = 0, hi_ = nu;
+    while (first < hi_) {
+      u32 mid = (first + hi_) >> 1;
+      if (G->blocks[mid].start < en.start) first = mid + 1;
+      else hi_ = mid;
+    }
+    if (first > 0) first--;
+    for (u32 b = first; b < nu && G->blocks[b].start < en.end; b++) {
       Block& B = G->blocks[b];
       if (B.start < en.end && B.end > en.start) {
         bool has = false;
@@ -510,36 +519,119 @@ HD inline bool has_normal_edge(const Block& P, i32 to) {
   return false;
 }
 
-// compute_dominators (cfg.py:160-220); idom[b] = -1 when b has no entry.  Scratch.
-HD NOINL i32* compute_dominators(Dc* C, const Cfg* G, i32 root, const u8* universe) {
+// Scratch shared by the dominator / loop passes of one analyze() call.  Block sets
+// are (stamp array, epoch) pairs plus a member list, so each per-handler
+// sub-analysis (pipeline.py:37-53) costs O(its own blocks + edges) instead of
+// O(all blocks) -- C4-shape objects run ~100 of them over ~2K blocks.
+struct BSet {
+  const i32* st;
+  i32 ep;
+  const i32* ls;
+  i32 n;
+  HD bool has(i32 b) const { return st[b] == ep; }
+};
+
+struct AnaWs {
+  i32 nb;
+  u32 E;
+  i32 ep;
+  i32* uni_st;   // universe membership
+  i32* seen_st;  // dominator DFS seen == set(idom)
+  i32* vis_st;   // loop DFS visited
+  i32* body_st;  // natural-loop body
+  u8* onstack;   // all-zero between DFS runs
+  i32* idom;
+  i32* rpo_index;
+  i32* uni_ls;
+  i32* order;
+  i32* stk_b;
+  u32* stk_q;
+  i32* ru;
+  i32* rv;
+  i32* work;
+  i32* hdrs;
+  Vec<i32>** tails;
+  i32* blist;
+};
+
+HD inline bool ana_ws_init(Dc* C, AnaWs* W, const Cfg* G) {
   i32 nb = G->n_blocks;
-  i32* idom = sarr<i32>(C, (u64)nb, false);
-  i32* rpo_index = sarr<i32>(C, (u64)nb, false);
-  u8* seen = sarr<u8>(C, (u64)nb);
-  i32* order = sarr<i32>(C, (u64)nb, false);
-  i32* stk_b = sarr<i32>(C, (u64)nb, false);
-  u32* stk_q = sarr<u32>(C, (u64)nb, false);
-  CKR(C, idom);
-  for (i32 b = 0; b < nb; b++) idom[b] = -1;
+  W->nb = nb;
+  W->E = total_edges(G) + 1;
+  W->ep = 0;
+  W->uni_st = sarr<i32>(C, (u64)nb);
+  W->seen_st = sarr<i32>(C, (u64)nb);
+  W->vis_st = sarr<i32>(C, (u64)nb);
+  W->body_st = sarr<i32>(C, (u64)nb);
+  W->onstack = sarr<u8>(C, (u64)nb);
+  W->idom = sarr<i32>(C, (u64)nb, false);
+  W->rpo_index = sarr<i32>(C, (u64)nb, false);
+  W->uni_ls = sarr<i32>(C, (u64)nb, false);
+  W->order = sarr<i32>(C, (u64)nb, false);
+  W->stk_b = sarr<i32>(C, (u64)nb, false);
+  W->stk_q = sarr<u32>(C, (u64)nb, false);
+  W->ru = sarr<i32>(C, W->E, false);
+  W->rv = sarr<i32>(C, W->E, false);
+  W->work = sarr<i32>(C, (u64)W->E + nb, false);
+  W->hdrs = sarr<i32>(C, (u64)nb + 1, false);
+  W->tails = sarr<Vec<i32>*>(C, (u64)nb + 1, false);
+  W->blist = sarr<i32>(C, (u64)nb + 1, false);
+  CKR(C, false);
+  for (i32 b = 0; b < nb; b++) W->idom[b] = -1;
+  return true;
+}
+
+// reachable_from(root, include_exc=False) (cfg.py:144-157) into W's universe, not
+// entering blocks in `stop` (analyze() passes the covered set, which is closed
+// under normal successors, so stopping there removes exactly the covered blocks
+// the reference filters out afterwards)
+HD inline BSet collect_reach(AnaWs* W, const Cfg* G, i32 root, const u8* stop) {
+  i32 ep = ++W->ep;
+  i32 n = 0;
+  u32 sp = 0;
+  W->work[sp++] = root;
+  while (sp) {
+    i32 b = W->work[--sp];
+    if (W->uni_st[b] == ep) continue;
+    W->uni_st[b] = ep;
+    W->uni_ls[n++] = b;
+    const Block& B = G->blocks[b];
+    for (u32 q = 0; q < B.succ->n; q++) {
+      i32 s = B.succ->d[q];
+      if (B.succ_kind->d[q] == EK_EXC || W->uni_st[s] == ep || (stop && stop[s])) continue;
+      W->work[sp++] = s;
+    }
+  }
+  return BSet{W->uni_st, ep, W->uni_ls, n};
+}
+
+// compute_dominators (cfg.py:160-220) over universe U; W->idom[b] = -1 when b has
+// no entry.  Returns set(idom) (the blocks the DFS reached, in postorder).
+HD NOINL BSet compute_dominators(Dc* C, AnaWs* W, const Cfg* G, i32 root, BSet U) {
+  i32* idom = W->idom;
+  i32* rpo_index = W->rpo_index;
+  i32* order = W->order;
+  for (i32 i = 0; i < U.n; i++) idom[U.ls[i]] = -1;
+  i32 ep = ++W->ep;
   // iterative DFS mirroring the recursive one (postorder)
   i32 no = 0, sp = 0;
-  seen[root] = 1;
-  stk_b[sp] = root;
-  stk_q[sp] = 0;
+  W->seen_st[root] = ep;
+  W->stk_b[sp] = root;
+  W->stk_q[sp] = 0;
   sp++;
   while (sp) {
-    i32 b = stk_b[sp - 1];
+    i32 b = W->stk_b[sp - 1];
     const Block& B = G->blocks[b];
-    u32& q = stk_q[sp - 1];
+    u32& q = W->stk_q[sp - 1];
     bool pushed = false;
     while (q < B.succ->n) {
       i32 s = B.succ->d[q];
       u8 k = B.succ_kind->d[q];
       q++;
-      if (k != EK_EXC && universe[s] && !seen[s]) {
-        seen[s] = 1;
-        stk_b[sp] = s;
-        stk_q[sp] = 0;
+      if (k != EK_EXC && U.has(s) && W->seen_st[s] != ep) {
+        W->seen_st[s] = ep;
+        W->stk_b[sp] = s;
+        W->stk_q[sp] = 0;
         sp++;
         pushed = true;
         break;
@@ -563,7 +655,7 @@ HD NOINL i32* compute_dominators(Dc* C, const Cfg* G, i32 root, const u8* univer
       i32 nw = -1;
       for (u32 q = 0; q < B.pred->n; q++) {
         i32 p = B.pred->d[q];
-        if (idom[p] < 0 || !universe[p] || !has_normal_edge(G->blocks[p], b)) continue;
+        if (!U.has(p) || idom[p] < 0 || !has_normal_edge(G->blocks[p], b)) continue;
         if (nw < 0) {
           nw = p;
           continue;
@@ -582,7 +674,7 @@ HD NOINL i32* compute_dominators(Dc* C, const Cfg* G, i32 root, const u8* univer
       }
     }
   }
-  return idom;
+  return BSet{W->seen_st, ep, order, no};
 }
 
 HD inline bool dominates(const i32* idom, i32 a, i32 b) {  // cfg.py:223-231
@@ -594,38 +686,34 @@ HD inline bool dominates(const i32* idom, i32 a, i32 b) {  // cfg.py:223-231
   }
 }
 
-// analyze_loops (cfg.py:241-313); appends loops whose header is new to G->loops
-// (persistent), everything else on the scratch stack.  Returns false when irreducible.
-HD NOINL bool analyze_loops(Dc* C, Cfg* G, const i32* idom, const u8* universe) {
-  i32 nb = G->n_blocks;
+// analyze_loops (cfg.py:241-313) over universe U with dominator tree W->idom;
+// appends loops whose header is new to G->loops (persistent).  Returns false when
+// irreducible.
+HD NOINL bool analyze_loops(Dc* C, AnaWs* W, Cfg* G, BSet U) {
+  const i32* idom = W->idom;
   // roots: universe blocks with no predecessor in the universe (any edge kind)
   i32 root = -1;
   i32 first_root = -1, min_u = -1;
-  for (i32 b = 0; b < nb; b++) {
-    if (!universe[b]) continue;
-    if (min_u < 0) min_u = b;
+  for (i32 i = 0; i < U.n; i++) {
+    i32 b = U.ls[i];
+    if (min_u < 0 || b < min_u) min_u = b;
     bool has = false;
     const Block& B = G->blocks[b];
-    for (u32 q = 0; q < B.pred->n && !has; q++) has = universe[B.pred->d[q]] != 0;
-    if (!has && first_root < 0) first_root = b;
+    for (u32 q = 0; q < B.pred->n && !has; q++) has = U.has(B.pred->d[q]);
+    if (!has && (first_root < 0 || b < first_root)) first_root = b;
   }
   // roots has at most one element (every other universe block was reached from
   // the dominator root through a predecessor in the universe), so its order is moot
   if (first_root >= 0) root = first_root;
-  else root = universe[G->entry] ? G->entry : min_u;
+  else root = U.has(G->entry) ? G->entry : min_u;
   if (root < 0) return true;
-  u32 E = total_edges(G) + 1;
-  u8* visited = sarr<u8>(C, (u64)nb);
-  u8* onstack = sarr<u8>(C, (u64)nb);
-  i32* stk_b = sarr<i32>(C, (u64)nb, false);
-  u32* stk_q = sarr<u32>(C, (u64)nb, false);
-  i32* ru = sarr<i32>(C, E, false);
-  i32* rv = sarr<i32>(C, E, false);
-  CKR(C, true);
+  i32 vep = ++W->ep;
+  i32* stk_b = W->stk_b;
+  u32* stk_q = W->stk_q;
   u32 nr = 0;
   i32 sp = 0;
-  visited[root] = 1;
-  onstack[root] = 1;
+  W->vis_st[root] = vep;
+  W->onstack[root] = 1;
   stk_b[0] = root;
   stk_q[0] = 0;
   sp = 1;
@@ -638,76 +726,72 @@ HD NOINL bool analyze_loops(Dc* C, Cfg* G, const i32* idom, const u8* universe) 
       i32 v = B.succ->d[q];
       u8 k = B.succ_kind->d[q];
       q++;
-      if (k == EK_EXC || !universe[v]) continue;
-      if (!visited[v]) {
-        visited[v] = 1;
-        onstack[v] = 1;
+      if (k == EK_EXC || !U.has(v)) continue;
+      if (W->vis_st[v] != vep) {
+        W->vis_st[v] = vep;
+        W->onstack[v] = 1;
         stk_b[sp] = v;
         stk_q[sp] = 0;
         sp++;
         pushed = true;
         break;
-      } else if (onstack[v]) {
-        ru[nr] = u;
-        rv[nr] = v;
+      } else if (W->onstack[v]) {
+        W->ru[nr] = u;
+        W->rv[nr] = v;
         nr++;
       }
     }
     if (!pushed) {
-      onstack[u] = 0;
+      W->onstack[u] = 0;
       sp--;
     }
   }
   bool reducible = true;
   // back edges grouped by header in first-seen order; tails are persistent
-  i32* hdrs = sarr<i32>(C, (u64)nb + 1, false);
-  Vec<i32>** tails = sarr<Vec<i32>*>(C, (u64)nb + 1, false);
-  CKR(C, true);
   u32 nh = 0;
   for (u32 e = 0; e < nr; e++) {
-    i32 u = ru[e], v = rv[e];
+    i32 u = W->ru[e], v = W->rv[e];
     if (dominates(idom, v, u)) {
       u32 h = 0;
-      while (h < nh && hdrs[h] != v) h++;
+      while (h < nh && W->hdrs[h] != v) h++;
       if (h == nh) {
-        hdrs[nh] = v;
-        tails[nh] = vnew<i32>(C, 2);
+        W->hdrs[nh] = v;
+        W->tails[nh] = vnew<i32>(C, 2);
         nh++;
       }
       CKR(C, true);
-      vpush(C, tails[h], u);
+      vpush(C, W->tails[h], u);
     } else {
       reducible = false;
     }
   }
-  u8* body = sarr<u8>(C, (u64)nb, false);
-  i32* work = sarr<i32>(C, E + nb, false);
   CKR(C, reducible);
   for (u32 h = 0; h < nh && !C->err; h++) {
-    i32 header = hdrs[h];
-    for (i32 b = 0; b < nb; b++) body[b] = 0;
-    u32 wn = 0;
-    body[header] = 1;
-    for (u32 t = 0; t < tails[h]->n; t++) work[wn++] = tails[h]->d[t];
+    i32 header = W->hdrs[h];
+    if (G->loop_of_header[header] >= 0) continue;  // only new headers are added
+    i32 bep = ++W->ep;
+    u32 wn = 0, cnt = 0;
+    W->body_st[header] = bep;
+    W->blist[cnt++] = header;
+    for (u32 t = 0; t < W->tails[h]->n; t++) W->work[wn++] = W->tails[h]->d[t];
     while (wn) {
-      i32 nn = work[--wn];
-      if (body[nn]) continue;
-      body[nn] = 1;
+      i32 nn = W->work[--wn];
+      if (W->body_st[nn] == bep) continue;
+      W->body_st[nn] = bep;
+      W->blist[cnt++] = nn;
       const Block& N = G->blocks[nn];
       for (u32 q = 0; q < N.pred->n; q++) {
         i32 p = N.pred->d[q];
-        if (universe[p] && has_normal_edge(G->blocks[p], nn)) work[wn++] = p;
+        if (U.has(p) && has_normal_edge(G->blocks[p], nn)) W->work[wn++] = p;
       }
     }
-    if (G->loop_of_header[header] >= 0) continue;  // only new headers are added
+    sort_u32((u32*)W->blist, (i32)cnt);  // body in block-id order, as the reference's
     Loop L;
     L.header = header;
-    u32 cnt = 0;
-    for (i32 b = 0; b < nb; b++) cnt += body[b];
     L.body = vnew<i32>(C, cnt);
-    for (i32 b = 0; b < nb; b++)
-      if (body[b]) vpush(C, L.body, b);
-    L.back_tails = tails[h];
+    CKR(C, reducible);
+    for (u32 i = 0; i < cnt; i++) vpush(C, L.body, W->blist[i]);
+    L.back_tails = W->tails[h];
     G->loop_of_header[header] = (i32)G->loops->n;
     vpush(C, G->loops, L);
   }
@@ -753,12 +837,14 @@ HD NOINL Cfg* analyze(Dc* C, Code* K) {
     G->loop_of_header = (i32*)ualloc(C, (u64)nb * sizeof(i32));
     if (C->err) break;
     for (i32 b = 0; b < nb; b++) G->loop_of_header[b] = -1;
-    u8* uni = reachable_from(C, G, G->entry, false);
-    i32* idom = compute_dominators(C, G, G->entry, uni);
+    AnaWs W;
     u8* covered = sarr<u8>(C, (u64)nb);  // universe of analyze_loops = set(idom), then grows
+    if (!ana_ws_init(C, &W, G)) break;
+    BSet uni = collect_reach(&W, G, G->entry, nullptr);
+    BSet dom = compute_dominators(C, &W, G, G->entry, uni);
     if (C->err) break;
-    for (i32 b = 0; b < nb; b++) covered[b] = idom[b] >= 0;
-    if (!analyze_loops(C, G, idom, covered)) {
+    for (i32 i = 0; i < dom.n; i++) covered[dom.ls[i]] = 1;
+    if (!analyze_loops(C, &W, G, dom)) {
       if (C->err) break;
       fail_struct(C, G->entry, "irreducible control flow");
       break;
@@ -767,32 +853,17 @@ HD NOINL Cfg* analyze(Dc* C, Code* K) {
     for (u32 e = 0; e < entries->n && !C->err; e++) {
       i32 root = block_at(G, entries->d[e].target);
       if (root < 0 || covered[root]) continue;
-      u64 inner = C->top;  // per-handler temporaries
-      u8* reach = reachable_from(C, G, root, false);
-      u8* uni2 = sarr<u8>(C, (u64)nb, false);
+      // universe = reachable(root) - covered, plus root (never empty: root is in it)
+      BSet uni2 = collect_reach(&W, G, root, covered);
+      BSet sub = compute_dominators(C, &W, G, root, uni2);
       if (C->err) break;
-      bool any = false;
-      for (i32 b = 0; b < nb; b++) {
-        uni2[b] = reach[b] && !covered[b];
-        any |= uni2[b] != 0;
-      }
-      if (!any) {
-        C->top = inner;
-        continue;
-      }
-      uni2[root] = 1;
-      i32* sub = compute_dominators(C, G, root, uni2);
-      u8* sub_set = sarr<u8>(C, (u64)nb, false);
-      if (C->err) break;
-      for (i32 b = 0; b < nb; b++) sub_set[b] = sub[b] >= 0;
-      if (!analyze_loops(C, G, sub, sub_set)) {
+      if (!analyze_loops(C, &W, G, sub)) {
         if (C->err) break;
         fail_struct(C, root, "irreducible control flow in handler");
         break;
       }
       if (C->err) break;
-      for (i32 b = 0; b < nb; b++) covered[b] |= sub_set[b];
-      C->top = inner;
+      for (i32 i = 0; i < sub.n; i++) covered[sub.ls[i]] = 1;
     }
   } while (0);
   if (!C->err) C->top = mark;

@@ -243,6 +243,12 @@ struct Structurer {
   Vec<i32>* active_regions;
   u8* active_loops;    // per block id
   u32 end_offset;
+  // _lexical_exits index: non-SETUP jumps in offset order, targets, and the max
+  // target of each run of 32 (built on first use; C3-shape objects never need it)
+  i32 nj;
+  u32* joff;
+  u32* jtgt;
+  u32* jblk;
 
   HD i64 new_temp() { return temp_counter++; }
 
@@ -262,26 +268,63 @@ struct Structurer {
     }
     return sim.simulate(b, stack);
   }
+  // first index in rbs_idx (sorted by start, then -end) whose region starts at pos, or n
+  HD u32 regions_at(i64 pos) {
+    u32 lo = 0, hi = rbs_idx->n;
+    while (lo < hi) {
+      u32 mid = (lo + hi) >> 1;
+      if ((i64)regions->d[rbs_idx->d[mid]].start < pos) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo;
+  }
   HD bool region_starts_at(i64 pos) {
-    for (u32 q = 0; q < rbs_idx->n; q++)
-      if ((i64)regions->d[rbs_idx->d[q]].start == pos) return true;
-    return false;
+    u32 q = regions_at(pos);
+    return q < rbs_idx->n && (i64)regions->d[rbs_idx->d[q]].start == pos;
   }
   HD bool region_active(i32 r) {
     for (u32 q = 0; q < active_regions->n; q++)
       if (active_regions->d[q] == r) return true;
     return false;
   }
-  HD i64 lexical_exit_max(i64 lo, i64 hi) {  // max of _lexical_exits (structurer.py:331-339), -1 if none
-    i64 best = -1;
-    for (i32 i = 0; i < K->n_ins; i++) {
-      const Ins& in = K->ins[i];
-      if ((i64)in.offset >= lo && (i64)in.offset < hi && ins_is_jump(in) && !is_setup_op(in.op)) {
-        i64 t = jump_target(K, in);
-        if (t >= hi && t > best) best = t;
+  // max(_lexical_exits(lo, hi)) (structurer.py:331-339), -1 if empty.  The exits are
+  // the targets >= hi of jumps in [lo, hi), so the answer is the range max of targets
+  // when that max is >= hi: answered from 32-wide block maxima instead of a full scan.
+  HD i64 lexical_exit_max(i64 lo, i64 hi) {
+    if (!joff) {
+      i32 n = 0;
+      for (i32 i = 0; i < K->n_ins; i++)
+        if (ins_is_jump(K->ins[i]) && !is_setup_op(K->ins[i].op)) n++;
+      joff = (u32*)ualloc(C, (u64)n * 4 + 4);
+      jtgt = (u32*)ualloc(C, (u64)n * 4 + 4);
+      jblk = (u32*)zalloc(C, (u64)(n / 32 + 1) * 4);
+      CKR(C, -1);
+      nj = 0;
+      for (i32 i = 0; i < K->n_ins; i++) {
+        const Ins& in = K->ins[i];
+        if (!ins_is_jump(in) || is_setup_op(in.op)) continue;
+        joff[nj] = in.offset;
+        jtgt[nj] = jump_target(K, in);
+        if (jtgt[nj] > jblk[nj >> 5]) jblk[nj >> 5] = jtgt[nj];
+        nj++;
       }
     }
-    return best;
+    auto lb = [&](i64 v) {
+      i32 a = 0, b = nj;
+      while (a < b) {
+        i32 mid = (a + b) >> 1;
+        if ((i64)joff[mid] < v) a = mid + 1;
+        else b = mid;
+      }
+      return a;
+    };
+    i32 i0 = lb(lo), i1 = lb(hi);
+    i64 m = -1;
+    i32 i = i0;
+    while (i < i1 && (i & 31)) m = (i64)jtgt[i] > m ? (i64)jtgt[i] : m, i++;
+    while (i + 32 <= i1) m = (i64)jblk[i >> 5] > m ? (i64)jblk[i >> 5] : m, i += 32;
+    while (i < i1) m = (i64)jtgt[i] > m ? (i64)jtgt[i] : m, i++;
+    return m >= hi ? m : -1;
   }
   HD WCtx* ctx_new(i64 c0, i64 c1, i64 brk) {
     WCtx* c = anew<WCtx>(C);
@@ -367,9 +410,10 @@ HD NOINL NV* Structurer::walk(Segs segs, NV* stack, const WCtx* ctx, WalkExit* e
     }
     // first region starting here that is not active (outermost first)
     i32 region = -1;
-    for (u32 q = 0; q < rbs_idx->n && region < 0; q++) {
+    for (u32 q = regions_at(pos); q < rbs_idx->n && region < 0; q++) {
       i32 r = rbs_idx->d[q];
-      if ((i64)regions->d[r].start == pos && !region_active(r)) region = r;
+      if ((i64)regions->d[r].start != pos) break;
+      if (!region_active(r)) region = r;
     }
     if (region >= 0) {
       pos = structure_region(region, out, &stack, ctx);
