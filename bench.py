@@ -206,6 +206,7 @@ def main():
     ap.add_argument("--arena-bytes", type=int, default=0)
     ap.add_argument("--tpb", type=int, default=0)
     ap.add_argument("--verify-stride", type=int, default=0, help="check every k-th output (0: 1, c5: 16)")
+    ap.add_argument("--pyc", type=int, default=1, help="also time the .pyc-bytes end-to-end path (0: skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -288,6 +289,12 @@ def main():
     barrier()
     e2e_ms = e0.elapsed_time(e1)
 
+    # ---------------- end to end from .pyc files in host memory:
+    # native loader (all host threads) -> H2D -> kernels -> D2H, wall clock
+    pyc = None
+    if args.pyc and args.workload in ("c3", "c3_311", "c5"):
+        pyc = pyc_e2e(pool, reps, local, args, pool_name, n_pool, barrier)
+
     # ---------------- max over ranks
     times = torch.tensor([total_ms, e2e_ms, sum(dec_ms), sum(st_ms)], dtype=torch.float64, device="cuda")
     if dist is not None:
@@ -356,12 +363,55 @@ def main():
                             "algorithmic_bytes_per_launch": alg_dec},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "objects/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e_pyc": pyc,
         "gpu_launches": 2 * args.steps + 2 * args.steps,
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def pyc_e2e(pool, reps, local, args, pool_name, n_pool, barrier):
+    """decompile_pyc path timed end to end: .pyc images back to back in host memory
+    -> upy_pyc_load (C++, all host threads) -> pinned H2D -> decode + decompile
+    kernels -> D2H of statuses and text.  Wall clock per step (host work is part
+    of it), outputs checked against the reference digests."""
+    import torch
+
+    from paper_2403_13839_b200.api import DeviceArena
+    from paper_2403_13839_b200.loader import load_pyc_buffer
+    from paper_2403_13839_b200.synth import marshal
+
+    blobs = [marshal.dump_pyc(co) for co in pool]
+    one = b"".join(blobs)
+    sizes = np.array([len(b) for b in blobs] * reps, dtype=np.uint64)
+    offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.uint64)
+    buf = np.frombuffer(one * reps, dtype=np.uint8)
+    n = len(sizes)
+    t_load, t_all = [], []
+    res = None
+    for k in range(1 + args.steps):  # first step is warm-up
+        barrier()
+        t0 = time.perf_counter()
+        arena, per_file = load_pyc_buffer(buf, offs, sizes)
+        t1 = time.perf_counter()
+        da = DeviceArena(arena, device=f"cuda:{local}")
+        da.upload()
+        da.run()
+        res = da.fetch()
+        barrier()
+        t2 = time.perf_counter()
+        if k:
+            t_load.append(t1 - t0)
+            t_all.append(t2 - t0)
+        del da, arena
+    n_checked, n_bad = verify(res, pool_name, n_pool, 1)
+    step = sum(t_all) / len(t_all)
+    return {"value": n / step, "unit": "objects/s", "files_per_step": n, "pyc_bytes_per_step": int(len(buf)),
+            "load_ms": 1000 * sum(t_load) / len(t_load), "step_ms": 1000 * step,
+            "loader_threads": os.cpu_count(), "parity": {"checked": n_checked, "mismatches": n_bad},
+            "timing": "wall clock, synchronized, mean of --steps after 1 warm-up"}
 
 
 def _count_instructions(arena):

@@ -3,18 +3,20 @@
 Drop-in for the reference's hot path `unpyre.decompile_source(code, style)`
 (/root/reference/pkg/src/unpyre/pipeline.py:143-160): `decompile` has the same
 signature, text and exception classes; `decompile_many` batches any number of
-code objects into one device arena.
+code objects into one device arena.  `load_pyc` / `decompile_pyc_many` read
+.pyc images natively (pyc.py:36-352) straight into that arena.
 """
-from .errors import (BadJumpTarget, InternalMarkerLeak, MalformedExceptionTable, StackDepthMismatch,
-                     StackUnderflow, StructuringFailed, TruncatedCode, UnknownOpcode, UnpyreError,
-                     UnsupportedOpcode, UnsupportedVersion)
+from .errors import (BadJumpTarget, InternalMarkerLeak, MalformedExceptionTable, MalformedMarshal,
+                     StackDepthMismatch, StackUnderflow, StructuringFailed, TruncatedCode, TruncatedHeader,
+                     UnknownMagic, UnknownOpcode, UnpyreError, UnsupportedOpcode, UnsupportedVersion)
 from .model import CodeObject, Const, EmitStyle, VersionTag, flatten_nested_codes
 
 __all__ = [
     "BadJumpTarget", "CodeObject", "Const", "EmitStyle", "InternalMarkerLeak", "MalformedExceptionTable",
-    "StackDepthMismatch", "StackUnderflow", "StructuringFailed", "TruncatedCode", "UnknownOpcode",
-    "UnpyreError", "UnsupportedOpcode", "UnsupportedVersion", "VersionTag", "decompile", "decompile_many",
-    "decompile_source", "flatten_nested_codes",
+    "MalformedMarshal", "StackDepthMismatch", "StackUnderflow", "StructuringFailed", "TruncatedCode",
+    "TruncatedHeader", "UnknownMagic", "UnknownOpcode", "UnpyreError", "UnsupportedOpcode",
+    "UnsupportedVersion", "VersionTag", "decompile", "decompile_many", "decompile_source",
+    "decompile_pyc_many", "flatten_nested_codes", "load_pyc", "load_pyc_batch",
 ]
 __version__ = "0.1.0"
 
@@ -26,4 +28,8 @@ def __getattr__(name):
         from . import api
 
         return getattr(api, name)
+    if name in ("load_pyc", "load_pyc_batch", "decompile_pyc_many"):
+        from . import loader
+
+        return getattr(loader, name)
     raise AttributeError(name)

@@ -45,12 +45,27 @@ class UpyOut(C.Structure):
     ]
 
 
+class UpyPycBatch(C.Structure):
+    _fields_ = [
+        ("image", C.c_void_p), ("image_bytes", C.c_uint64),
+        ("section_off", C.c_uint64 * 7), ("section_count", C.c_int64 * 7),
+        ("max_code_len", C.c_uint64), ("total_code_units", C.c_uint64),
+        ("n_files", C.c_int64),
+        ("file_status", C.POINTER(C.c_int32)),
+        ("file_root", C.POINTER(C.c_int32)),
+        ("file_aux", C.POINTER(C.c_int64)),
+        ("messages", C.c_void_p),
+        ("msg_off", C.POINTER(C.c_uint64)),
+        ("msg_len", C.POINTER(C.c_uint32)),
+    ]
+
+
 SIZES = {0: 152, 1: 40, 2: 16, 3: C.sizeof(UpyArena), 4: C.sizeof(UpyOptions), 5: C.sizeof(UpyOut),
          6: 12, 7: 24}
 
 # symbols declared by include/upy.h
 EXPORTS = ("upy_abi_sizeof", "upy_abi_version", "upy_query_workspace", "upy_decompile_batch",
-           "upy_decode_batch", "upy_last_error")
+           "upy_decode_batch", "upy_last_error", "upy_pyc_load", "upy_pyc_free")
 
 
 def arena_struct(arena, base_ptr: int) -> UpyArena:

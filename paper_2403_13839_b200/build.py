@@ -2,13 +2,19 @@
 
     python -m paper_2403_13839_b200.build [--force]
 
-libupy_cuda.so is compiled with nvcc for sm_100a only.  The decompile kernel
-is one large, recursive, divergent function: full ptxas -O3 on it takes >10
-minutes for little gain on pointer-chasing code, so ptxas runs at -O2 (cicc
-stays at -O3).  See DESIGN.md "Build".
+libupy_cuda.so is linked from two nvcc objects compiled for sm_100a only:
+
+* ``decode_kernel.o`` -- the HBM-bound decode kernel, full -O3;
+* ``upy.o`` -- the decompile kernel and the C ABI.  The decompile kernel is one
+  large, recursive, divergent function: ptxas -O3 on it takes >10 minutes for
+  less speed than -O1 (measured below), so ptxas runs at -O1 there.
+
+Each object is content-addressed (a stamp holds the digest of its sources and
+flags), so tuning the decode kernel does not rebuild the decompile kernel.
 """
 from __future__ import annotations
 
+import hashlib
 import os
 import subprocess
 import sys
@@ -16,15 +22,34 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
+OBJDIR = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libupy_cuda.so")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # Measured on B200 (C3, 1M objects): cicc -O3 / ptxas -O1  2.75M obj/s (build ~5 min)
 #                                    cicc -O3 / ptxas -O3  2.55M obj/s (build ~6 min)
 #                                    cicc -O1 / ptxas -O1  1.67M obj/s (build ~30 s)
 # UPY_FAST_BUILD=1 selects the last one for edit-compile-test loops.
 CICC_OPT = "-O1" if os.environ.get("UPY_FAST_BUILD") else "-O3"
-NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-Xcicc", CICC_OPT, "-Xptxas", "-O1",
-              "-diag-suppress", "550"]
+COMMON = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-diag-suppress", "550"]
+BASE_DEPS = ["../../include/upy.h", "common.h", "optables.h", "unicode_tables.h"]
+OBJECTS = {
+    "decode_kernel": {"src": "decode_kernel.cu", "deps": BASE_DEPS + ["decode.h"],
+                      "flags": COMMON + ["-Xptxas", "-O3"]},
+    "pyc_loader": {"src": "pyc_loader.cpp", "deps": None, "flags": COMMON},
+    "upy": {"src": "upy.cu", "deps": None,  # every header
+            "flags": COMMON + ["-Xcicc", CICC_OPT, "-Xptxas", "-O1"]},
+}
+LINK_FLAGS = [*ARCH, "-shared", "-Xcompiler", "-fPIC"]
+NVCC_FLAGS = OBJECTS["upy"]["flags"]  # kept for tools that print the main flags
+
+
+def _obj_deps(spec):
+    if spec["deps"] is None:
+        deps = [os.path.join(ROOT, "include", "upy.h")]
+        deps += [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith(".h")]
+    else:
+        deps = [os.path.normpath(os.path.join(CSRC, d)) for d in spec["deps"]]
+    return deps + [os.path.join(CSRC, spec["src"])]
 
 
 def _deps():
@@ -34,8 +59,6 @@ def _deps():
 
 
 def _digest(deps, flags):
-    import hashlib
-
     h = hashlib.sha256(" ".join(flags).encode())
     for d in deps:
         with open(d, "rb") as f:
@@ -44,8 +67,8 @@ def _digest(deps, flags):
 
 
 def up_to_date(target, deps, flags=()):
-    """Content-addressed: a stamp next to the library records the digest of
-    the sources and flags it was built from (mtimes do not survive copies)."""
+    """Content-addressed: a stamp next to the target records the digest of the
+    sources and flags it was built from (mtimes do not survive copies)."""
     stamp = target + ".stamp"
     if not os.path.exists(target) or not os.path.exists(stamp):
         return False
@@ -53,19 +76,39 @@ def up_to_date(target, deps, flags=()):
         return f.read().strip() == _digest(deps, flags)
 
 
-def build_cuda(force=False, verbose=True):
-    deps = _deps()
-    if not force and up_to_date(LIB, deps, NVCC_FLAGS):
-        return LIB
-    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB + ".tmp", os.path.join(CSRC, "upy.cu")]
+def _run(cmd, verbose):
     if verbose:
         print("[build]", " ".join(cmd), flush=True)
-    digest = _digest(deps, NVCC_FLAGS)  # of the sources as they were when compilation started
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    with open(LIB + ".stamp", "w") as f:
+
+
+def _stamp(target, digest):
+    with open(target + ".stamp", "w") as f:
         f.write(digest)
+
+
+def build_cuda(force=False, verbose=True):
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    os.makedirs(OBJDIR, exist_ok=True)
+    objs, link_digest = [], hashlib.sha256(" ".join(LINK_FLAGS).encode())
+    for name, spec in OBJECTS.items():
+        obj = os.path.join(OBJDIR, name + ".o")
+        deps, flags = _obj_deps(spec), spec["flags"]
+        digest = _digest(deps, flags)  # of the sources as they were when compilation started
+        if force or not up_to_date(obj, deps, flags):
+            _run([nvcc, *flags, "-c", "-o", obj + ".tmp", os.path.join(CSRC, spec["src"])], verbose)
+            os.replace(obj + ".tmp", obj)
+            _stamp(obj, digest)
+        objs.append(obj)
+        link_digest.update(digest.encode())
+    link_digest = link_digest.hexdigest()
+    if not force and os.path.exists(LIB) and os.path.exists(LIB + ".stamp"):
+        with open(LIB + ".stamp") as f:
+            if f.read().strip() == link_digest:
+                return LIB
+    _run([nvcc, *LINK_FLAGS, "-o", LIB + ".tmp", *objs], verbose)
+    os.replace(LIB + ".tmp", LIB)
+    _stamp(LIB, link_digest)
     return LIB
 
 

@@ -17,10 +17,12 @@
 #define HD __host__ __device__
 #define DI __device__ __forceinline__
 #define NOINL __noinline__
+#define FORCEINL __forceinline__
 #else
 #define HD
 #define DI inline
 #define NOINL __attribute__((noinline))
+#define FORCEINL inline __attribute__((always_inline))
 #endif
 
 typedef uint8_t u8;
@@ -304,6 +306,16 @@ HD inline void t_put(Dc* C, Text* t, char ch) {
 }
 HD inline void t_puts(Dc* C, Text* t, const char* s) { t_putn(C, t, s, (u32)cstrlen(s)); }
 HD inline void t_str(Dc* C, Text* t, Str s) { t_putn(C, t, s.p, s.n); }
+HD inline void t_u32(Dc* C, Text* t, u32 v) {
+  char buf[10];
+  int k = 0;
+  do {
+    buf[k++] = (char)('0' + (v % 10));
+    v /= 10;
+  } while (v);
+  if (!t_grow(C, t, t->n + (u32)k)) return;
+  while (k) t->d[t->n++] = buf[--k];
+}
 HD inline void t_i64(Dc* C, Text* t, i64 v) {
   char buf[24];
   int k = 0;

@@ -161,7 +161,7 @@ __device__ __forceinline__ ExtRun shfl_run(ExtRun x, int src) {
 // so the chunk's records leave as coalesced 4-byte stores.
 __device__ __forceinline__ void decode_warp(const u8* __restrict__ code, u32 len, int minor,
                                             upy_ins* __restrict__ rec, upy_decoded* res,
-                                            const u32* __restrict__ tab, upy_ins* stage) {
+                                            const u32* __restrict__ tab, upy_ins* stage, uint4 first) {
   const int lane = threadIdx.x & 31;
   if (len == 0 || (len & 1)) {
     if (lane == 0) {
@@ -180,30 +180,25 @@ __device__ __forceinline__ void decode_warp(const u8* __restrict__ code, u32 len
   for (u32 base = 0; base < units; base += 256) {
     // 128-bit load: lane owns units [base + 8*lane, +8)
     u32 u0 = base + 8 * lane;
-    uint4 w = make_uint4(0, 0, 0, 0);
+    // (code is 16-B aligned and readable to the next 16-B boundary, upy.h; bytes
+    // past the end are never interpreted: every use is guarded by q < nu)
+    uint4 w = first;
     u32 nu = 0;
     if (u0 < units) {
       nu = units - u0 < 8 ? units - u0 : 8;
-      if (nu == 8) {
-        w = *reinterpret_cast<const uint4*>(code + 2 * u0);
-      } else {
-        u32 tmp[4] = {0, 0, 0, 0};
-        for (u32 q = 0; q < 2 * nu; q++) tmp[q >> 2] |= (u32)code[2 * u0 + q] << (8 * (q & 3));
-        w = make_uint4(tmp[0], tmp[1], tmp[2], tmp[3]);
-      }
+      if (base) w = *reinterpret_cast<const uint4*>(code + 2 * u0);
     }
-    u32 words[4] = {w.x, w.y, w.z, w.w};
-    // per-unit opcode/arg bytes and table entries
-    u32 ops[8], argb[8], ent[8];
+    const u32 words[4] = {w.x, w.y, w.z, w.w};
+#define UNIT_OP(q) ((words[(q) >> 1] >> (16 * ((q) & 1))) & 0xFFu)
+#define UNIT_ARG(q) ((words[(q) >> 1] >> (16 * ((q) & 1) + 8)) & 0xFFu)
+    // per-unit table entries
+    u32 ent[8];
     u32 ext_mask = 0, unknown_mask = 0;
 #pragma unroll
     for (int q = 0; q < 8; q++) {
-      u32 wd = words[q >> 1] >> (16 * (q & 1));
-      ops[q] = wd & 0xFF;
-      argb[q] = (wd >> 8) & 0xFF;
-      ent[q] = (u32)q < nu ? tab[ops[q]] : 0;
+      ent[q] = (u32)q < nu ? tab[UNIT_OP(q)] : 0;
       if ((u32)q < nu) {
-        if (ops[q] == EXT_OP) ext_mask |= 1u << q;
+        if (UNIT_OP(q) == EXT_OP) ext_mask |= 1u << q;
         if (!ent[q]) unknown_mask |= 1u << q;
       }
     }
@@ -215,83 +210,131 @@ __device__ __forceinline__ void decode_warp(const u8* __restrict__ code, u32 len
         int q = __ffs(unknown_mask) - 1;
         res->status = UPY_ST_UNKNOWN_OPCODE;
         res->n_instrs = 0;
-        res->aux0 = ops[q];
+        res->aux0 = UNIT_OP(q);
         res->aux1 = 2 * (u0 + q);
       }
       return;
     }
-    // lane summary of its 8 units
-    ExtRun mine;
-    {
-      u32 valid_mask = nu >= 8 ? 0xFF : ((1u << nu) - 1);
-      mine.all = (nu > 0 && (ext_mask & valid_mask) == valid_mask) ? 1 : (nu == 0 ? 1 : 0);
-      // trailing run: from the top valid unit downward
-      u32 len_ = 0;
-      u64 val = 0;
-      for (int q = (int)nu - 1; q >= 0 && ((ext_mask >> q) & 1); q--) len_++;
-      for (u32 q = nu - len_; q < nu; q++) val = (val << 8) | argb[q];
-      mine.len = len_;
-      mine.val = val;
-    }
-    // inclusive scan over lanes, then exclusive = shifted
-    ExtRun inc = mine;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      ExtRun o = shfl_up_run(inc, d);
-      if (lane >= d) inc = ext_combine(o, inc);
-    }
-    ExtRun excl = shfl_up_run(inc, 1);
-    if (lane == 0) excl = ExtRun{1, 0, 0};
-    excl = ext_combine(carry, excl);
-    // instruction slots: non-EXT units before this lane
-    u32 my_ins = (u32)__popc((~ext_mask) & (nu >= 8 ? 0xFF : ((1u << nu) - 1)));
-    u32 pre = my_ins;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      u32 o = __shfl_up_sync(0xffffffffu, pre, d);
-      if (lane >= d) pre += o;
-    }
-    u32 total = __shfl_sync(0xffffffffu, pre, 31);
-    u32 idx = n_before + pre - my_ins;
-    // walk my units with the incoming run
-    u32 run_len = excl.len;  // trailing EXTENDED_ARG run entering my span
-    u64 run_val = excl.val;
+    // Fast path (warp-uniform): no EXTENDED_ARG in the chunk and none pending, so
+    // every unit is one instruction, lane L's records start at 8*L and need no
+    // scans; a single-chunk object with no EXTENDED_ARG also has every even
+    // in-range offset as an extent start.
+    const bool fast = __ballot_sync(0xffffffffu, ext_mask != 0) == 0 && carry.len == 0;
+    u32 total;
     i64 my_bad = -1, my_bad_off = 0, my_bad_tgt = 0;
-    for (u32 q = 0; q < nu; q++) {
-      u32 u = u0 + q;
-      if ((ext_mask >> q) & 1) {
-        run_val = (run_val << 8) | argb[q];
-        run_len++;
-        continue;
-      }
-      u32 e = ent[q];
-      bool has_arg = UPY_ENT_HASARG(e);
-      u64 ext = run_len ? (run_len >= 8 ? 0 : (run_val << 8)) : 0;
-      bool sat = run_len >= 8;
-      u64 arg = has_arg ? (argb[q] | ext) : 0;
-      bool big = has_arg && (sat || (arg >> 32));
-      upy_ins r;
-      r.offset = 2 * (u - run_len);
-      r.arg = big ? 0xFFFFFFFFu : (u32)arg;
-      r.opcode = (u8)ops[q];
-      r.n_prefixes = (u8)(run_len > 255 ? 255 : run_len);
-      r.cache_units = 0;
-      r.flags = (u8)((has_arg ? 1 : 0) | (big ? 2 : 0));
-      stage[idx - n_before] = r;
-      u32 kind = UPY_ENT_KIND(e);
-      if (my_bad < 0 && (kind == K_JUMP_REL || kind == K_JUMP_ABS || kind == K_JUMP_BACK)) {
-        bool okk;
-        i64 t = jump_target_u64(minor, kind, 2ull * u, arg, &okk);
-        bool valid = !big && t >= 0 && t < (i64)len && !(t & 1) && (t == 0 || code[t - 2] != EXT_OP);
-        if (!valid) {
-          my_bad = idx;
-          my_bad_off = r.offset;
-          my_bad_tgt = t;
+    ExtRun inc = {0, 0, 0};
+    if (fast) {
+      total = units - base < 256 ? units - base : 256;
+      const bool no_ext_obj = units <= 256;
+      uint4* st4 = reinterpret_cast<uint4*>(stage) + 6 * lane;
+#pragma unroll
+      for (int g = 0; g < 2; g++) {  // 4 records = 12 words = 3 uint4 per group
+        u32 wr[12];
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+          const int q = 4 * g + r;
+          u32 u = u0 + q;
+          u32 e = ent[q];
+          u32 has_arg = UPY_ENT_HASARG(e) ? 1u : 0u;
+          u32 arg = has_arg ? UNIT_ARG(q) : 0u;
+          wr[3 * r] = 2 * u;
+          wr[3 * r + 1] = arg;
+          wr[3 * r + 2] = UNIT_OP(q) | (has_arg << 24);
+          u32 kind = UPY_ENT_KIND(e);
+          if ((u32)q < nu && my_bad < 0 && (kind == K_JUMP_REL || kind == K_JUMP_ABS || kind == K_JUMP_BACK)) {
+            bool okk;
+            i64 t = jump_target_u64(minor, kind, 2ull * u, arg, &okk);
+            bool valid = t >= 0 && t < (i64)len && !(t & 1) && (no_ext_obj || t == 0 || code[t - 2] != EXT_OP);
+            if (!valid) {
+              my_bad = n_before + 8 * lane + q;
+              my_bad_off = 2 * u;
+              my_bad_tgt = t;
+            }
+          }
         }
+#pragma unroll
+        for (int k = 0; k < 3; k++) st4[3 * g + k] = make_uint4(wr[4 * k], wr[4 * k + 1], wr[4 * k + 2], wr[4 * k + 3]);
       }
-      idx++;
-      run_len = 0;
-      run_val = 0;
+    } else {
+      // lane summary of its 8 units
+      ExtRun mine;
+      {
+        u32 valid_mask = nu >= 8 ? 0xFF : ((1u << nu) - 1);
+        mine.all = (nu > 0 && (ext_mask & valid_mask) == valid_mask) ? 1 : (nu == 0 ? 1 : 0);
+        // trailing run: from the top valid unit downward
+        u32 len_ = 0;
+        u64 val = 0;
+        bool in_run = true;
+#pragma unroll
+        for (int q = 7; q >= 0; q--) {
+          if ((u32)q >= nu) continue;
+          in_run = in_run && ((ext_mask >> q) & 1);
+          if (in_run) len_++;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; q++)
+          if ((u32)q < nu && (u32)q >= nu - len_) val = (val << 8) | UNIT_ARG(q);
+        mine.len = len_;
+        mine.val = val;
+      }
+      // inclusive scan over lanes, then exclusive = shifted
+      inc = mine;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        ExtRun o = shfl_up_run(inc, d);
+        if (lane >= d) inc = ext_combine(o, inc);
+      }
+      ExtRun excl = shfl_up_run(inc, 1);
+      if (lane == 0) excl = ExtRun{1, 0, 0};
+      excl = ext_combine(carry, excl);
+      // instruction slots: non-EXT units before this lane
+      u32 my_ins = (u32)__popc((~ext_mask) & (nu >= 8 ? 0xFF : ((1u << nu) - 1)));
+      u32 pre = my_ins;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        u32 o = __shfl_up_sync(0xffffffffu, pre, d);
+        if (lane >= d) pre += o;
+      }
+      total = __shfl_sync(0xffffffffu, pre, 31);
+      u32 idx = n_before + pre - my_ins;
+      // walk my units with the incoming run
+      u32 run_len = excl.len;  // trailing EXTENDED_ARG run entering my span
+      u64 run_val = excl.val;
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        if ((u32)q >= nu) continue;
+        u32 u = u0 + q;
+        if ((ext_mask >> q) & 1) {
+          run_val = (run_val << 8) | UNIT_ARG(q);
+          run_len++;
+          continue;
+        }
+        u32 e = ent[q];
+        bool has_arg = UPY_ENT_HASARG(e);
+        u64 ext = run_len ? (run_len >= 8 ? 0 : (run_val << 8)) : 0;
+        bool sat = run_len >= 8;
+        u64 arg = has_arg ? (UNIT_ARG(q) | ext) : 0;
+        bool big = has_arg && (sat || (arg >> 32));
+        u32* sw = reinterpret_cast<u32*>(stage) + 3 * (idx - n_before);
+        u32 off = 2 * (u - run_len);
+        sw[0] = off;
+        sw[1] = big ? 0xFFFFFFFFu : (u32)arg;
+        sw[2] = UNIT_OP(q) | ((run_len > 255 ? 255u : run_len) << 8) | (((has_arg ? 1u : 0u) | (big ? 2u : 0u)) << 24);
+        u32 kind = UPY_ENT_KIND(e);
+        if (my_bad < 0 && (kind == K_JUMP_REL || kind == K_JUMP_ABS || kind == K_JUMP_BACK)) {
+          bool okk;
+          i64 t = jump_target_u64(minor, kind, 2ull * u, arg, &okk);
+          bool valid = !big && t >= 0 && t < (i64)len && !(t & 1) && (t == 0 || code[t - 2] != EXT_OP);
+          if (!valid) {
+            my_bad = idx;
+            my_bad_off = off;
+            my_bad_tgt = t;
+          }
+        }
+        idx++;
+        run_len = 0;
+        run_val = 0;
+      }
     }
     // first bad jump of the chunk (lowest instruction index)
     u32 badm = __ballot_sync(0xffffffffu, my_bad >= 0);
@@ -301,16 +344,28 @@ __device__ __forceinline__ void decode_warp(const u8* __restrict__ code, u32 len
       bad_off = __shfl_sync(0xffffffffu, my_bad_off, bl);
       bad_tgt = __shfl_sync(0xffffffffu, my_bad_tgt, bl);
     }
-    // carry into the next chunk: state after the whole chunk
-    carry = ext_combine(carry, shfl_run(inc, 31));
+    // carry into the next chunk: state after the whole chunk (a chunk without
+    // EXTENDED_ARG leaves no pending run)
+    if (fast) carry = ExtRun{0, 0, 0};
+    else carry = ext_combine(carry, shfl_run(inc, 31));
     __syncwarp();
-    {  // coalesced write-out of this chunk's records (3 words each)
-      const u32* src = reinterpret_cast<const u32*>(stage);
+    {  // coalesced write-out of this chunk's records (12 B each)
+      u32 nw = 3 * total;
       u32* dst = reinterpret_cast<u32*>(rec + n_before);
-      for (u32 w = lane; w < 3 * total; w += 32) dst[w] = src[w];
+      const u32* src = reinterpret_cast<const u32*>(stage);
+      u32 done = 0;
+      if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+        const uint4* s4 = reinterpret_cast<const uint4*>(stage);
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+        for (u32 w = lane; w < nw / 4; w += 32) d4[w] = s4[w];
+        done = nw & ~3u;
+      }
+      for (u32 w = done + lane; w < nw; w += 32) dst[w] = src[w];
     }
     __syncwarp();
     n_before += total;
+#undef UNIT_OP
+#undef UNIT_ARG
   }
   if (lane == 0) {
     if (carry.len) {  // code ends inside an EXTENDED_ARG run
@@ -330,4 +385,5 @@ __device__ __forceinline__ void decode_warp(const u8* __restrict__ code, u32 len
     }
   }
 }
+
 #endif

@@ -249,14 +249,37 @@ struct Emitter {
   HD bool target(Text* t, Node* e, bool nested);
   HD int prec_of(const Node* e, bool* ok);
   HD bool expr(Text* t, Node* e, int parent = 0, bool right_side = false);
+  // sub() with the leaf cases inline: names and None / small non-negative int
+  // constants are atoms (never parenthesised, never None-text), so they skip the
+  // recursive call (its register save/restore was the emitter's main cost).
+  HD FORCEINL bool sub(Text* t, Node* e, int parent = 0, bool right_side = false) {
+    if (e && !C->err) {
+      if (e->k == E_NAME && !s_is_none(e->s)) {
+        t_str(C, t, e->s);
+        return false;
+      }
+      if (e->k == E_CONST && e->cid < CID_NONE_SYN) {
+        const upy_const* c = cget(C, e->cid);
+        if (c->kind == UPY_C_INT && c->n == 1 && c->ival >= 0) {
+          t_u32(C, t, C->A->limbs[c->off]);
+          return false;
+        }
+        if (c->kind == UPY_C_NONE) {
+          t_puts(C, t, "None");
+          return false;
+        }
+      }
+    }
+    return expr(t, e, parent, right_side);
+  }
   HD void expr_body(Text* t, Node* e);
   HD bool callarg(Text* t, Node* a) {
     if (is_k(a, E_STARRED)) {
       t_put(C, t, '*');
-      concat_none(expr(t, a->a, P_LAMBDA));
+      concat_none(sub(t, a->a, P_LAMBDA));
       return false;
     }
-    return expr(t, a, P_LAMBDA);
+    return sub(t, a, P_LAMBDA);
   }
   HD void index(Text* t, Node* idx);
   HD void slice(Text* t, Node* s);
@@ -571,7 +594,7 @@ HD NOINL bool Emitter::expr(Text* t, Node* e, int parent, bool right_side) {
   return !paren && e->k == E_NAME && s_is_none(e->s);
 }
 
-HD NOINL void Emitter::expr_body(Text* t, Node* e) {
+HD FORCEINL void Emitter::expr_body(Text* t, Node* e) {  // only caller: sub()
   switch (e->k) {
     case E_CONST: render_constant(t, e->cid); return;
     case E_NAME: name_text(t, e->s); return;
@@ -579,30 +602,30 @@ HD NOINL void Emitter::expr_body(Text* t, Node* e) {
     case E_BINOP: {
       int p = binop_prec(e->op);
       if (e->op == BO_POW) {
-        expr(t, e->a, p, true);
+        sub(t, e->a, p, true);
         t_puts(C, t, " ** ");
-        expr(t, e->b, p);
+        sub(t, e->b, p);
       } else {
-        expr(t, e->a, p);
+        sub(t, e->a, p);
         t_put(C, t, ' ');
         t_puts(C, t, binop_str(e->op));
         t_put(C, t, ' ');
-        expr(t, e->b, p, true);
+        sub(t, e->b, p, true);
       }
       return;
     }
     case E_UNARY:
       if (e->op == UO_NOT) {
         t_puts(C, t, "not ");
-        expr(t, e->a, P_NOT);
+        sub(t, e->a, P_NOT);
       } else {
         t_puts(C, t, unary_str(e->op));
-        expr(t, e->a, P_UNARY);
+        sub(t, e->a, P_UNARY);
       }
       return;
     case E_COMPARE: {  // " ".join([left, op, operand, ...])
       Join j = join0();
-      join_item(j, expr(t, e->a, P_COMPARE, true));
+      join_item(j, sub(t, e->a, P_COMPARE, true));
       u32 n = e->l1->n < e->l2->n ? e->l1->n : e->l2->n;
       for (u32 q = 0; q < n && !C->err; q++) {
         u8 c = e->l1->d[q]->op;
@@ -610,7 +633,7 @@ HD NOINL void Emitter::expr_body(Text* t, Node* e) {
         t_put(C, t, ' ');
         t_puts(C, t, cmp_str(c));
         t_put(C, t, ' ');
-        join_item(j, expr(t, e->l2->d[q], P_COMPARE, true));
+        join_item(j, sub(t, e->l2->d[q], P_COMPARE, true));
       }
       join_end(j);
       return;
@@ -620,17 +643,17 @@ HD NOINL void Emitter::expr_body(Text* t, Node* e) {
       Join j = join0();
       for (u32 q = 0; q < e->l1->n && !C->err; q++) {
         if (q) t_puts(C, t, e->op ? " or " : " and ");
-        join_item(j, expr(t, e->l1->d[q], p, q > 0));
+        join_item(j, sub(t, e->l1->d[q], p, q > 0));
       }
       join_end(j);
       return;
     }
     case E_TERNARY:
-      expr(t, e->b, P_TERNARY, true);
+      sub(t, e->b, P_TERNARY, true);
       t_puts(C, t, " if ");
-      expr(t, e->a, P_TERNARY, true);
+      sub(t, e->a, P_TERNARY, true);
       t_puts(C, t, " else ");
-      expr(t, e->c, P_TERNARY);
+      sub(t, e->c, P_TERNARY);
       return;
     case E_LAMBDA: {
       Text pt = {nullptr, 0, 0};
@@ -643,7 +666,7 @@ HD NOINL void Emitter::expr_body(Text* t, Node* e) {
       } else {
         t_puts(C, t, "lambda: ");
       }
-      concat_none(expr(t, e->a, P_LAMBDA));
+      concat_none(sub(t, e->a, P_LAMBDA));
       return;
     }
     case E_NAMED:
@@ -653,10 +676,10 @@ HD NOINL void Emitter::expr_body(Text* t, Node* e) {
       }
       name_text(t, e->a->s);
       t_puts(C, t, " := ");
-      expr(t, e->b, P_LAMBDA);
+      sub(t, e->b, P_LAMBDA);
       return;
     case E_CALL: {
-      expr(t, e->a, P_ATOM);
+      sub(t, e->a, P_ATOM);
       t_put(C, t, '(');
       bool first = true;
       Join j = join0();
@@ -671,11 +694,11 @@ HD NOINL void Emitter::expr_body(Text* t, Node* e) {
         Node* kw = e->l2->d[q];
         if (s_is_none(kw->s)) {
           t_puts(C, t, "**");
-          concat_none(expr(t, kw->a, P_LAMBDA));
+          concat_none(sub(t, kw->a, P_LAMBDA));
         } else {
           t_str(C, t, kw->s);
           t_put(C, t, '=');
-          expr(t, kw->a, P_LAMBDA);
+          sub(t, kw->a, P_LAMBDA);
         }
         join_item(j, false);
       }
@@ -686,18 +709,18 @@ HD NOINL void Emitter::expr_body(Text* t, Node* e) {
     case E_ATTR: {
       bool wrap = is_k(e->a, E_CONST) && e->a->cid != CID_INVALID && ckind(C, e->a->cid) == UPY_C_INT;
       if (is_k(e->a, E_CONST) && e->a->cid == CID_INVALID) {
-        expr(t, e->a, P_ATOM);
+        sub(t, e->a, P_ATOM);
         return;
       }
       if (wrap) t_put(C, t, '(');
-      expr(t, e->a, P_ATOM);
+      sub(t, e->a, P_ATOM);
       if (wrap) t_put(C, t, ')');
       t_put(C, t, '.');
       name_text(t, e->s);
       return;
     }
     case E_SUBSCR:
-      expr(t, e->a, P_ATOM);
+      sub(t, e->a, P_ATOM);
       t_put(C, t, '[');
       index(t, e->b);
       t_put(C, t, ']');
@@ -746,11 +769,11 @@ HD NOINL void Emitter::expr_body(Text* t, Node* e) {
         Node* k = e->l1->d[q];
         if (!k) {
           t_puts(C, t, "**");
-          concat_none(expr(t, e->l2->d[q], P_LAMBDA));
+          concat_none(sub(t, e->l2->d[q], P_LAMBDA));
         } else {
-          expr(t, k, P_LAMBDA);
+          sub(t, k, P_LAMBDA);
           t_puts(C, t, ": ");
-          expr(t, e->l2->d[q], P_LAMBDA);
+          sub(t, e->l2->d[q], P_LAMBDA);
         }
       }
       t_put(C, t, '}');
@@ -758,7 +781,7 @@ HD NOINL void Emitter::expr_body(Text* t, Node* e) {
     }
     case E_STARRED:
       t_put(C, t, '*');
-      concat_none(expr(t, e->a, P_LAMBDA));
+      concat_none(sub(t, e->a, P_LAMBDA));
       return;
     case E_YIELD: {
       bool bare = !e->a;
@@ -772,13 +795,13 @@ HD NOINL void Emitter::expr_body(Text* t, Node* e) {
         return;
       }
       t_puts(C, t, "(yield ");
-      expr(t, e->a, P_LAMBDA);
+      sub(t, e->a, P_LAMBDA);
       t_put(C, t, ')');
       return;
     }
     case E_YIELDFROM:
       t_puts(C, t, "(yield from ");
-      expr(t, e->a, P_LAMBDA);
+      sub(t, e->a, P_LAMBDA);
       t_put(C, t, ')');
       return;
     case E_COMP: {
@@ -790,18 +813,18 @@ HD NOINL void Emitter::expr_body(Text* t, Node* e) {
         t_puts(C, &sp, "for ");
         target(&sp, g->a, false);
         t_puts(C, &sp, " in ");
-        expr(&sp, g->b, P_TERNARY);
+        sub(&sp, g->b, P_TERNARY);
         for (u32 w = 0; w < g->l1->n && !C->err; w++) {
           t_puts(C, &sp, " if ");
-          expr(&sp, g->l1->d[w], P_TERNARY);
+          sub(&sp, g->l1->d[w], P_TERNARY);
         }
       }
       CK(C);
       if (e->op == 2) {
         t_put(C, t, '{');
-        expr(t, e->b, P_TERNARY);
+        sub(t, e->b, P_TERNARY);
         t_puts(C, t, ": ");
-        expr(t, e->c, P_TERNARY);
+        sub(t, e->c, P_TERNARY);
         t_put(C, t, ' ');
         t_putn(C, t, sp.d, sp.n);
         t_put(C, t, '}');
@@ -810,7 +833,7 @@ HD NOINL void Emitter::expr_body(Text* t, Node* e) {
       char open = e->op == 0 ? '[' : e->op == 1 ? '{' : '(';
       char close = e->op == 0 ? ']' : e->op == 1 ? '}' : ')';
       Text el = {nullptr, 0, 0};
-      expr(&el, e->a, P_TERNARY);
+      sub(&el, e->a, P_TERNARY);
       t_put(C, t, open);
       t_putn(C, t, el.d, el.n);
       t_put(C, t, ' ');
@@ -860,7 +883,7 @@ HD NOINL void Emitter::format_part(Text* t, Node* fv) {  // emitter.py:510-519
     return;
   }
   Text inner = {nullptr, 0, 0};
-  bool none = expr(&inner, fv->a, P_TERNARY);
+  bool none = sub(&inner, fv->a, P_TERNARY);
   CK(C);
   if (none) {  // inner.startswith("{") on the None object
     py_error(C, UPY_ST_PY_ATTRIBUTE_ERROR, "'NoneType' object has no attribute 'startswith'");
@@ -903,7 +926,7 @@ HD inline void Emitter::format_spec(Text* t, Node* spec) {  // emitter.py:521-53
     return;
   }
   t_put(C, t, '{');
-  concat_none(expr(t, spec, P_TERNARY));
+  concat_none(sub(t, spec, P_TERNARY));
   t_put(C, t, '}');
 }
 
@@ -924,22 +947,22 @@ HD inline void Emitter::index(Text* t, Node* idx) {  // emitter.py:420-430
           slice(t, el);
           join_item(j, false);
         } else {
-          join_item(j, expr(t, el));
+          join_item(j, sub(t, el));
         }
       }
       join_end(j);
       return;
     }
   }
-  expr(t, idx);
+  sub(t, idx);
 }
 HD inline void Emitter::slice(Text* t, Node* s) {
-  if (s->a) expr(t, s->a, P_TERNARY);
+  if (s->a) sub(t, s->a, P_TERNARY);
   t_put(C, t, ':');
-  if (s->b) expr(t, s->b, P_TERNARY);
+  if (s->b) sub(t, s->b, P_TERNARY);
   if (s->c) {
     t_put(C, t, ':');
-    expr(t, s->c, P_TERNARY);
+    sub(t, s->c, P_TERNARY);
   }
 }
 
@@ -966,7 +989,7 @@ HD inline bool Emitter::target(Text* t, Node* e, bool nested) {  // emitter.py:3
     concat_none(target(t, e->a, nested));
     return false;
   }
-  return expr(t, e);
+  return sub(t, e);
 }
 
 HD NOINL void Emitter::params(Text* t, Node* p) {  // emitter.py:285-308
@@ -983,7 +1006,7 @@ HD NOINL void Emitter::params(Text* t, Node* p) {  // emitter.py:285-308
     i64 di = (i64)i - ((i64)nargs - (i64)nd);
     if (di >= 0) {
       t_put(C, t, '=');
-      expr(t, p->l1->d[di]);
+      sub(t, p->l1->d[di]);
     }
     if (p->i && (i64)i + 1 == (i64)p->i) {
       sep();
@@ -1005,7 +1028,7 @@ HD NOINL void Emitter::params(Text* t, Node* p) {  // emitter.py:285-308
     const Node* kd = kw_lookup(p->l2, k);
     if (kd) {
       t_put(C, t, '=');
-      expr(t, kd->a);
+      sub(t, kd->a);
     }
   }
   if (!s_is_none(p->s2) && p->s2.n) {
@@ -1020,7 +1043,7 @@ HD NOINL void Emitter::emit_if(Node* s, const char* kw) {
   line_start();
   t_puts(C, out, kw);
   t_put(C, out, ' ');
-  expr(out, s->a);
+  sub(out, s->a);
   t_put(C, out, ':');
   line_end();
   block(s->l1);
@@ -1060,7 +1083,7 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
       }
       join_end(j);
       t_puts(C, out, " = ");
-      expr(out, s->a);
+      sub(out, s->a);
       line_end();
       return;
     }
@@ -1070,12 +1093,12 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
       t_put(C, out, ' ');
       t_puts(C, out, binop_str(s->op));
       t_puts(C, out, "= ");
-      expr(out, s->b);
+      sub(out, s->b);
       line_end();
       return;
     case S_EXPR:
       line_start();
-      expr(out, s->a);
+      sub(out, s->a);
       line_end();
       return;
     case S_RETURN: {
@@ -1090,7 +1113,7 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
         t_puts(C, out, "return None");
       } else {
         t_puts(C, out, "return ");
-        expr(out, s->a);
+        sub(out, s->a);
       }
       line_end();
       return;
@@ -1101,10 +1124,10 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
         t_puts(C, out, "raise");
       } else {
         t_puts(C, out, "raise ");
-        expr(out, s->a);
+        sub(out, s->a);
         if (s->b) {
           t_puts(C, out, " from ");
-          expr(out, s->b);
+          sub(out, s->b);
         }
       }
       line_end();
@@ -1142,10 +1165,10 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
     case S_ASSERT:
       line_start();
       t_puts(C, out, "assert ");
-      expr(out, s->a);
+      sub(out, s->a);
       if (s->b) {
         t_puts(C, out, ", ");
-        expr(out, s->b);
+        sub(out, s->b);
       }
       line_end();
       return;
@@ -1212,7 +1235,7 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
     case S_WHILE:
       line_start();
       t_puts(C, out, "while ");
-      expr(out, s->a);
+      sub(out, s->a);
       t_put(C, out, ':');
       line_end();
       block(s->l1);
@@ -1226,7 +1249,7 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
       t_puts(C, out, "for ");
       target(out, s->a, false);
       t_puts(C, out, " in ");
-      expr(out, s->b);
+      sub(out, s->b);
       t_put(C, out, ':');
       line_end();
       block(s->l1);
@@ -1245,7 +1268,7 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
           t_puts(C, out, "except:");
         } else {
           t_puts(C, out, "except ");
-          expr(out, hd->a);
+          sub(out, hd->a);
           if (!s_is_none(hd->s) && hd->s.n) {
             t_puts(C, out, " as ");
             t_str(C, out, hd->s);
@@ -1271,7 +1294,7 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
       for (u32 q = 0; q < s->l1->n && !C->err; q++) {
         if (q) t_puts(C, out, ", ");
         Node* it = s->l1->d[q];
-        bool none = expr(out, it->a);
+        bool none = sub(out, it->a);
         if (it->b) {
           t_puts(C, out, " as ");
           target(out, it->b, true);
@@ -1291,7 +1314,7 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
       for (u32 q = 0; q < s->l2->n && !C->err; q++) {
         line_start();
         t_put(C, out, '@');
-        concat_none(expr(out, s->l2->d[q]));
+        concat_none(sub(out, s->l2->d[q]));
         line_end();
       }
       line_start();
@@ -1307,7 +1330,7 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
       for (u32 q = 0; q < s->l4->n && !C->err; q++) {
         line_start();
         t_put(C, out, '@');
-        concat_none(expr(out, s->l4->d[q]));
+        concat_none(sub(out, s->l4->d[q]));
         line_end();
       }
       line_start();
@@ -1320,14 +1343,14 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
       for (u32 q = 0; q < s->l1->n && !C->err; q++) {
         if (!first) t_puts(C, out, ", ");
         first = false;
-        join_item(j, expr(out, s->l1->d[q]));
+        join_item(j, sub(out, s->l1->d[q]));
       }
       for (u32 q = 0; q < s->l2->n && !C->err; q++) {
         if (!first) t_puts(C, out, ", ");
         first = false;
         name_text(out, s->l2->d[q]->s);
         t_put(C, out, '=');
-        expr(out, s->l2->d[q]->a);
+        sub(out, s->l2->d[q]->a);
       }
       join_end(j);
       if (na) t_put(C, out, ')');

@@ -127,7 +127,7 @@ HD inline bool is_k(const Node* n, u8 k) { return n && n->k == k; }
 
 #define NODE_END(f) (offsetof(Node, f) + sizeof(((Node*)0)->f))
 // bytes of the Node prefix a kind uses (see the field table above)
-HD inline u32 node_bytes(u8 k) {
+HD constexpr u32 node_bytes_sw(u8 k) {
   switch (k) {
     case E_CONST: case E_STACKTEMP: case E_NULL: case E_METHSELF: case E_EXCVALUE: case E_FINSENT:
     case E_BUILDCLASS:
@@ -156,6 +156,21 @@ HD inline u32 node_bytes(u8 k) {
   }
   return sizeof(Node);  // S_IMPORTSTAR (cid), S_IMPORTFROM (src), anything else: full record
 }
+// ... as a 256-entry table (mk() is inlined at hundreds of sites; a switch there
+// was an out-of-line call per node)
+struct NodeSizeTable {
+  u8 v[256];
+  HD constexpr NodeSizeTable() : v() {
+    for (int k = 0; k < 256; k++) v[k] = (u8)node_bytes_sw((u8)k);
+  }
+};
+static_assert(sizeof(Node) <= 255, "node sizes are stored as u8");
+#ifdef __CUDA_ARCH__
+__constant__ NodeSizeTable NODE_SIZES;
+#else
+static constexpr NodeSizeTable NODE_SIZES;
+#endif
+HD inline u32 node_bytes(u8 k) { return NODE_SIZES.v[k]; }
 
 HD inline Node* mk(Dc* C, u8 k) {
   Node* n = (Node*)zalloc(C, node_bytes(k));

@@ -34,14 +34,14 @@ struct Code {
   Vec<Str>* kwnames;
 };
 
-HD inline Str argval_name(Dc* C, const Code* K, const Ins& in) {
+HD FORCEINL Str argval_name(Dc* C, const Code* K, const Ins& in) {
   // kind == name (disasm.py:134-138)
   u64 idx = in.arg;
   if (K->minor >= 11 && in.op == OP_LOAD_GLOBAL) idx = in.arg >> 1;
   if ((in.flags & 2) || idx >= K->o->n_names) return Snone();
   return obj_tab(C, K->o->names_off, (u32)idx);
 }
-HD inline Str argval_local(Dc* C, const Code* K, const Ins& in) {
+HD FORCEINL Str argval_local(Dc* C, const Code* K, const Ins& in) {
   if (in.flags & 2) return Snone();
   if (K->minor <= 10) {
     if (in.arg >= K->o->n_varnames) return Snone();
@@ -51,13 +51,13 @@ HD inline Str argval_local(Dc* C, const Code* K, const Ins& in) {
   Str s = obj_localsplus(C, K->oi, in.arg, &ok);
   return ok ? s : Snone();
 }
-HD inline Str argval_free(Dc* C, const Code* K, const Ins& in) {
+HD FORCEINL Str argval_free(Dc* C, const Code* K, const Ins& in) {
   if (in.flags & 2) return Snone();
   bool ok;
   Str s = obj_deref_name(C, K->oi, in.arg, &ok);
   return ok ? s : Snone();
 }
-HD inline u32 argval_const(Dc* C, const Code* K, const Ins& in) {
+HD FORCEINL u32 argval_const(Dc* C, const Code* K, const Ins& in) {
   if ((in.flags & 2) || in.arg >= K->o->n_consts) return CID_INVALID;
   return obj_const_id(C, K->oi, in.arg);
 }
@@ -192,7 +192,7 @@ struct Sim {
   Dc* C;
   Code* K;
 
-  HD Node* pop(NV* st, const Ins* ins) {
+  HD FORCEINL Node* pop(NV* st, const Ins* ins) {
     if (st->n == 0) {
       fail_underflow(C, ins);
       return nullptr;
@@ -200,17 +200,20 @@ struct Sim {
     return st->d[--st->n];
   }
   // pop for expression use, folding pending walrus targets (symexec.py:217-228)
-  HD Node* pop_value(NV* st, const Ins* ins) {
+  HD FORCEINL Node* pop_value(NV* st, const Ins* ins) {
     Node* v = pop(st, ins);
     CKR(C, nullptr);
     NV* pend = v->pend;
-    if (pend && pend->n) {
-      Node* target = pend->d[--pend->n];
-      Node* inner = v;
-      v->pend = nullptr;
-      v = mk2(C, E_NAMED, target, inner);
-      for (i32 i = (i32)pend->n - 1; i >= 0; i--) v = mk2(C, E_NAMED, pend->d[i], v);
-    }
+    if (pend && pend->n) v = fold_pending(v);
+    return v;
+  }
+  HD NOINL Node* fold_pending(Node* v) {  // walrus targets pending on a popped value
+    NV* pend = v->pend;
+    Node* target = pend->d[--pend->n];
+    Node* inner = v;
+    v->pend = nullptr;
+    v = mk2(C, E_NAMED, target, inner);
+    for (i32 i = (i32)pend->n - 1; i >= 0; i--) v = mk2(C, E_NAMED, pend->d[i], v);
     return v;
   }
   HD NV* pops(NV* st, const Ins* ins, u64 n) {
@@ -525,7 +528,9 @@ struct Sim {
 
 #define BR_PUSH(x) push(st, (x))
 
-HD NOINL int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out) {
+// Inlined into simulate() (its only caller): as a call, its register save/restore
+// was ~30% of the kernel's local-memory traffic (ncu source page, round 1).
+HD FORCEINL int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out) {
   const Ins& in = *ins;
   switch (in.op) {
     // ------------------------------------------------ loads (symexec.py:239-268)

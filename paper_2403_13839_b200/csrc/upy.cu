@@ -1,6 +1,6 @@
 // upy.cu -- sm_100a kernels and the C ABI of include/upy.h.
 //
-//   upy_decode_kernel      one warp per code object (roots and nested): HBM-bound
+//   upy_decode_kernel      (decode_kernel.cu) one warp per code object (roots and nested): HBM-bound
 //                          decode of co_code into 12-byte instruction records
 //                          (disasm.py:71-172).
 //   upy_decompile_kernel   persistent, one thread per root object at a time:
@@ -10,7 +10,9 @@
 #include <cuda_runtime.h>
 #include <stdio.h>
 #include "pipeline.h"
-#include "decode.h"
+
+// decode_kernel.cu
+cudaError_t upy_decode_launch(const upy_arena* arena, upy_ins* ins, upy_decoded* dec, cudaStream_t s, int sms);
 
 #define MSG_BYTES 4096u
 #define SLOT_HEADER (MSG_BYTES + SINK_BYTES)
@@ -18,35 +20,6 @@
 static __thread char g_last_error[512];
 static void set_err(const char* fmt, const char* a = "") {
   snprintf(g_last_error, sizeof g_last_error, fmt, a);
-}
-
-__global__ void __launch_bounds__(256) upy_decode_kernel(upy_arena A, upy_ins* __restrict__ ins,
-                                                         upy_decoded* __restrict__ dec) {
-  const int lane = threadIdx.x & 31;
-  const i64 warp = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
-  __shared__ u32 tab[3][256];              // 3.8-3.10 opcode tables
-  __shared__ upy_ins stage[256 / 32][256];  // per-warp record staging (24 KB)
-  for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) tab[i >> 8][i & 255] = UPY_OPTABLE_DEV[i >> 8][i & 255];
-  __syncthreads();
-  upy_ins* my_stage = stage[threadIdx.x >> 5];
-  for (i64 o = warp; o < A.n_objs; o += nwarps) {
-    const upy_obj* ob = &A.objs[o];
-    const u8* code = A.bytes + ob->code_off;
-    upy_ins* rec = ins + (ob->code_off >> 1);
-    int minor = (int)ob->minor;
-    if (minor >= 8 && minor <= 10) {
-      decode_warp(code, ob->code_len, minor, rec, &dec[o], tab[minor - 8], my_stage);
-    } else if (lane == 0) {
-      if (minor == 11) {
-        decode_scalar(code, ob->code_len, minor, rec, &dec[o]);
-      } else {
-        dec[o].status = UPY_ST_INTERNAL;
-        dec[o].n_instrs = 0;
-      }
-    }
-    __syncwarp();
-  }
 }
 
 struct KParams {
@@ -207,14 +180,7 @@ int upy_decode_batch(const upy_arena* arena, upy_ins* ins, upy_decoded* dec, voi
     return 1;
   }
   if (arena->n_objs == 0) return 0;
-  cudaStream_t s = (cudaStream_t)stream;
-  int threads = 256;
-  i64 warps = arena->n_objs;
-  i64 blocks = (warps * 32 + threads - 1) / threads;
-  i64 max_blocks = (i64)sm_count() * 64;
-  if (blocks > max_blocks) blocks = max_blocks;
-  upy_decode_kernel<<<(unsigned)blocks, threads, 0, s>>>(*arena, ins, dec);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = upy_decode_launch(arena, ins, dec, (cudaStream_t)stream, sm_count());
   if (e != cudaSuccess) {
     set_err("decode launch: %s", cudaGetErrorString(e));
     return 2;

@@ -19,6 +19,24 @@ class UnsupportedVersion(UnpyreError):
         self.minor = minor
 
 
+# ---------------------------------------------------------------- loaders (errors.py:19-34)
+
+class UnknownMagic(UnpyreError):
+    def __init__(self, magic):
+        super().__init__(f"unknown pyc magic {magic:#06x} (unsupported interpreter version)")
+        self.magic = magic
+
+
+class TruncatedHeader(UnpyreError):
+    pass
+
+
+class MalformedMarshal(UnpyreError):
+    def __init__(self, message, offset):
+        super().__init__(f"{message} (at byte offset {offset})")
+        self.offset = offset
+
+
 class UnknownOpcode(UnpyreError):
     def __init__(self, opcode, offset):
         super().__init__(f"unknown opcode {opcode} at offset {offset}")
@@ -88,6 +106,9 @@ ST_UNSUPPORTED_OPCODE = 7
 ST_STACK_DEPTH_MISMATCH = 8
 ST_STRUCTURING_FAILED = 9
 ST_MARKER_LEAK = 10
+ST_UNKNOWN_MAGIC = 11
+ST_TRUNCATED_HEADER = 12
+ST_MALFORMED_MARSHAL = 13
 ST_PY_INDEX_ERROR = 20
 ST_PY_ATTRIBUTE_ERROR = 21
 ST_PY_TYPE_ERROR = 22
@@ -146,6 +167,16 @@ def make_exception(status, message, aux):
         return e
     if status == ST_MARKER_LEAK:
         return InternalMarkerLeak(message)
+    if status == ST_UNKNOWN_MAGIC:
+        e = _bare(UnknownMagic, message)
+        e.magic = a0
+        return e
+    if status == ST_TRUNCATED_HEADER:
+        return TruncatedHeader(message)
+    if status == ST_MALFORMED_MARSHAL:
+        e = _bare(MalformedMarshal, message)
+        e.offset = a0
+        return e
     py = {
         ST_PY_INDEX_ERROR: IndexError,
         ST_PY_ATTRIBUTE_ERROR: AttributeError,

@@ -49,3 +49,32 @@ def mismatches(recs, got, strict=True):
             continue
         bad.append((r["case"], r["status"], g[0], r["text"][:300], g[1][:300]))
     return bad
+
+
+def code_key(co):
+    """Canonical structural key of a CodeObject tree (all fields, incl. filename,
+    line/exception tables and qualname; floats by bit pattern)."""
+    import struct
+
+    def ck(c):
+        v = c.value
+        if c.kind == "code":
+            return ("code", code_key(v))
+        if c.kind in ("tuple", "frozenset"):
+            return (c.kind, tuple(ck(x) for x in v))
+        if c.kind == "float":
+            return ("float", struct.pack("<d", v))
+        if c.kind == "complex":
+            return ("complex", struct.pack("<dd", v.real, v.imag))
+        return (c.kind, v)
+
+    return (co.version.minor, co.argcount, co.posonlyargcount, co.kwonlyargcount, co.nlocals, co.stacksize,
+            co.flags, bytes(co.code), tuple(ck(c) for c in co.consts), tuple(co.names), tuple(co.varnames),
+            tuple(co.freevars), tuple(co.cellvars), co.name, co.filename, co.firstlineno, bytes(co.linetable),
+            bytes(co.exceptiontable), co.qualname)
+
+
+def code_key_sha(co):
+    import hashlib
+
+    return hashlib.sha256(repr(code_key(co)).encode("utf-8", "surrogatepass")).hexdigest()[:24]
