@@ -86,6 +86,8 @@ typedef struct {
   uint64_t arena_bytes;      /* bytes per slot arena; 0 = auto from max_code_len */
   int32_t decode_only;       /* 1: run only the decode kernel */
   int32_t skip_decode;       /* 1: reuse the records of a previous decode_only call on the same workspace */
+  int32_t schedule;          /* 0: each thread takes the next root; 1: a warp takes 32 roots and runs
+                                the pipeline stages in lockstep */
 } upy_options;
 
 /* Per-root results (device pointers, caller-allocated). */
@@ -120,7 +122,7 @@ enum {
   UPY_ST_BAD_JUMP_TARGET = 4, UPY_ST_MALFORMED_EXCTABLE = 5, UPY_ST_STACK_UNDERFLOW = 6,
   UPY_ST_UNSUPPORTED_OPCODE = 7, UPY_ST_STACK_DEPTH_MISMATCH = 8, UPY_ST_STRUCTURING_FAILED = 9,
   UPY_ST_MARKER_LEAK = 10,
-  /* loader errors (upy_pyc_load, pyc.py:36-352) */
+  /* loader errors (upy_pyc_load, include/upy_pyc.h; pyc.py:36-352) */
   UPY_ST_UNKNOWN_MAGIC = 11, UPY_ST_TRUNCATED_HEADER = 12, UPY_ST_MALFORMED_MARSHAL = 13,
   UPY_ST_PY_INDEX_ERROR = 20, UPY_ST_PY_ATTRIBUTE_ERROR = 21, UPY_ST_PY_TYPE_ERROR = 22,
   UPY_ST_PY_KEY_ERROR = 23, UPY_ST_PY_VALUE_ERROR = 24, UPY_ST_PY_RECURSION_ERROR = 25,
@@ -151,38 +153,6 @@ int upy_decode_batch(const upy_arena* arena, upy_ins* ins, upy_decoded* dec, voi
 /* Last API-level error message of this thread ("" when none). */
 const char* upy_last_error(void);
 
-/* ---------------------------------------------------------------- loader
- * Host-side .pyc loader (≡ unpyre.pyc.load_pyc per file, pyc.py:36-52, with
- * parse_marshal :78-352): parses a batch of .pyc images (PEP 552 header +
- * marshal stream, CPython 3.8-3.11) straight into one arena image in host
- * memory, ready for a single H2D copy and upy_decompile_batch.  Files are
- * parsed on n_threads host threads (<= 0: all hardware threads).
- *
- * Per file: file_status is UPY_ST_OK or UPY_ST_UNKNOWN_MAGIC /
- * UPY_ST_TRUNCATED_HEADER / UPY_ST_MALFORMED_MARSHAL with the reference's
- * exception text in messages[msg_off .. +msg_len] and file_aux = the magic or
- * the byte offset; file_root is the file's index in the roots section (-1 on
- * error).  Section order: objs, consts, strs, refs, limbs, bytes, roots; the
- * device arena is {image + section_off[i], section_count[i]}. */
-typedef struct {
-  uint8_t*        image;              /* host arena image, sections 256-B aligned */
-  uint64_t        image_bytes;
-  uint64_t        section_off[7];
-  int64_t         section_count[7];
-  uint64_t        max_code_len, total_code_units;
-  int64_t         n_files;
-  const int32_t*  file_status;
-  const int32_t*  file_root;
-  const int64_t*  file_aux;
-  const char*     messages;
-  const uint64_t* msg_off;
-  const uint32_t* msg_len;
-} upy_pyc_batch;
-
-/* Returns 0 on success (per-file failures are in the batch), 1 on bad arguments. */
-int upy_pyc_load(const uint8_t* const* data, const uint64_t* sizes, int64_t n_files, int n_threads,
-                 upy_pyc_batch** out);
-void upy_pyc_free(upy_pyc_batch* batch);
 
 #ifdef __cplusplus
 }

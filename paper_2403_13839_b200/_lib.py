@@ -43,8 +43,10 @@ def load():
     lib.upy_decode_batch.restype = C.c_int
     lib.upy_decode_batch.argtypes = [C.POINTER(_abi.UpyArena), C.c_void_p, C.c_void_p, C.c_void_p]
     lib.upy_pyc_load.restype = C.c_int
-    lib.upy_pyc_load.argtypes = [C.POINTER(C.c_void_p), C.POINTER(C.c_uint64), C.c_int64, C.c_int,
+    lib.upy_pyc_load.argtypes = [C.POINTER(C.c_void_p), C.POINTER(C.c_uint64), C.c_int64, C.c_int, C.c_int,
                                  C.POINTER(C.POINTER(_abi.UpyPycBatch))]
+    lib.upy_pyc_write_image.restype = C.c_int
+    lib.upy_pyc_write_image.argtypes = [C.POINTER(_abi.UpyPycBatch), C.c_void_p, C.c_uint64]
     lib.upy_pyc_free.restype = None
     lib.upy_pyc_free.argtypes = [C.POINTER(_abi.UpyPycBatch)]
     _lib = lib

@@ -11,6 +11,7 @@ limits; nothing is ever computed on the CPU.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -18,6 +19,11 @@ import numpy as np
 from . import _abi, _lib
 from .arena import Arena, pack
 from .errors import RETRYABLE, ST_OK, DeviceCapacityError, make_exception
+
+
+# decompile-kernel schedule (upy_options.schedule): 0 = per-thread root queue,
+# 1 = warp-lockstep stages
+DEFAULT_SCHEDULE = int(os.environ.get("UPY_SCHEDULE", "0"))
 
 
 def _torch():
@@ -56,17 +62,20 @@ class DeviceArena:
     `run()` on HBM-resident inputs and `upload()+run()+fetch()` end to end)."""
 
     def __init__(self, arena: Arena, style=None, device=None, text_cap=None, arena_bytes=0, slots=0,
-                 threads_per_block=0, pinned=None):
+                 threads_per_block=0, pinned=None, schedule=None):
         torch = _torch()
         self.torch = torch
         self.lib = _lib.load()
         self.arena = arena
         self.device = torch.device(device or "cuda")
+        if pinned is None:
+            pinned = getattr(arena, "pinned", None)  # image already page-locked (loader.load_pyc_batch)
         self.host = pinned if pinned is not None else torch.from_numpy(arena.blob).pin_memory()
         self.dev = torch.empty(self.host.numel(), dtype=torch.uint8, device=self.device)
         self.A = _abi.arena_struct(arena, self.dev.data_ptr())
         self.opts = _abi.options(style, arena_bytes=arena_bytes, slots=slots,
-                                 threads_per_block=threads_per_block)
+                                 threads_per_block=threads_per_block,
+                                 schedule=DEFAULT_SCHEDULE if schedule is None else schedule)
         ws = C.c_size_t(0)
         _lib.check(self.lib.upy_query_workspace(C.byref(self.A), C.byref(self.opts), C.byref(ws)),
                    "upy_query_workspace")

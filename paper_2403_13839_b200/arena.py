@@ -59,6 +59,7 @@ class Arena:
         self.counts = counts            # section -> element count
         self.max_code_len = int(max_code_len)
         self.total_code_units = int(total_code_units)
+        self.pinned = None               # optional page-locked torch view of blob
 
     def section(self, name):
         dt = {"objs": OBJ_DTYPE, "consts": CONST_DTYPE, "strs": STR_DTYPE, "refs": np.dtype("<u4"),

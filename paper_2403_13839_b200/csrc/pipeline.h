@@ -115,9 +115,8 @@ struct Validator {
   }
 };
 
-// function_tree / module_tree (pipeline.py:121-140)
-HD NOINL NV* root_tree(Dc* C, u32 oi) {
-  NV* body = decompile_body(C, oi);
+// function_tree / module_tree (pipeline.py:121-140) around a decompiled body
+HD NOINL NV* root_tree_of(Dc* C, u32 oi, NV* body) {
   CKR(C, nullptr);
   if (s_eqc(obj_name(C, oi), "<module>")) {
     if (body->n && is_k(body->d[0], S_ASSIGN)) {
@@ -143,14 +142,27 @@ HD NOINL NV* root_tree(Dc* C, u32 oi) {
   return nv1(C, fn);
 }
 
-// decompile_source (pipeline.py:143-160) + emit_module (emitter.py:535-547)
-HD NOINL void decompile_source(Dc* C, u32 oi, const EmitOpts* opt, Text* out) {
+HD inline NV* root_tree(Dc* C, u32 oi) { return root_tree_of(C, oi, decompile_body(C, oi)); }
+
+// decompile_source (pipeline.py:143-160) + emit_module (emitter.py:535-547) as
+// stages: validate | analyze | structure | finish + tree | emit.  The kernel
+// either runs them back to back per thread or in warp lockstep.
+enum { DS_VALIDATE, DS_ANALYZE, DS_STRUCTURE, DS_FINISH, DS_EMIT, DS_STAGES };
+struct SourceJob {
+  u32 oi;
+  BodyJob body;
+  NV* tree;
+  const EmitOpts* opt;
+  Text* out;
+};
+
+HD NOINL void ds_validate(Dc* C, SourceJob* S) {
   Validator V;
   V.C = C;
   V.rep = {nullptr, 0, 0};
   V.n_viol = 0;
   V.path_n = 0;
-  V.one(oi, Str{"", 0});
+  V.one(S->oi, Str{"", 0});
   if (C->err) return;
   if (V.n_viol) {
     Text m;
@@ -159,19 +171,22 @@ HD NOINL void decompile_source(Dc* C, u32 oi, const EmitOpts* opt, Text* out) {
       m_putn(C, &m, V.rep.d, V.rep.n);
       fail_end(C, &m);
     }
-    return;
   }
-  NV* tree = root_tree(C, oi);
-  CK(C);
+}
+
+HD NOINL void ds_emit(Dc* C, SourceJob* S) {
+  u32 oi = S->oi;
+  NV* tree = S->tree;
+  Text* out = S->out;
   t_grow(C, out, 3 * obj_at(C, oi)->code_len + 256);  // text is ~1.5-4.5x co_code
   Emitter E;
   E.C = C;
   E.out = out;
   E.depth = 0;
-  E.indent = opt->indent;
-  if (opt->header) {
+  E.indent = S->opt->indent;
+  if (S->opt->header) {
     t_puts(C, out, "# decompiled by ");
-    t_str(C, out, opt->tool);
+    t_str(C, out, S->opt->tool);
     t_puts(C, out, " from ");
     Str qn = obj_qualname(C, oi);
     t_str(C, out, qn.n ? qn : obj_name(C, oi));
@@ -181,4 +196,34 @@ HD NOINL void decompile_source(Dc* C, u32 oi, const EmitOpts* opt, Text* out) {
   }
   if (!tree->n) E.simple_line("pass");
   for (u32 q = 0; q < tree->n && !C->err; q++) E.stmt(tree->d[q]);
+}
+
+// one stage of the root object; the root body holds one depth-guard level
+// across its stages, like decompile_body's GUARD
+HD inline void ds_stage(Dc* C, SourceJob* S, int stage) {
+  if (C->err) return;
+  switch (stage) {
+    case DS_VALIDATE: ds_validate(C, S); return;
+    case DS_ANALYZE:
+      S->body.oi = S->oi;
+      if (++C->depth > C->max_depth) fail_msg(C, UPY_ST_DEPTH_LIMIT, "device recursion guard");
+      else body_analyze(C, &S->body);
+      return;
+    case DS_STRUCTURE: body_structure(C, &S->body); return;
+    case DS_FINISH:
+      if (body_finish(C, &S->body)) {
+        C->depth--;
+        S->tree = root_tree_of(C, S->oi, S->body.stmts);
+      }
+      return;
+    case DS_EMIT: ds_emit(C, S); return;
+  }
+}
+
+HD inline void decompile_source(Dc* C, u32 oi, const EmitOpts* opt, Text* out) {
+  SourceJob S;
+  S.oi = oi;
+  S.opt = opt;
+  S.out = out;
+  for (int st = 0; st < DS_STAGES; st++) ds_stage(C, &S, st);
 }

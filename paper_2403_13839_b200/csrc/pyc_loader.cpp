@@ -36,6 +36,7 @@
 // Python str repr in error messages) gets its own namespace.
 namespace pyc_host {
 #include "numfmt.h"
+#include "../../include/upy_pyc.h"
 }  // namespace pyc_host
 using namespace pyc_host;
 
@@ -691,33 +692,98 @@ u64 al(u64 x, u64 a) { return (x + a - 1) / a * a; }
 
 struct upy_pyc_batch_impl {
   upy_pyc_batch pub;  // first member: the public handle points here
-  u8* image = nullptr;
-  std::vector<i32> status, root;
+  u8* image = nullptr;  // owned when materialised by upy_pyc_load
+  int n_threads = 0;
+  std::vector<ThreadOut> outs;
+  std::vector<u64> b_obj, b_const, b_str, b_ref, b_limb, b_code, b_rest;
+  u64 code_end = 0, offs[S_N] = {}, ends[S_N] = {}, total = 0;
+  std::vector<i32> status, root, pos;  // root: object index; pos: position in the roots section
   std::vector<i64> aux;
   std::vector<u64> msg_off;
   std::vector<u32> msg_len;
   std::string messages;
   ~upy_pyc_batch_impl() { free(image); }
+  void write(u8* img) const;
 };
 
+// Concatenate the workers' sections into img (total bytes), rebasing every index.
+void upy_pyc_batch_impl::write(u8* img) const {
+  for (int s = 0; s < S_N; s++) memset(img + ends[s], 0, (s + 1 < S_N ? offs[s + 1] : total) - ends[s]);
+  upy_obj* objs = (upy_obj*)(img + offs[S_OBJS]);
+  upy_const* consts = (upy_const*)(img + offs[S_CONSTS]);
+  upy_str* strs = (upy_str*)(img + offs[S_STRS]);
+  u32* refs = (u32*)(img + offs[S_REFS]);
+  u32* limbs = (u32*)(img + offs[S_LIMBS]);
+  u8* bytes = img + offs[S_BYTES];
+  i32* roots = (i32*)(img + offs[S_ROOTS]);
+  for (i64 f = 0, r = 0; f < pub.n_files; f++)
+    if (status[f] == UPY_ST_OK) roots[r++] = root[f];
+  std::vector<std::thread> pool;
+  for (int t = 0; t < n_threads; t++)
+    pool.emplace_back([&, t] {
+      const ThreadOut& T = outs[t];
+      u64 rest_base = code_end + b_rest[t];
+      for (size_t i = 0; i < T.objs.size(); i++) {
+        upy_obj o = T.objs[i];
+        o.code_off += b_code[t];
+        o.exc_off = o.exc_len ? o.exc_off + rest_base : 0;  // empty table: no address
+        o.lnt_off += rest_base;
+        o.consts_off += (u32)b_ref[t];
+        o.names_off += (u32)b_ref[t];
+        o.varnames_off += (u32)b_ref[t];
+        o.freevars_off += (u32)b_ref[t];
+        o.cellvars_off += (u32)b_ref[t];
+        o.name += (u32)b_str[t];
+        o.filename += (u32)b_str[t];
+        o.qualname += (u32)b_str[t];
+        objs[b_obj[t] + i] = o;
+      }
+      for (size_t i = 0; i < T.consts.size(); i++) {
+        upy_const c = T.consts[i];
+        switch (c.kind) {
+          case UPY_C_STR: case UPY_C_BYTES: c.off += c.pad ? b_code[t] : rest_base; c.pad = 0; break;
+          case UPY_C_INT: c.off += b_limb[t]; break;
+          case UPY_C_TUPLE: case UPY_C_FROZENSET: c.off += b_ref[t]; break;
+          case UPY_C_CODE: c.off += b_obj[t]; break;
+          default: break;
+        }
+        consts[b_const[t] + i] = c;
+      }
+      for (size_t i = 0; i < T.strs.size(); i++) {
+        upy_str s = T.strs[i];
+        s.off += rest_base;
+        strs[b_str[t] + i] = s;
+      }
+      const u32 cb = (u32)b_const[t], sb = (u32)b_str[t];
+      for (size_t i = 0; i < T.refs.size(); i++) refs[b_ref[t] + i] = T.refs[i] + (T.ref_is_str[i] ? sb : cb);
+      if (!T.limbs.empty()) memcpy(limbs + b_limb[t], T.limbs.data(), T.limbs.size() * 4);
+      if (!T.code.empty()) memcpy(bytes + b_code[t], T.code.data(), T.code.size());
+      if (!T.rest.empty()) memcpy(bytes + rest_base, T.rest.data(), T.rest.size());
+    });
+  for (auto& th : pool) th.join();
+}
+
 extern "C" int upy_pyc_load(const uint8_t* const* data, const uint64_t* sizes, int64_t n_files, int n_threads,
-                            upy_pyc_batch** out) {
+                            int flags, upy_pyc_batch** out) {
   if (!out || n_files < 0 || (n_files && (!data || !sizes))) return 1;
   if (n_threads <= 0) {
     unsigned hc = std::thread::hardware_concurrency();
     n_threads = hc ? (int)hc : 1;
   }
   if ((i64)n_threads > n_files) n_threads = (int)(n_files ? n_files : 1);
+  upy_pyc_batch_impl* B = new upy_pyc_batch_impl();
+  B->n_threads = n_threads;
+  B->pub.n_files = n_files;
   // contiguous slices of files per worker (file order is kept inside a slice)
   std::vector<i64> lo(n_threads + 1);
   for (int t = 0; t <= n_threads; t++) lo[t] = n_files * t / n_threads;
-  std::vector<ThreadOut> outs((size_t)n_threads);
+  B->outs.resize((size_t)n_threads);
   std::vector<FileRes> res((size_t)n_files);
   {
     std::vector<std::thread> pool;
     for (int t = 0; t < n_threads; t++)
       pool.emplace_back([&, t] {
-        ThreadOut& T = outs[t];
+        ThreadOut& T = B->outs[t];
         u64 in_bytes = 0;
         for (i64 f = lo[t]; f < lo[t + 1]; f++) in_bytes += sizes[f];
         T.rest.reserve(in_bytes);
@@ -729,54 +795,29 @@ extern "C" int upy_pyc_load(const uint8_t* const* data, const uint64_t* sizes, i
     for (auto& th : pool) th.join();
   }
   // section sizes and per-thread bases
-  std::vector<u64> b_obj(n_threads + 1), b_const(n_threads + 1), b_str(n_threads + 1), b_ref(n_threads + 1),
-      b_limb(n_threads + 1), b_code(n_threads + 1), b_rest(n_threads + 1);
+  for (auto* v : {&B->b_obj, &B->b_const, &B->b_str, &B->b_ref, &B->b_limb, &B->b_code, &B->b_rest})
+    v->assign(n_threads + 1, 0);
   u64 max_code = 0;
   for (int t = 0; t < n_threads; t++) {
-    const ThreadOut& T = outs[t];
-    b_obj[t + 1] = b_obj[t] + T.objs.size();
-    b_const[t + 1] = b_const[t] + T.consts.size();
-    b_str[t + 1] = b_str[t] + T.strs.size();
-    b_ref[t + 1] = b_ref[t] + T.refs.size();
-    b_limb[t + 1] = b_limb[t] + T.limbs.size();
-    b_code[t + 1] = b_code[t] + T.code.size();
-    b_rest[t + 1] = b_rest[t] + T.rest.size();
+    const ThreadOut& T = B->outs[t];
+    B->b_obj[t + 1] = B->b_obj[t] + T.objs.size();
+    B->b_const[t + 1] = B->b_const[t] + T.consts.size();
+    B->b_str[t + 1] = B->b_str[t] + T.strs.size();
+    B->b_ref[t + 1] = B->b_ref[t] + T.refs.size();
+    B->b_limb[t + 1] = B->b_limb[t] + T.limbs.size();
+    B->b_code[t + 1] = B->b_code[t] + T.code.size();
+    B->b_rest[t + 1] = B->b_rest[t] + T.rest.size();
     if (T.max_code > max_code) max_code = T.max_code;
   }
-  u64 n_roots = 0;
-  for (i64 f = 0; f < n_files; f++) n_roots += res[(size_t)f].status == UPY_ST_OK;
-  u64 code_end = b_code[n_threads];
-  u64 counts[S_N] = {b_obj[n_threads], b_const[n_threads], b_str[n_threads], b_ref[n_threads], b_limb[n_threads],
-                     code_end + b_rest[n_threads], n_roots};
-  const u64 esz[S_N] = {sizeof(upy_obj), sizeof(upy_const), sizeof(upy_str), 4, 4, 1, 4};
-  u64 offs[S_N], ends[S_N], total = 0;
-  for (int s = 0; s < S_N; s++) {
-    offs[s] = total;
-    ends[s] = total + counts[s] * esz[s];
-    total = al(ends[s], 256);
-  }
-  if (total < 256) total = 256;
-  upy_pyc_batch_impl* B = new upy_pyc_batch_impl();
-  B->image = (u8*)malloc(total);
-  if (!B->image) {
-    delete B;
-    return 2;
-  }
-  u8* img = B->image;
-  for (int s = 0; s < S_N; s++) memset(img + ends[s], 0, (s + 1 < S_N ? offs[s + 1] : total) - ends[s]);
-  upy_obj* objs = (upy_obj*)(img + offs[S_OBJS]);
-  upy_const* consts = (upy_const*)(img + offs[S_CONSTS]);
-  upy_str* strs = (upy_str*)(img + offs[S_STRS]);
-  u32* refs = (u32*)(img + offs[S_REFS]);
-  u32* limbs = (u32*)(img + offs[S_LIMBS]);
-  u8* bytes = img + offs[S_BYTES];
-  i32* roots = (i32*)(img + offs[S_ROOTS]);
+  B->code_end = B->b_code[n_threads];
   B->status.resize(n_files);
   B->root.resize(n_files);
+  B->pos.resize(n_files);
   B->aux.resize(n_files);
   B->msg_off.resize(n_files);
   B->msg_len.resize(n_files);
   u64 r = 0;
+  std::vector<i32> root_obj((size_t)n_files, -1);
   for (int t = 0; t < n_threads; t++)
     for (i64 f = lo[t]; f < lo[t + 1]; f++) {
       const FileRes& R = res[(size_t)f];
@@ -785,72 +826,57 @@ extern "C" int upy_pyc_load(const uint8_t* const* data, const uint64_t* sizes, i
       B->msg_off[f] = B->messages.size();
       B->msg_len[f] = (u32)R.msg.size();
       B->messages += R.msg;
-      B->root[f] = R.status == UPY_ST_OK ? (i32)r : -1;
-      if (R.status == UPY_ST_OK) roots[r++] = (i32)(b_obj[t] + R.root);
+      if (R.status == UPY_ST_OK) {
+        B->root[f] = (i32)(B->b_obj[t] + R.root);
+        B->pos[f] = (i32)r++;
+      } else {
+        B->root[f] = B->pos[f] = -1;
+      }
     }
-  {
-    std::vector<std::thread> pool;
-    for (int t = 0; t < n_threads; t++)
-      pool.emplace_back([&, t] {
-        const ThreadOut& T = outs[t];
-        u64 rest_base = code_end + b_rest[t];
-        for (size_t i = 0; i < T.objs.size(); i++) {
-          upy_obj o = T.objs[i];
-          o.code_off += b_code[t];
-          o.exc_off = o.exc_len ? o.exc_off + rest_base : 0;  // empty table: no address
-          o.lnt_off += rest_base;
-          o.consts_off += (u32)b_ref[t];
-          o.names_off += (u32)b_ref[t];
-          o.varnames_off += (u32)b_ref[t];
-          o.freevars_off += (u32)b_ref[t];
-          o.cellvars_off += (u32)b_ref[t];
-          o.name += (u32)b_str[t];
-          o.filename += (u32)b_str[t];
-          o.qualname += (u32)b_str[t];
-          objs[b_obj[t] + i] = o;
-        }
-        for (size_t i = 0; i < T.consts.size(); i++) {
-          upy_const c = T.consts[i];
-          switch (c.kind) {
-            case UPY_C_STR: case UPY_C_BYTES: c.off += c.pad ? b_code[t] : rest_base; c.pad = 0; break;
-            case UPY_C_INT: c.off += b_limb[t]; break;
-            case UPY_C_TUPLE: case UPY_C_FROZENSET: c.off += b_ref[t]; break;
-            case UPY_C_CODE: c.off += b_obj[t]; break;
-            default: break;
-          }
-          consts[b_const[t] + i] = c;
-        }
-        for (size_t i = 0; i < T.strs.size(); i++) {
-          upy_str s = T.strs[i];
-          s.off += rest_base;
-          strs[b_str[t] + i] = s;
-        }
-        const u32 cb = (u32)b_const[t], sb = (u32)b_str[t];
-        for (size_t i = 0; i < T.refs.size(); i++) refs[b_ref[t] + i] = T.refs[i] + (T.ref_is_str[i] ? sb : cb);
-        if (!T.limbs.empty()) memcpy(limbs + b_limb[t], T.limbs.data(), T.limbs.size() * 4);
-        if (!T.code.empty()) memcpy(bytes + b_code[t], T.code.data(), T.code.size());
-        if (!T.rest.empty()) memcpy(bytes + rest_base, T.rest.data(), T.rest.size());
-      });
-    for (auto& th : pool) th.join();
+  u64 counts[S_N] = {B->b_obj[n_threads], B->b_const[n_threads], B->b_str[n_threads], B->b_ref[n_threads],
+                     B->b_limb[n_threads], B->code_end + B->b_rest[n_threads], r};
+  const u64 esz[S_N] = {sizeof(upy_obj), sizeof(upy_const), sizeof(upy_str), 4, 4, 1, 4};
+  u64 total = 0;
+  for (int s = 0; s < S_N; s++) {
+    B->offs[s] = total;
+    B->ends[s] = total + counts[s] * esz[s];
+    total = al(B->ends[s], 256);
   }
+  B->total = total < 256 ? 256 : total;
   upy_pyc_batch& P = B->pub;
   memset(&P, 0, sizeof P);
-  P.image = img;
-  P.image_bytes = total;
+  P.image_bytes = B->total;
   for (int s = 0; s < S_N; s++) {
-    P.section_off[s] = offs[s];
+    P.section_off[s] = B->offs[s];
     P.section_count[s] = (int64_t)counts[s];
   }
   P.max_code_len = max_code;
-  P.total_code_units = (code_end + 1) / 2;
+  P.total_code_units = (B->code_end + 1) / 2;
   P.n_files = n_files;
   P.file_status = B->status.data();
-  P.file_root = B->root.data();
   P.file_aux = B->aux.data();
   P.messages = B->messages.data();
   P.msg_off = B->msg_off.data();
   P.msg_len = B->msg_len.data();
+  P.file_root = B->pos.data();
+  if (!(flags & UPY_PYC_DEFER_IMAGE)) {
+    B->image = (u8*)malloc(B->total);
+    if (!B->image) {
+      delete B;
+      return 2;
+    }
+    B->write(B->image);
+    P.image = B->image;
+  }
   *out = &B->pub;
+  return 0;
+}
+
+extern "C" int upy_pyc_write_image(upy_pyc_batch* b, uint8_t* dst, uint64_t dst_bytes) {
+  if (!b || !dst) return 1;
+  upy_pyc_batch_impl* B = reinterpret_cast<upy_pyc_batch_impl*>(b);
+  if (dst_bytes < B->total) return 1;
+  B->write(dst);
   return 0;
 }
 

@@ -557,43 +557,62 @@ HD inline bool is_return_none(Dc* C, Node* s) {  // pipeline.py:113-118
   return node_ckind(C, s->a) == UPY_C_NONE;
 }
 
-// decompile_body (pipeline.py:90-110)
-HD NOINL NV* decompile_body(Dc* C, u32 oi) {
-  GUARD(C);
-  CKR(C, nullptr);
-  Code* K = anew<Code>(C);
-  CKR(C, nullptr);
-  u32 defs_before = C->n_defs;
-  if (!load_instructions(C, K, oi)) return nullptr;
-  Cfg* G = analyze(C, K);
-  CKR(C, nullptr);
-  Structurer* S_ = make_structurer(C, K, G);
-  CKR(C, nullptr);
+// decompile_body (pipeline.py:90-110), as stages so the kernel can run a root
+// object's stages in warp lockstep (upy.cu); nested bodies run them back to back.
+struct BodyJob {
+  u32 oi;
+  u32 defs_before;
+  Code* K;
+  Cfg* G;
+  NV* stmts;
+};
+HD NOINL bool body_analyze(Dc* C, BodyJob* J) {  // decode check + CFG (pipeline.py:92, 17-54)
+  J->K = anew<Code>(C);
+  CKR(C, false);
+  J->defs_before = C->n_defs;
+  if (!load_instructions(C, J->K, J->oi)) return false;
+  J->G = analyze(C, J->K);
+  return !C->err;
+}
+HD NOINL bool body_structure(Dc* C, BodyJob* J) {  // Structurer + canonicalize (pipeline.py:93-95)
+  Structurer* S_ = make_structurer(C, J->K, J->G);
+  CKR(C, false);
   NV* stmts = S_->structure();
-  CKR(C, nullptr);
-  stmts = canonicalize_tree(C, stmts);
-  CKR(C, nullptr);
+  CKR(C, false);
+  J->stmts = canonicalize_tree(C, stmts);
+  return !C->err;
+}
+HD NOINL bool body_finish(Dc* C, BodyJob* J) {  // DefRecovery, scope decls, implicit return (:96-110)
+  NV* stmts = J->stmts;
   // DefRecovery (recover.py:81-227) only ever changes a tree through FuncExpr
   // and BuildClass nodes (pre/post hooks, _match_def); everything else it does
   // is rebuilding lists with identical contents.  When the simulation of this
   // object created neither, the pass is skipped: the output is identical.
-  if (C->n_defs != defs_before) {
+  if (C->n_defs != J->defs_before) {
     Recovery R;
     R.C = C;
-    R.oi = oi;
+    R.oi = J->oi;
     R.hoisted = vnew<Node*>(C);
     R.lambda_counter = 0;
     stmts = R.rewrite_block(stmts);
-    CKR(C, nullptr);
+    CKR(C, false);
   }
-  stmts = add_scope_decls(C, stmts, oi);
-  CKR(C, nullptr);
-  const upy_obj* o = obj_at(C, oi);
+  stmts = add_scope_decls(C, stmts, J->oi);
+  CKR(C, false);
+  const upy_obj* o = obj_at(C, J->oi);
   if (o->flags & (0x20 | 0x200)) {
     while (stmts->n && is_return_none(C, vlast(stmts))) stmts->n--;
   } else if (stmts->n && is_return_none(C, vlast(stmts))) {
     stmts->n--;
   }
+  J->stmts = stmts;
+  return !C->err;
+}
+HD NOINL NV* decompile_body(Dc* C, u32 oi) {
+  GUARD(C);
   CKR(C, nullptr);
-  return stmts;
+  BodyJob J;
+  J.oi = oi;
+  if (!body_analyze(C, &J) || !body_structure(C, &J) || !body_finish(C, &J)) return nullptr;
+  return J.stmts;
 }

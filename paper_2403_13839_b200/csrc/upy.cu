@@ -32,6 +32,7 @@ struct KParams {
   u32* next_root;
   int header;
   int max_depth;
+  int schedule;  // 0: per-thread root queue, 1: warp-lockstep stages
   int indent_len, tool_len;
   char indent[64];
   char tool[64];
@@ -40,6 +41,55 @@ struct KParams {
 #ifndef UPY_MINB
 #define UPY_MINB 8  // <= 64 registers: 32 resident warps per SM (measured +43% vs unbounded)
 #endif
+// Per-thread state reset for a new root object.
+__device__ __forceinline__ void dc_reset(Dc& C, const KParams& P, u8* base) {
+  C.msg = (char*)base;
+  C.msg_len = 0;
+  C.msg_cap = MSG_BYTES;
+  C.sink = base + MSG_BYTES;
+  C.base = base + SLOT_HEADER;
+  C.cap = P.slot_bytes - SLOT_HEADER;
+  C.used = 0;
+  C.top = C.cap;
+  C.low_top = C.cap;
+  C.err = 0;
+  C.aux0 = C.aux1 = 0;
+  C.A = &P.A;
+  C.ins_all = P.ins;
+  C.dec_all = P.dec;
+  C.depth = 0;
+  C.max_depth = P.max_depth;
+  C.n_defs = 0;
+}
+
+// Text (or the error message) of root r into the flat output buffer.
+__device__ __forceinline__ void emit_result(const KParams& P, Dc& C, u32 r, const Text& out) {
+  const char* src;
+  u32 len;
+  if (C.err) {
+    src = C.msg;
+    len = C.msg_len;
+  } else {
+    src = out.d;
+    len = out.n;
+  }
+  int status = C.err;
+  // reservations are 16-byte granular so the copy-out is whole uint4 stores
+  u64 resv = ((u64)len + 15) & ~(u64)15;
+  u64 off = atomicAdd((unsigned long long*)P.out.text_used, (unsigned long long)resv);
+  if (off + resv > P.out.text_cap) {
+    status = UPY_ST_OUTPUT_OVERFLOW;
+    len = 0;
+  } else if (len) {
+    copy16(P.out.text + off, src, len);
+  }
+  P.out.text_off[r] = off;
+  P.out.text_len[r] = len;
+  P.out.status[r] = status;
+  P.out.aux[2 * (u64)r] = C.aux0;
+  P.out.aux[2 * (u64)r + 1] = C.aux1;
+}
+
 __global__ void __launch_bounds__(128, UPY_MINB) upy_decompile_kernel(KParams P) {
   const u64 slot = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   u8* base = P.slots_base + slot * P.slot_bytes;
@@ -52,53 +102,42 @@ __global__ void __launch_bounds__(128, UPY_MINB) upy_decompile_kernel(KParams P)
   // stack takes those accesses off the L1/L2/DRAM path.
   __shared__ Dc dcs[128];
   Dc& C = dcs[threadIdx.x];
-  while (true) {
-    u32 r = atomicAdd(P.next_root, 1u);
-    if (r >= (u64)P.A.n_roots) break;
-    u32 oi = (u32)P.A.roots[r];
-    C.msg = (char*)base;
-    C.msg_len = 0;
-    C.msg_cap = MSG_BYTES;
-    C.sink = base + MSG_BYTES;
-    C.base = base + SLOT_HEADER;
-    C.cap = P.slot_bytes - SLOT_HEADER;
-    C.used = 0;
-    C.top = C.cap;
-    C.low_top = C.cap;
-    C.err = 0;
-    C.aux0 = C.aux1 = 0;
-    C.A = &P.A;
-    C.ins_all = P.ins;
-    C.dec_all = P.dec;
-    C.depth = 0;
-    C.max_depth = P.max_depth;
-    C.n_defs = 0;
-    Text out = {nullptr, 0, 0};
-    decompile_source(&C, oi, &opt, &out);
-    const char* src;
-    u32 len;
-    if (C.err) {
-      src = C.msg;
-      len = C.msg_len;
-    } else {
-      src = out.d;
-      len = out.n;
+  const u64 n_roots = (u64)P.A.n_roots;
+  if (P.schedule == 0) {
+    // each thread takes the next root from the global queue
+    while (true) {
+      u32 r = atomicAdd(P.next_root, 1u);
+      if (r >= n_roots) break;
+      dc_reset(C, P, base);
+      Text out = {nullptr, 0, 0};
+      decompile_source(&C, (u32)P.A.roots[r], &opt, &out);
+      emit_result(P, C, r, out);
     }
-    int status = C.err;
-    // reservations are 16-byte granular so the copy-out is whole uint4 stores
-    u64 resv = ((u64)len + 15) & ~(u64)15;
-    u64 off = atomicAdd((unsigned long long*)P.out.text_used, (unsigned long long)resv);
-    if (off + resv > P.out.text_cap) {
-      status = UPY_ST_OUTPUT_OVERFLOW;
-      len = 0;
-    } else if (len) {
-      copy16(P.out.text + off, src, len);
+  } else {
+    // warp lockstep: a warp takes 32 consecutive roots and runs each stage of
+    // decompile_source for all of them before the next stage, so the lanes
+    // execute the same code (instruction cache, SIMT efficiency)
+    const int lane = threadIdx.x & 31;
+    while (true) {
+      u32 b0 = 0;
+      if (lane == 0) b0 = atomicAdd(P.next_root, 32u);
+      b0 = __shfl_sync(0xffffffffu, b0, 0);
+      if (b0 >= n_roots) break;
+      u32 r = b0 + lane;
+      bool have = r < n_roots;
+      dc_reset(C, P, base);
+      Text out = {nullptr, 0, 0};
+      SourceJob S;
+      S.oi = have ? (u32)P.A.roots[r] : 0;
+      S.opt = &opt;
+      S.out = &out;
+      for (int st = 0; st < DS_STAGES; st++) {
+        if (have) ds_stage(&C, &S, st);
+        __syncwarp();
+      }
+      if (have) emit_result(P, C, r, out);
+      __syncwarp();
     }
-    P.out.text_off[r] = off;
-    P.out.text_len[r] = len;
-    P.out.status[r] = status;
-    P.out.aux[2 * (u64)r] = C.aux0;
-    P.out.aux[2 * (u64)r + 1] = C.aux1;
   }
 }
 
@@ -114,6 +153,13 @@ static int sm_count() {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
   return n;
+}
+
+// threads per block: <= 128 (shared Dc array), whole warps (the lockstep
+// schedule shuffles across all 32 lanes)
+static int eff_tpb(const upy_options* o) {
+  int tpb = o && o->threads_per_block > 0 && o->threads_per_block < 128 ? o->threads_per_block : 128;
+  return tpb < 32 ? 32 : tpb & ~31;
 }
 
 static WsLayout layout(const upy_arena* a, const upy_options* o) {
@@ -139,7 +185,7 @@ static WsLayout layout(const upy_arena* a, const upy_options* o) {
   }
   if (slots > (u64)a->n_roots) slots = (u64)a->n_roots;
   if (slots < 1) slots = 1;
-  int tpb = o && o->threads_per_block > 0 && o->threads_per_block < 128 ? o->threads_per_block : 128;
+  int tpb = eff_tpb(o);
   slots = (slots + tpb - 1) / tpb * tpb;
   L.slots = slots;
   L.total = L.slots_off + slots * sb;
@@ -231,6 +277,7 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
   P.slot_bytes = L.slot_bytes;
   P.next_root = ctr;
   P.max_depth = 600;
+  P.schedule = opt ? opt->schedule : 0;
   if (opt) {
     P.header = opt->header;
     P.indent_len = opt->indent_len > 64 ? 64 : opt->indent_len;
@@ -243,7 +290,7 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
     P.tool_len = 6;
     memcpy(P.tool, "unpyre", 6);
   }
-  int tpb = opt && opt->threads_per_block > 0 && opt->threads_per_block < 128 ? opt->threads_per_block : 128;
+  int tpb = eff_tpb(opt);
   unsigned blocks = (unsigned)(L.slots / tpb);
   upy_decompile_kernel<<<blocks, tpb, 0, s>>>(P);
   cudaError_t e = cudaGetLastError();

@@ -21,20 +21,22 @@ from .arena import SECTIONS, Arena, unpack
 from .errors import ST_OK, make_exception
 
 
-def load_pyc_batch(blobs, n_threads=0):
+def load_pyc_batch(blobs, n_threads=0, pinned=False):
     """Parse .pyc images into one Arena.  Returns (arena, per_file) where
     per_file[i] is the root position of file i in the arena or the exception
-    instance the reference's load_pyc raises for it."""
+    instance the reference's load_pyc raises for it.  pinned=True writes the
+    image into page-locked memory (torch's caching host allocator, reused across
+    calls) so the H2D copy is a direct DMA."""
     lib = _lib.load()
     blobs = [bytes(b) for b in blobs]
     n = len(blobs)
     bufs = [C.create_string_buffer(b, len(b)) if b else C.create_string_buffer(1) for b in blobs]
     ptrs = (C.c_void_p * max(n, 1))(*[C.addressof(x) for x in bufs])
     sizes = (C.c_uint64 * max(n, 1))(*[len(b) for b in blobs])
-    return _load(lib, ptrs, sizes, n, n_threads)
+    return _load(lib, ptrs, sizes, n, n_threads, pinned)
 
 
-def load_pyc_buffer(buf, offsets, sizes, n_threads=0):
+def load_pyc_buffer(buf, offsets, sizes, n_threads=0, pinned=False):
     """load_pyc_batch over files stored back to back in one buffer (numpy uint8 /
     bytes) at `offsets` with `sizes`: no per-file Python objects at all."""
     lib = _lib.load()
@@ -42,23 +44,30 @@ def load_pyc_buffer(buf, offsets, sizes, n_threads=0):
     offsets = np.asarray(offsets, dtype=np.uint64)
     sizes = np.ascontiguousarray(np.asarray(sizes, dtype=np.uint64))
     ptrs = np.ascontiguousarray(offsets + np.uint64(base.ctypes.data))
-    arena, per_file = _load(lib, ptrs.ctypes.data_as(C.POINTER(C.c_void_p)),
-                            sizes.ctypes.data_as(C.POINTER(C.c_uint64)), len(sizes), n_threads)
-    arena._keep_input = base
-    return arena, per_file
+    return _load(lib, ptrs.ctypes.data_as(C.POINTER(C.c_void_p)), sizes.ctypes.data_as(C.POINTER(C.c_uint64)),
+                 len(sizes), n_threads, pinned)
 
 
-def _load(lib, ptrs, sizes, n, n_threads):
+def _load(lib, ptrs, sizes, n, n_threads, pinned):
     out = C.POINTER(_abi.UpyPycBatch)()
-    rc = lib.upy_pyc_load(ptrs, sizes, n, int(n_threads), C.byref(out))
+    rc = lib.upy_pyc_load(ptrs, sizes, n, int(n_threads), _abi.PYC_DEFER_IMAGE if pinned else 0, C.byref(out))
     _lib.check(rc, "upy_pyc_load")
     b = out.contents
-    # the arena views the library's image (no copy); freed with the arena
-    image = np.ctypeslib.as_array(C.cast(b.image, C.POINTER(C.c_uint8)), shape=(int(b.image_bytes),))
+    host = None
+    if pinned:
+        import torch
+
+        host = torch.empty(int(b.image_bytes), dtype=torch.uint8, pin_memory=True)
+        _lib.check(lib.upy_pyc_write_image(out, C.c_void_p(host.data_ptr()), C.c_uint64(host.numel())),
+                   "upy_pyc_write_image")
+        image = host.numpy()
+    else:
+        # the arena views the library's image (no copy); freed with the arena
+        image = np.ctypeslib.as_array(C.cast(b.image, C.POINTER(C.c_uint8)), shape=(int(b.image_bytes),))
     offsets = {s: int(b.section_off[i]) for i, s in enumerate(SECTIONS)}
     counts = {s: int(b.section_count[i]) for i, s in enumerate(SECTIONS)}
     arena = Arena(image, offsets, counts, int(b.max_code_len), int(b.total_code_units))
-    weakref.finalize(arena, lib.upy_pyc_free, out)
+    arena.pinned = host  # torch pinned tensor (DeviceArena uploads from it directly) or None
     status = np.ctypeslib.as_array(b.file_status, shape=(n,)).copy() if n else np.zeros(0, np.int32)
     per_file = []
     if n and (status == ST_OK).all():
@@ -72,6 +81,10 @@ def _load(lib, ptrs, sizes, n, n_threads):
                 o, ln = int(b.msg_off[i]), int(b.msg_len[i])
                 per_file.append(make_exception(int(status[i]), msgs[o:o + ln].decode("utf-8", "replace"),
                                                (int(b.file_aux[i]), 0)))
+    if pinned:
+        lib.upy_pyc_free(out)
+    else:
+        weakref.finalize(arena, lib.upy_pyc_free, out)
     return arena, per_file
 
 
@@ -90,7 +103,7 @@ def decompile_pyc_many(blobs, style=None, device=None, n_threads=0):
     or the exception the reference's `load_pyc` + `decompile_source` raise."""
     from .api import run_arena
 
-    arena, per_file = load_pyc_batch(blobs, n_threads)
+    arena, per_file = load_pyc_batch(blobs, n_threads, pinned=True)
     out = list(per_file)
     if arena.n_roots:
         vals = run_arena(arena, style, device).values()

@@ -65,8 +65,10 @@ def test_cuda_library_exports_every_declared_symbol():
     import re
 
     lib = ctypes.CDLL(_lib_path("libupy_cuda.so"))
-    with open(os.path.join(ROOT, "include", "upy.h")) as f:
-        declared = set(re.findall(r"\b(upy_[a-z_]+)\s*\(", f.read()))
+    declared = set()
+    for h in sorted(os.listdir(os.path.join(ROOT, "include"))):
+        with open(os.path.join(ROOT, "include", h)) as f:
+            declared |= set(re.findall(r"\b(upy_[a-z_]+)\s*\(", f.read()))
     assert declared == set(_abi.EXPORTS)
     for sym in declared:
         assert hasattr(lib, sym), sym
