@@ -34,6 +34,10 @@ WORKLOADS = {
     "c3_311": ("c3_311", 1_000_000, "C3 (3.11 variant): synthetic 1M code objects x ~200 units + caches"),
     "c4": ("c4_310", 65_536, "C4: synthetic 64K code objects x ~10K units (3.10), nested if/for/while/try"),
     "c4_311": ("c4_311", 65_536, "C4 (3.11 variant): synthetic 64K code objects x ~10K units, exception tables"),
+    # C2 (BASELINE configs[1]): the reference's own syntax corpus, one batch of its 110
+    # modules (nested defs/classes/lambdas/comprehensions decompiled through their roots)
+    "c2": ("c2_310", 110, "C2: the reference's pkg/corpus, 110 modules (+nested code, 3.10) in one batch"),
+    "c2x": ("c2_310", 110 * 4096, "C2 x4096: the reference's pkg/corpus modules (3.10) tiled to 450,560 roots"),
     # C5: one 16M-object corpus split across the ranks (strong scaling)
     "c5": ("c3_310", 16_777_216, "C5: synthetic 16M code objects x ~200 units (3.10) sharded by object across GPUs"),
 }
@@ -293,7 +297,7 @@ def main():
     # ---------------- end to end from .pyc files in host memory:
     # native loader (all host threads) -> H2D -> kernels -> D2H, wall clock
     pyc = None
-    if args.pyc and args.workload in ("c3", "c3_311", "c5"):
+    if args.pyc and args.workload in ("c2", "c2x", "c3", "c3_311", "c5"):
         pyc = pyc_e2e(pool, reps, local, args, pool_name, n_pool, barrier)
 
     # ---------------- max over ranks
@@ -348,6 +352,7 @@ def main():
         "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": {"workload": desc, "objects_per_gpu": n_roots, "objects_total": objs_total,
+                   "code_objects_per_gpu": int(len(arena.section("objs"))),
                    "pool": f"{pool_name} ({n_pool} distinct reference-checked objects tiled x{reps})",
                    "python": POOLS[pool_name]["minor"], "code_bytes_per_gpu": code_bytes,
                    "instructions_per_gpu": n_instr,

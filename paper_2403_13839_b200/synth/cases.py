@@ -24,6 +24,12 @@ def build(spec):
         from . import fuzz
 
         return fuzz.program(spec["seed"], m, **kw)
+    if g == "c2":
+        # compiled from the reference's corpus sources in the build container
+        # (tests/golden/make_c2_golden.py); the fixture carries the tree
+        from . import codejson
+
+        return codejson.from_json(spec["tree"])
     raise KeyError(g)
 
 

@@ -1,6 +1,6 @@
 """Reference digests for the benchmark pools (run in the build container):
 
-    python tests/golden/make_pools.py
+    python tests/golden/make_pools.py [pool ...]   # default: all pools
 
 bench.py tiles a pool of distinct synthetic objects up to the configured
 corpus size and checks EVERY device output against these SHA-256 digests of
@@ -42,9 +42,15 @@ def _digest_range(args):
 
 
 def main():
+    only = sys.argv[1:]
     res = {}
+    if only:
+        with open(os.path.join(HERE, "pools.json")) as f:
+            res = json.load(f)
     with Pool(os.cpu_count()) as p:
         for name, spec in POOLS.items():
+            if only and name not in only:
+                continue
             t0 = time.time()
             n = spec["size"]
             step = max(1, n // (4 * os.cpu_count()))

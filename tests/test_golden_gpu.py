@@ -8,7 +8,7 @@ from helpers import inputs, mismatches, outcome, style_of
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("gset", ["c1", "c3", "c4", "snippets", "fuzz", "mutant"])
+@pytest.mark.parametrize("gset", ["c1", "c2", "c3", "c4", "snippets", "fuzz", "mutant"])
 def test_gpu_matches_reference(gset):
     from paper_2403_13839_b200 import api
 
@@ -33,7 +33,7 @@ def test_gpu_single_decompile_raises_reference_class():
     assert ei.value.offset == 0
 
 
-@pytest.mark.parametrize("gset", ["c4", "fuzz", "mutant", "snippets"])
+@pytest.mark.parametrize("gset", ["c2", "c4", "fuzz", "mutant", "snippets"])
 def test_gpu_lockstep_schedule_matches_reference(gset, monkeypatch):
     """The warp-lockstep schedule (upy_options.schedule = 1) runs the same stages
     in a different order across threads; results must be identical."""
@@ -49,3 +49,14 @@ def test_gpu_lockstep_schedule_matches_reference(gset, monkeypatch):
         got = [outcome(v) for v in api.decompile_many(inputs(group), style_of(group[0]))]
         bad += mismatches(group, got)
     assert not bad, bad[:3]
+
+
+def test_gpu_c2_from_pyc_images_matches_reference():
+    """C2 modules as .pyc images (synth/marshal.py) through the native loader and
+    the kernels: same text as the reference decompiling the compiled tree."""
+    from paper_2403_13839_b200 import loader
+    from paper_2403_13839_b200.synth import marshal
+
+    recs = [r for r in golden_cases(["c2"]) if not r.get("style")]
+    got = [outcome(v) for v in loader.decompile_pyc_many([marshal.dump_pyc(co) for co in inputs(recs)])]
+    assert not mismatches(recs, got)

@@ -11,7 +11,7 @@ from helpers import inputs, style_of
 from oracle import port
 
 
-@pytest.mark.parametrize("gset", ["c1", "c3", "c4", "snippets", "fuzz", "mutant"])
+@pytest.mark.parametrize("gset", ["c1", "c2", "c3", "c4", "snippets", "fuzz", "mutant"])
 def test_oracle_matches_reference_goldens(gset):
     recs = golden_cases([gset])
     bad = []
