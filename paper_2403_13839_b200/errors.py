@@ -37,6 +37,14 @@ class MalformedMarshal(UnpyreError):
         self.offset = offset
 
 
+class SchemaError(UnpyreError):
+    """JSON code-object dump does not match the schema (errors.py:37-40)."""
+
+    def __init__(self, message, path):
+        super().__init__(f"{message} (at {path})")
+        self.path = path
+
+
 class UnknownOpcode(UnpyreError):
     def __init__(self, opcode, offset):
         super().__init__(f"unknown opcode {opcode} at offset {offset}")

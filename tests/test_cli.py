@@ -1,0 +1,78 @@
+"""Batch CLI (paper_2403_13839_b200/cli.py) against runs of the
+REAL reference CLI recorded in tests/golden/cli.jsonl (make_cli_golden.py):
+same exit codes, stdout, stderr and written files.  verify's elapsed-time
+line / field is masked.  GPU tier (the decompile batches run on the device);
+the JSON-dump reader is checked on CPU."""
+import base64
+import contextlib
+import io
+import json
+import os
+import re
+
+import pytest
+
+from conftest import load_golden
+
+
+def _mask(s):
+    s = re.sub(r"total (\d+) cases in [0-9.]+s", r"total \1 cases in Xs", s)
+    return re.sub(r'"elapsed_seconds": [0-9.]+', '"elapsed_seconds": X', s)
+
+
+def _run(tmp_path, rec):
+    from paper_2403_13839_b200 import cli
+
+    for rel, b64 in rec["files"].items():
+        p = tmp_path / rel
+        p.parent.mkdir(parents=True, exist_ok=True)
+        p.write_bytes(base64.b64decode(b64))
+    out, err = io.StringIO(), io.StringIO()
+    cwd = os.getcwd()
+    os.chdir(tmp_path)
+    os.environ["UNPYRE_COLOR"] = "never"
+    try:
+        with contextlib.redirect_stdout(out), contextlib.redirect_stderr(err):
+            rc = cli.main(rec["argv"])
+    finally:
+        os.chdir(cwd)
+    produced = {}
+    if (tmp_path / "outdir").is_dir():
+        for fn in sorted(os.listdir(tmp_path / "outdir")):
+            produced[f"outdir/{fn}"] = (tmp_path / "outdir" / fn).read_text(encoding="utf-8")
+    return rc, out.getvalue(), err.getvalue(), produced
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rec", load_golden("cli"), ids=lambda r: r["case"])
+def test_cli_matches_reference_cli(tmp_path, rec):
+    rc, out, err, produced = _run(tmp_path, rec)
+    assert rc == rec["rc"]
+    assert _mask(out) == _mask(rec["stdout"])
+    assert _mask(err) == _mask(rec["stderr"])
+    assert produced == rec["out_files"]
+
+
+def test_json_dump_reader_roundtrip_and_schema_errors():
+    from paper_2403_13839_b200 import errors, jsondump
+    from paper_2403_13839_b200.synth import codejson
+
+    from helpers import code_key
+
+    recs = [r for r in load_golden("c2") if not r.get("style")][:20]
+    for r in recs:
+        co = codejson.from_json(r["tree"])
+        (back,) = jsondump.load_json_dump(jsondump.dumps(co))
+        assert code_key(back) == code_key(co)
+    # the schema errors the reference's CLI reported for the broken dumps
+    want = {}
+    for rec in load_golden("cli"):
+        for line in rec["stderr"].splitlines():
+            m = re.match(r"(\w+\.json): SchemaError: (.*)$", line)
+            if m:
+                want[m.group(1)] = (m.group(2), base64.b64decode(rec["files"][m.group(1)]))
+    assert len(want) >= 3
+    for name, (msg, data) in want.items():
+        with pytest.raises(errors.SchemaError) as ei:
+            jsondump.load_json_dump(data.decode())
+        assert str(ei.value) == msg, name
