@@ -3,8 +3,9 @@
 // decode_scalar: one thread walks the object in reference order (used for
 //   3.11 objects, whose cache-unit skipping makes instruction starts a serial
 //   chain, and by the host harness).
-// decode_warp:   one warp per object for 3.8-3.10 (no caches: every unit is an
-//   instruction unit).  Lanes own 8 consecutive units (one 128-bit load each),
+// decode_chunk:  one warp per object for 3.8-3.10 (no caches: every unit is an
+//   instruction unit), one 256-unit chunk per call (the kernel streams chunks
+//   into shared memory with TMA bulk copies, decode_kernel.cu).  Lanes own 8 consecutive units (one 128-bit load each),
 //   EXTENDED_ARG runs are folded with a warp shuffle scan over (all-prefix,
 //   run length, run value) summaries, record slots come from a popc scan, and
 //   jump targets are validated inline: in <=3.10 an offset is an extent start
@@ -155,234 +156,213 @@ __device__ __forceinline__ ExtRun shfl_run(ExtRun x, int src) {
   return r;
 }
 
-// One warp decodes one <=3.10 object.  Must be called by all 32 lanes.
-// tab: this version's opcode table staged in shared memory (divergent
-// __constant__ reads serialize); stage: 256 records of shared scratch per warp
-// so the chunk's records leave as coalesced 4-byte stores.
-__device__ __forceinline__ void decode_warp(const u8* __restrict__ code, u32 len, int minor,
-                                            upy_ins* __restrict__ rec, upy_decoded* res,
-                                            const u32* __restrict__ tab, upy_ins* stage, uint4 first) {
+// Per-object state carried across the 256-unit chunks of one <=3.10 object.
+struct ChunkState {
+  ExtRun carry;   // EXTENDED_ARG run pending at the end of the previous chunk
+  u32 n_before;   // records emitted by earlier chunks
+  i64 bad_ins;    // first bad jump (instruction index) so far, -1 if none
+  i64 bad_off, bad_tgt;
+};
+__device__ __forceinline__ void chunk_state_init(ChunkState& st) {
+  st.carry = ExtRun{0, 0, 0};
+  st.n_before = 0;
+  st.bad_ins = -1;
+  st.bad_off = st.bad_tgt = 0;
+}
+
+// One warp decodes chunk [base, base+256) units of a <=3.10 object.  Must be
+// called by all 32 lanes.  w: this lane's 16 code bytes (units base+8*lane ..
+// +8); code: the object's bytes in global memory (only read for jump-target
+// checks of objects with EXTENDED_ARG or more than one chunk); tab: this
+// version's opcode table in shared memory; stage: 256 records of shared
+// memory the chunk's records are written to (the caller stores them out).
+// Returns the number of records, or -1 after an UnknownOpcode (res written).
+__device__ __forceinline__ int decode_chunk(const u8* __restrict__ code, u32 len, int minor, u32 base,
+                                            const u32* __restrict__ tab, upy_ins* stage, uint4 w,
+                                            ChunkState& st, upy_decoded* res) {
   const int lane = threadIdx.x & 31;
-  if (len == 0 || (len & 1)) {
-    if (lane == 0) {
-      res->status = UPY_ST_TRUNCATED_CODE;
-      res->n_instrs = 0;
-      res->aux0 = len == 0 ? 1 : 2;
-      res->aux1 = 0;
-    }
-    return;
-  }
   const u32 units = len >> 1;
-  ExtRun carry = {0, 0, 0};     // state entering the chunk
-  u32 n_before = 0;              // instructions emitted in earlier chunks
-  i64 bad_ins = -1;              // first bad jump (instruction index) so far
-  i64 bad_off = 0, bad_tgt = 0;
-  for (u32 base = 0; base < units; base += 256) {
-    // 128-bit load: lane owns units [base + 8*lane, +8)
-    u32 u0 = base + 8 * lane;
-    // (code is 16-B aligned and readable to the next 16-B boundary, upy.h; bytes
-    // past the end are never interpreted: every use is guarded by q < nu)
-    uint4 w = first;
-    u32 nu = 0;
-    if (u0 < units) {
-      nu = units - u0 < 8 ? units - u0 : 8;
-      if (base) w = *reinterpret_cast<const uint4*>(code + 2 * u0);
-    }
-    const u32 words[4] = {w.x, w.y, w.z, w.w};
+  const u32 u0 = base + 8 * lane;
+  u32 nu = 0;
+  if (u0 < units) nu = units - u0 < 8 ? units - u0 : 8;
+  const u32 words[4] = {w.x, w.y, w.z, w.w};
 #define UNIT_OP(q) ((words[(q) >> 1] >> (16 * ((q) & 1))) & 0xFFu)
 #define UNIT_ARG(q) ((words[(q) >> 1] >> (16 * ((q) & 1) + 8)) & 0xFFu)
-    // per-unit table entries
-    u32 ent[8];
-    u32 ext_mask = 0, unknown_mask = 0;
+  u32 ent[8];
+  u32 ext_mask = 0, unknown_mask = 0;
 #pragma unroll
-    for (int q = 0; q < 8; q++) {
-      ent[q] = (u32)q < nu ? tab[UNIT_OP(q)] : 0;
-      if ((u32)q < nu) {
-        if (UNIT_OP(q) == EXT_OP) ext_mask |= 1u << q;
-        if (!ent[q]) unknown_mask |= 1u << q;
-      }
+  for (int q = 0; q < 8; q++) {
+    ent[q] = (u32)q < nu ? tab[UNIT_OP(q)] : 0;
+    if ((u32)q < nu) {
+      if (UNIT_OP(q) == EXT_OP) ext_mask |= 1u << q;
+      if (!ent[q]) unknown_mask |= 1u << q;
     }
-    // first unknown opcode of the warp chunk (reference order): stop the object
-    u32 has_unknown = __ballot_sync(0xffffffffu, unknown_mask != 0);
-    if (has_unknown) {
-      int first_lane = __ffs(has_unknown) - 1;
-      if (lane == first_lane) {
-        int q = __ffs(unknown_mask) - 1;
-        res->status = UPY_ST_UNKNOWN_OPCODE;
-        res->n_instrs = 0;
-        res->aux0 = UNIT_OP(q);
-        res->aux1 = 2 * (u0 + q);
-      }
-      return;
+  }
+  // first unknown opcode of the chunk (reference order) stops the object
+  u32 has_unknown = __ballot_sync(0xffffffffu, unknown_mask != 0);
+  if (has_unknown) {
+    int first_lane = __ffs(has_unknown) - 1;
+    if (lane == first_lane) {
+      int q = __ffs(unknown_mask) - 1;
+      res->status = UPY_ST_UNKNOWN_OPCODE;
+      res->n_instrs = 0;
+      res->aux0 = UNIT_OP(q);
+      res->aux1 = 2 * (u0 + q);
     }
-    // Fast path (warp-uniform): no EXTENDED_ARG in the chunk and none pending, so
-    // every unit is one instruction, lane L's records start at 8*L and need no
-    // scans; a single-chunk object with no EXTENDED_ARG also has every even
-    // in-range offset as an extent start.
-    const bool fast = __ballot_sync(0xffffffffu, ext_mask != 0) == 0 && carry.len == 0;
-    u32 total;
-    i64 my_bad = -1, my_bad_off = 0, my_bad_tgt = 0;
-    ExtRun inc = {0, 0, 0};
-    if (fast) {
-      total = units - base < 256 ? units - base : 256;
-      const bool no_ext_obj = units <= 256;
-      uint4* st4 = reinterpret_cast<uint4*>(stage) + 6 * lane;
+    return -1;
+  }
+  // Fast path (warp-uniform): no EXTENDED_ARG in the chunk and none pending, so
+  // every unit is one instruction, lane L's records start at 8*L and need no
+  // scans; a single-chunk object with no EXTENDED_ARG also has every even
+  // in-range offset as an extent start.
+  const bool fast = __ballot_sync(0xffffffffu, ext_mask != 0) == 0 && st.carry.len == 0;
+  u32 total;
+  i64 my_bad = -1, my_bad_off = 0, my_bad_tgt = 0;
+  ExtRun inc = {0, 0, 0};
+  if (fast) {
+    total = units - base < 256 ? units - base : 256;
+    const bool no_ext_obj = units <= 256;
+    uint4* st4 = reinterpret_cast<uint4*>(stage) + 6 * lane;
 #pragma unroll
-      for (int g = 0; g < 2; g++) {  // 4 records = 12 words = 3 uint4 per group
-        u32 wr[12];
+    for (int g = 0; g < 2; g++) {  // 4 records = 12 words = 3 uint4 per group
+      u32 wr[12];
 #pragma unroll
-        for (int r = 0; r < 4; r++) {
-          const int q = 4 * g + r;
-          u32 u = u0 + q;
-          u32 e = ent[q];
-          u32 has_arg = UPY_ENT_HASARG(e) ? 1u : 0u;
-          u32 arg = has_arg ? UNIT_ARG(q) : 0u;
-          wr[3 * r] = 2 * u;
-          wr[3 * r + 1] = arg;
-          wr[3 * r + 2] = UNIT_OP(q) | (has_arg << 24);
-          u32 kind = UPY_ENT_KIND(e);
-          if ((u32)q < nu && my_bad < 0 && (kind == K_JUMP_REL || kind == K_JUMP_ABS || kind == K_JUMP_BACK)) {
-            bool okk;
-            i64 t = jump_target_u64(minor, kind, 2ull * u, arg, &okk);
-            bool valid = t >= 0 && t < (i64)len && !(t & 1) && (no_ext_obj || t == 0 || code[t - 2] != EXT_OP);
-            if (!valid) {
-              my_bad = n_before + 8 * lane + q;
-              my_bad_off = 2 * u;
-              my_bad_tgt = t;
-            }
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < 3; k++) st4[3 * g + k] = make_uint4(wr[4 * k], wr[4 * k + 1], wr[4 * k + 2], wr[4 * k + 3]);
-      }
-    } else {
-      // lane summary of its 8 units
-      ExtRun mine;
-      {
-        u32 valid_mask = nu >= 8 ? 0xFF : ((1u << nu) - 1);
-        mine.all = (nu > 0 && (ext_mask & valid_mask) == valid_mask) ? 1 : (nu == 0 ? 1 : 0);
-        // trailing run: from the top valid unit downward
-        u32 len_ = 0;
-        u64 val = 0;
-        bool in_run = true;
-#pragma unroll
-        for (int q = 7; q >= 0; q--) {
-          if ((u32)q >= nu) continue;
-          in_run = in_run && ((ext_mask >> q) & 1);
-          if (in_run) len_++;
-        }
-#pragma unroll
-        for (int q = 0; q < 8; q++)
-          if ((u32)q < nu && (u32)q >= nu - len_) val = (val << 8) | UNIT_ARG(q);
-        mine.len = len_;
-        mine.val = val;
-      }
-      // inclusive scan over lanes, then exclusive = shifted
-      inc = mine;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        ExtRun o = shfl_up_run(inc, d);
-        if (lane >= d) inc = ext_combine(o, inc);
-      }
-      ExtRun excl = shfl_up_run(inc, 1);
-      if (lane == 0) excl = ExtRun{1, 0, 0};
-      excl = ext_combine(carry, excl);
-      // instruction slots: non-EXT units before this lane
-      u32 my_ins = (u32)__popc((~ext_mask) & (nu >= 8 ? 0xFF : ((1u << nu) - 1)));
-      u32 pre = my_ins;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        u32 o = __shfl_up_sync(0xffffffffu, pre, d);
-        if (lane >= d) pre += o;
-      }
-      total = __shfl_sync(0xffffffffu, pre, 31);
-      u32 idx = n_before + pre - my_ins;
-      // walk my units with the incoming run
-      u32 run_len = excl.len;  // trailing EXTENDED_ARG run entering my span
-      u64 run_val = excl.val;
-#pragma unroll
-      for (int q = 0; q < 8; q++) {
-        if ((u32)q >= nu) continue;
+      for (int r = 0; r < 4; r++) {
+        const int q = 4 * g + r;
         u32 u = u0 + q;
-        if ((ext_mask >> q) & 1) {
-          run_val = (run_val << 8) | UNIT_ARG(q);
-          run_len++;
-          continue;
-        }
         u32 e = ent[q];
-        bool has_arg = UPY_ENT_HASARG(e);
-        u64 ext = run_len ? (run_len >= 8 ? 0 : (run_val << 8)) : 0;
-        bool sat = run_len >= 8;
-        u64 arg = has_arg ? (UNIT_ARG(q) | ext) : 0;
-        bool big = has_arg && (sat || (arg >> 32));
-        u32* sw = reinterpret_cast<u32*>(stage) + 3 * (idx - n_before);
-        u32 off = 2 * (u - run_len);
-        sw[0] = off;
-        sw[1] = big ? 0xFFFFFFFFu : (u32)arg;
-        sw[2] = UNIT_OP(q) | ((run_len > 255 ? 255u : run_len) << 8) | (((has_arg ? 1u : 0u) | (big ? 2u : 0u)) << 24);
+        u32 has_arg = UPY_ENT_HASARG(e) ? 1u : 0u;
+        u32 arg = has_arg ? UNIT_ARG(q) : 0u;
+        wr[3 * r] = 2 * u;
+        wr[3 * r + 1] = arg;
+        wr[3 * r + 2] = UNIT_OP(q) | (has_arg << 24);
         u32 kind = UPY_ENT_KIND(e);
-        if (my_bad < 0 && (kind == K_JUMP_REL || kind == K_JUMP_ABS || kind == K_JUMP_BACK)) {
+        if ((u32)q < nu && my_bad < 0 && (kind == K_JUMP_REL || kind == K_JUMP_ABS || kind == K_JUMP_BACK)) {
           bool okk;
           i64 t = jump_target_u64(minor, kind, 2ull * u, arg, &okk);
-          bool valid = !big && t >= 0 && t < (i64)len && !(t & 1) && (t == 0 || code[t - 2] != EXT_OP);
+          bool valid = t >= 0 && t < (i64)len && !(t & 1) && (no_ext_obj || t == 0 || code[t - 2] != EXT_OP);
           if (!valid) {
-            my_bad = idx;
-            my_bad_off = off;
+            my_bad = st.n_before + 8 * lane + q;
+            my_bad_off = 2 * u;
             my_bad_tgt = t;
           }
         }
-        idx++;
-        run_len = 0;
-        run_val = 0;
       }
+#pragma unroll
+      for (int k = 0; k < 3; k++) st4[3 * g + k] = make_uint4(wr[4 * k], wr[4 * k + 1], wr[4 * k + 2], wr[4 * k + 3]);
     }
-    // first bad jump of the chunk (lowest instruction index)
-    u32 badm = __ballot_sync(0xffffffffu, my_bad >= 0);
-    if (badm && bad_ins < 0) {
-      int bl = __ffs(badm) - 1;
-      bad_ins = __shfl_sync(0xffffffffu, my_bad, bl);
-      bad_off = __shfl_sync(0xffffffffu, my_bad_off, bl);
-      bad_tgt = __shfl_sync(0xffffffffu, my_bad_tgt, bl);
-    }
-    // carry into the next chunk: state after the whole chunk (a chunk without
-    // EXTENDED_ARG leaves no pending run)
-    if (fast) carry = ExtRun{0, 0, 0};
-    else carry = ext_combine(carry, shfl_run(inc, 31));
-    __syncwarp();
-    {  // coalesced write-out of this chunk's records (12 B each)
-      u32 nw = 3 * total;
-      u32* dst = reinterpret_cast<u32*>(rec + n_before);
-      const u32* src = reinterpret_cast<const u32*>(stage);
-      u32 done = 0;
-      if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-        const uint4* s4 = reinterpret_cast<const uint4*>(stage);
-        uint4* d4 = reinterpret_cast<uint4*>(dst);
-        for (u32 w = lane; w < nw / 4; w += 32) d4[w] = s4[w];
-        done = nw & ~3u;
+  } else {
+    // lane summary of its 8 units
+    ExtRun mine;
+    {
+      u32 valid_mask = nu >= 8 ? 0xFF : ((1u << nu) - 1);
+      mine.all = (nu > 0 && (ext_mask & valid_mask) == valid_mask) ? 1 : (nu == 0 ? 1 : 0);
+      u32 len_ = 0;
+      u64 val = 0;
+      bool in_run = true;
+#pragma unroll
+      for (int q = 7; q >= 0; q--) {
+        if ((u32)q >= nu) continue;
+        in_run = in_run && ((ext_mask >> q) & 1);
+        if (in_run) len_++;
       }
-      for (u32 w = done + lane; w < nw; w += 32) dst[w] = src[w];
+#pragma unroll
+      for (int q = 0; q < 8; q++)
+        if ((u32)q < nu && (u32)q >= nu - len_) val = (val << 8) | UNIT_ARG(q);
+      mine.len = len_;
+      mine.val = val;
     }
-    __syncwarp();
-    n_before += total;
+    // inclusive scan over lanes, then exclusive = shifted
+    inc = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      ExtRun o = shfl_up_run(inc, d);
+      if (lane >= d) inc = ext_combine(o, inc);
+    }
+    ExtRun excl = shfl_up_run(inc, 1);
+    if (lane == 0) excl = ExtRun{1, 0, 0};
+    excl = ext_combine(st.carry, excl);
+    // instruction slots: non-EXT units before this lane
+    u32 my_ins = (u32)__popc((~ext_mask) & (nu >= 8 ? 0xFF : ((1u << nu) - 1)));
+    u32 pre = my_ins;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      u32 o = __shfl_up_sync(0xffffffffu, pre, d);
+      if (lane >= d) pre += o;
+    }
+    total = __shfl_sync(0xffffffffu, pre, 31);
+    u32 idx = st.n_before + pre - my_ins;
+    u32 run_len = excl.len;  // trailing EXTENDED_ARG run entering my span
+    u64 run_val = excl.val;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      if ((u32)q >= nu) continue;
+      u32 u = u0 + q;
+      if ((ext_mask >> q) & 1) {
+        run_val = (run_val << 8) | UNIT_ARG(q);
+        run_len++;
+        continue;
+      }
+      u32 e = ent[q];
+      bool has_arg = UPY_ENT_HASARG(e);
+      u64 ext = run_len ? (run_len >= 8 ? 0 : (run_val << 8)) : 0;
+      bool sat = run_len >= 8;
+      u64 arg = has_arg ? (UNIT_ARG(q) | ext) : 0;
+      bool big = has_arg && (sat || (arg >> 32));
+      u32* sw = reinterpret_cast<u32*>(stage) + 3 * (idx - st.n_before);
+      u32 off = 2 * (u - run_len);
+      sw[0] = off;
+      sw[1] = big ? 0xFFFFFFFFu : (u32)arg;
+      sw[2] = UNIT_OP(q) | ((run_len > 255 ? 255u : run_len) << 8) | (((has_arg ? 1u : 0u) | (big ? 2u : 0u)) << 24);
+      u32 kind = UPY_ENT_KIND(e);
+      if (my_bad < 0 && (kind == K_JUMP_REL || kind == K_JUMP_ABS || kind == K_JUMP_BACK)) {
+        bool okk;
+        i64 t = jump_target_u64(minor, kind, 2ull * u, arg, &okk);
+        bool valid = !big && t >= 0 && t < (i64)len && !(t & 1) && (t == 0 || code[t - 2] != EXT_OP);
+        if (!valid) {
+          my_bad = idx;
+          my_bad_off = off;
+          my_bad_tgt = t;
+        }
+      }
+      idx++;
+      run_len = 0;
+      run_val = 0;
+    }
+  }
+  // first bad jump of the chunk (lowest instruction index)
+  u32 badm = __ballot_sync(0xffffffffu, my_bad >= 0);
+  if (badm && st.bad_ins < 0) {
+    int bl = __ffs(badm) - 1;
+    st.bad_ins = __shfl_sync(0xffffffffu, my_bad, bl);
+    st.bad_off = __shfl_sync(0xffffffffu, my_bad_off, bl);
+    st.bad_tgt = __shfl_sync(0xffffffffu, my_bad_tgt, bl);
+  }
+  // carry into the next chunk (a chunk without EXTENDED_ARG leaves no pending run)
+  if (fast) st.carry = ExtRun{0, 0, 0};
+  else st.carry = ext_combine(st.carry, shfl_run(inc, 31));
 #undef UNIT_OP
 #undef UNIT_ARG
-  }
-  if (lane == 0) {
-    if (carry.len) {  // code ends inside an EXTENDED_ARG run
-      res->status = UPY_ST_TRUNCATED_CODE;
-      res->n_instrs = 0;
-      res->aux0 = 3;
-      res->aux1 = len;
-    } else if (bad_ins >= 0) {
-      res->status = UPY_ST_BAD_JUMP_TARGET;
-      res->n_instrs = 0;
-      res->aux0 = bad_off;
-      res->aux1 = bad_tgt;
-    } else {
-      res->status = UPY_ST_OK;
-      res->n_instrs = (i32)n_before;
-      res->aux0 = res->aux1 = 0;
-    }
+  return (int)total;
+}
+
+// Final status of a <=3.10 object after its last chunk (reference error order:
+// UnknownOpcode / TruncatedCode pre-empt BadJumpTarget).
+__device__ __forceinline__ void chunk_finish(u32 len, const ChunkState& st, upy_decoded* res) {
+  if (st.carry.len) {  // code ends inside an EXTENDED_ARG run
+    res->status = UPY_ST_TRUNCATED_CODE;
+    res->n_instrs = 0;
+    res->aux0 = 3;
+    res->aux1 = len;
+  } else if (st.bad_ins >= 0) {
+    res->status = UPY_ST_BAD_JUMP_TARGET;
+    res->n_instrs = 0;
+    res->aux0 = st.bad_off;
+    res->aux1 = st.bad_tgt;
+  } else {
+    res->status = UPY_ST_OK;
+    res->n_instrs = (i32)st.n_before;
+    res->aux0 = res->aux1 = 0;
   }
 }
 

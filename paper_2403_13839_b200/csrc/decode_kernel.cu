@@ -1,72 +1,227 @@
 // decode_kernel.cu -- the sm_100a decode kernel (disasm.py:71-172) and its
 // launcher, compiled as its own object so it can be tuned without rebuilding
 // the decompile kernel (upy.cu).
+//
+// HBM-bound streaming design.  Every warp is an independent pipeline over
+// groups of 32 consecutive objects (group g = warp, warp + nwarps, ...):
+//   * the 32 object headers of the current and the next group sit one per lane
+//     (two coalesced header loads per 32 objects), broadcast by shuffles;
+//   * code bytes move global -> shared in 512-B chunks (256 units) by TMA bulk
+//     copies (cp.async.bulk ... mbarrier::complete_tx) into a DSTAGES-deep ring
+//     with one mbarrier per stage; lane 0 keeps the ring DSTAGES chunks ahead of
+//     the decoder across object and group boundaries, so several KB per warp
+//     are in flight with no registers held for them;
+//   * each chunk's records are built in a shared staging buffer (double
+//     buffered) and leave as ONE bulk shared -> global copy (cp.async.bulk
+//     .global.shared::cta.bulk_group) when the destination is 16-B aligned,
+//     else as coalesced 16-B / 4-B stores.
+// 3.11 objects (inline caches make instruction starts a serial chain) are
+// decoded by lane 0 straight from global memory (decode_scalar).
 #include <cuda_runtime.h>
 #include "decode.h"
 
-// One warp per object (grid-stride); tables and record staging in shared memory.
-// Software-pipelined: while a warp decodes object o, the header of o + 2*stride
-// and the first 512 code bytes of o + stride are already in flight.
-__device__ __forceinline__ void obj_hdr(const upy_arena& A, i64 x, u64* off, u32* len, u32* minor) {
-  if (x < A.n_objs) {
-    const upy_obj* ob = &A.objs[x];
-    *off = ob->code_off;
-    *len = ob->code_len;
-    *minor = ob->minor;
-  } else {
-    *off = 0;
-    *len = 0;
-    *minor = 0;
-  }
+#define DSTAGES 4
+#define DWARPS 4  // warps per block
+
+struct __align__(128) DecWarpSmem {
+  uint4 in[DSTAGES][32];    // DSTAGES x 512 B of code
+  upy_ins out[2][256];      // 2 x 3 KB of records
+  unsigned long long bar[DSTAGES];
+};
+
+__device__ __forceinline__ u32 smem_addr(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, u32 n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(n) : "memory");
 }
-__device__ __forceinline__ uint4 first_chunk(const upy_arena& A, u64 off, u32 len, u32 minor, int lane) {
-  if (minor >= 8 && minor <= 10 && !(len & 1) && 8u * lane < (len >> 1))
-    return *reinterpret_cast<const uint4*>(A.bytes + off + 16 * lane);
-  return make_uint4(0, 0, 0, 0);
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
 }
-__global__ void __launch_bounds__(256, 2) upy_decode_kernel(upy_arena A, upy_ins* __restrict__ ins,
-                                                            upy_decoded* __restrict__ dec) {
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, u32 parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_addr(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, unsigned long long* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(b))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, u32 bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// chunks a <=3.10 object streams through the ring (0: handled from global memory)
+__device__ __forceinline__ u32 n_chunks(u32 len, u32 minor) {
+  if (minor < 8 || minor > 10 || len == 0 || (len & 1)) return 0;
+  return ((len >> 1) + 255) >> 8;
+}
+
+__global__ void __launch_bounds__(DWARPS * 32, 6) upy_decode_kernel(upy_arena A, upy_ins* __restrict__ ins,
+                                                                    upy_decoded* __restrict__ dec) {
+  __shared__ u32 tab[3][256];  // 3.8-3.10 opcode tables
+  __shared__ DecWarpSmem wsm[DWARPS];
   const int lane = threadIdx.x & 31;
-  const i64 warp = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
-  __shared__ u32 tab[3][256];              // 3.8-3.10 opcode tables
-  __shared__ __align__(16) upy_ins stage[256 / 32][256];  // per-warp record staging (24 KB)
+  const int wid = threadIdx.x >> 5;
+  DecWarpSmem& S = wsm[wid];
   for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) tab[i >> 8][i & 255] = UPY_OPTABLE_DEV[i >> 8][i & 255];
+  if (lane == 0) {
+    for (int s = 0; s < DSTAGES; s++) mbar_init(&S.bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
-  upy_ins* my_stage = stage[threadIdx.x >> 5];
-  u64 off0, off1, off2;
-  u32 len0, len1, len2, min0, min1, min2;
-  obj_hdr(A, warp, &off0, &len0, &min0);
-  uint4 w0 = first_chunk(A, off0, len0, min0, lane);
-  obj_hdr(A, warp + nwarps, &off1, &len1, &min1);
-  for (i64 o = warp; o < A.n_objs; o += nwarps) {
-    uint4 w1 = first_chunk(A, off1, len1, min1, lane);
-    obj_hdr(A, o + 2 * nwarps, &off2, &len2, &min2);
-    const u8* code = A.bytes + off0;
-    upy_ins* rec = ins + (off0 >> 1);
-    int minor = (int)min0;
-    if (minor >= 8 && minor <= 10) {
-      decode_warp(code, len0, minor, rec, &dec[o], tab[minor - 8], my_stage, w0);
-    } else if (lane == 0) {
-      if (minor == 11) {
-        decode_scalar(code, len0, minor, rec, &dec[o]);
-      } else {
-        dec[o].status = UPY_ST_INTERNAL;
-        dec[o].n_instrs = 0;
+
+  const i64 nw = (i64)gridDim.x * DWARPS;
+  const i64 n_groups = (A.n_objs + 31) >> 5;
+  i64 g = (i64)blockIdx.x * DWARPS + wid;
+  if (g >= n_groups) return;
+
+  // headers: lane j holds object 32*group + j of the current (c) and next (n) group
+  auto load_hdr = [&](i64 grp, u64& off, u32& len, u32& minor) {
+    i64 o = grp * 32 + lane;
+    if (grp < n_groups && o < A.n_objs) {
+      const upy_obj* ob = &A.objs[o];
+      off = ob->code_off;
+      len = ob->code_len;
+      minor = ob->minor;
+    } else {
+      off = 0;
+      len = 0;
+      minor = 0;
+    }
+  };
+  u64 c_off, n_off;
+  u32 c_len, c_min, n_len, n_min;
+  load_hdr(g, c_off, c_len, c_min);
+  load_hdr(g + nw, n_off, n_len, n_min);
+
+  // producer cursor (warp-uniform): group selector (0 current, 1 next, 2 none),
+  // object within the group, chunk within the object
+  u32 psel = 0, pj = 0, pc = 0;
+  u32 prod = 0, cons = 0;  // chunks issued / consumed
+  auto pump = [&]() {
+    while (prod < cons + DSTAGES && psel < 2) {
+      const i64 grp = g + (i64)psel * nw;
+      const i64 o = grp * 32 + pj;
+      if (grp >= n_groups || o >= A.n_objs) {
+        psel = 2;
+        break;
+      }
+      const u64 off = __shfl_sync(0xffffffffu, psel ? n_off : c_off, pj);
+      const u32 len = __shfl_sync(0xffffffffu, psel ? n_len : c_len, pj);
+      const u32 minor = __shfl_sync(0xffffffffu, psel ? n_min : c_min, pj);
+      const u32 nch = n_chunks(len, minor);
+      if (pc < nch) {
+        const u32 s = prod % DSTAGES;
+        const u32 start = pc * 512u;
+        u32 bytes = len - start < 512u ? len - start : 512u;
+        bytes = (bytes + 15u) & ~15u;  // code is readable to the next 16-B boundary (upy.h)
+        if (lane == 0) {
+          fence_async_smem();
+          mbar_expect_tx(&S.bar[s], bytes);
+          bulk_g2s(&S.in[s][0], A.bytes + off + start, bytes, &S.bar[s]);
+        }
+        prod++;
+        pc++;
+      }
+      if (pc >= nch) {
+        pc = 0;
+        if (++pj == 32) {
+          pj = 0;
+          psel++;
+        }
       }
     }
-    __syncwarp();
-    off0 = off1, len0 = len1, min0 = min1, w0 = w1;
-    off1 = off2, len1 = len2, min1 = min2;
+  };
+
+  u32 ob = 0;  // output staging buffer toggle
+  for (; g < n_groups; g += nw) {
+    for (u32 j = 0; j < 32; j++) {
+      const i64 o = g * 32 + j;
+      if (o >= A.n_objs) break;
+      const u64 off = __shfl_sync(0xffffffffu, c_off, j);
+      const u32 len = __shfl_sync(0xffffffffu, c_len, j);
+      const u32 minor = __shfl_sync(0xffffffffu, c_min, j);
+      const u32 nch = n_chunks(len, minor);
+      upy_ins* rec = ins + (off >> 1);
+      if (nch == 0) {
+        if (lane == 0) {
+          if (minor == 11 || ((minor >= 8 && minor <= 10) && (len == 0 || (len & 1)))) {
+            decode_scalar(A.bytes + off, len, (int)minor, rec, &dec[o]);
+          } else {
+            dec[o].status = UPY_ST_INTERNAL;
+            dec[o].n_instrs = 0;
+            dec[o].aux0 = dec[o].aux1 = 0;
+          }
+        }
+        continue;
+      }
+      ChunkState st;
+      chunk_state_init(st);
+      bool stopped = false;
+      for (u32 c = 0; c < nch; c++) {
+        pump();
+        const u32 s = cons % DSTAGES;
+        mbar_wait(&S.bar[s], (cons / DSTAGES) & 1);
+        if (!stopped) {
+          const uint4 w = S.in[s][lane];
+          // the staging buffer was last stored out two chunks ago: its bulk read must be done
+          if (lane == 0) bulk_wait_read1();
+          __syncwarp();
+          upy_ins* stage = S.out[ob];
+          const int total = decode_chunk(A.bytes + off, len, (int)minor, c * 256u, tab[minor - 8], stage, w, st, &dec[o]);
+          if (total < 0) {
+            stopped = true;
+          } else {
+            __syncwarp();
+            upy_ins* dst = rec + st.n_before;
+            // bulk store: 16-B aligned destination, size rounded up to 16 B -- only on
+            // the object's last chunk (the overshoot, < 16 B, stays inside this object's
+            // record slots, which extend to 6 * round16(len) bytes) or when exact, so an
+            // async store never overlaps a later chunk's records
+            if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0 && (c + 1 == nch || (total & 3) == 0)) {
+              if (lane == 0) {
+                fence_async_smem();
+                bulk_s2g(dst, stage, ((u32)total * 12u + 15u) & ~15u);
+              }
+              ob ^= 1;
+            } else {
+              const u32 nwd = 3u * (u32)total;
+              u32* d = reinterpret_cast<u32*>(dst);
+              const u32* sw = reinterpret_cast<const u32*>(stage);
+              for (u32 k = lane; k < nwd; k += 32) d[k] = sw[k];
+              __syncwarp();
+            }
+            st.n_before += (u32)total;
+          }
+        }
+        __syncwarp();
+        cons++;
+      }
+      if (!stopped && lane == 0) chunk_finish(len, st, &dec[o]);
+    }
+    // shift the header window; the producer cursor moves down one group
+    c_off = n_off, c_len = n_len, c_min = n_min;
+    load_hdr(g + 2 * nw, n_off, n_len, n_min);
+    if (psel > 0) psel--;
   }
+  if (lane == 0) bulk_wait_all();
 }
 
 // Launcher used by upy_decode_batch (upy.cu); returns the launch error.
+// Grid: at most 6 resident blocks of 4 warps per SM, one warp per 32-object group.
 cudaError_t upy_decode_launch(const upy_arena* arena, upy_ins* ins, upy_decoded* dec, cudaStream_t s, int sms) {
-  const int threads = 256;
-  i64 blocks = (arena->n_objs * 32 + threads - 1) / threads;
-  i64 max_blocks = (i64)sms * 64;
+  const i64 groups = (arena->n_objs + 31) / 32;
+  i64 blocks = (groups + DWARPS - 1) / DWARPS;
+  const i64 max_blocks = (i64)sms * 6;
   if (blocks > max_blocks) blocks = max_blocks;
-  upy_decode_kernel<<<(unsigned)blocks, threads, 0, s>>>(*arena, ins, dec);
+  upy_decode_kernel<<<(unsigned)blocks, DWARPS * 32, 0, s>>>(*arena, ins, dec);
   return cudaGetLastError();
 }
