@@ -38,6 +38,7 @@ WORKLOADS = {
     # modules (nested defs/classes/lambdas/comprehensions decompiled through their roots)
     "c2": ("c2_310", 110, "C2: the reference's pkg/corpus, 110 modules (+nested code, 3.10) in one batch"),
     "c2x": ("c2_310", 110 * 4096, "C2 x4096: the reference's pkg/corpus modules (3.10) tiled to 450,560 roots"),
+    "c2_311": ("c2_311", 110, "C2 (3.11): the reference's pkg/corpus, 110 modules (+nested code) in one batch"),
     # C5: one 16M-object corpus split across the ranks (strong scaling)
     "c5": ("c3_310", 16_777_216, "C5: synthetic 16M code objects x ~200 units (3.10) sharded by object across GPUs"),
 }
@@ -297,7 +298,7 @@ def main():
     # ---------------- end to end from .pyc files in host memory:
     # native loader (all host threads) -> H2D -> kernels -> D2H, wall clock
     pyc = None
-    if args.pyc and args.workload in ("c2", "c2x", "c3", "c3_311", "c5"):
+    if args.pyc and args.workload in ("c2", "c2x", "c2_311", "c3", "c3_311", "c5"):
         pyc = pyc_e2e(pool, reps, local, args, pool_name, n_pool, barrier)
 
     # ---------------- max over ranks

@@ -15,10 +15,11 @@ POOLS = {
     # C2: the reference's 110-module syntax corpus compiled to 3.10 (fixture
     # tests/golden/c2.jsonl, made by make_c2_golden.py); roots are modules
     "c2_310": {"gen": "c2", "minor": 10, "size": 110},
+    "c2_311": {"gen": "c2", "minor": 11, "size": 110},
 }
 
 
-def _c2_trees():
+def _c2_trees(minor):
     import json
     import os
 
@@ -27,14 +28,14 @@ def _c2_trees():
     path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden", "c2.jsonl")
     with open(path) as f:
         recs = [json.loads(line) for line in f]
-    return [codejson.from_json(r["tree"]) for r in recs if not r.get("style")]
+    return [codejson.from_json(r["tree"]) for r in recs if not r.get("style") and r["minor"] == minor]
 
 
 def pool_objects(name, lo=0, hi=None):
     spec = POOLS[name]
     hi = spec["size"] if hi is None else hi
     if spec["gen"] == "c2":
-        return _c2_trees()[lo:hi]
+        return _c2_trees(spec["minor"])[lo:hi]
     if spec["gen"] == "c3":
         return [corpus.c3(i, spec["minor"]) for i in range(lo, hi)]
     return [corpus.c4(i, spec["minor"], spec["units"]) for i in range(lo, hi)]

@@ -52,8 +52,11 @@ CMPOP = {ast.Lt: 0, ast.LtE: 1, ast.Eq: 2, ast.NotEq: 3, ast.Gt: 4, ast.GtE: 5}
 
 JUMPS = {"JUMP_ABSOLUTE", "JUMP_FORWARD", "POP_JUMP_IF_FALSE", "POP_JUMP_IF_TRUE",
          "JUMP_IF_FALSE_OR_POP", "JUMP_IF_TRUE_OR_POP", "JUMP_IF_NOT_EXC_MATCH", "FOR_ITER",
-         "SETUP_FINALLY", "SETUP_WITH"}
-UNCOND = {"JUMP_ABSOLUTE", "JUMP_FORWARD"}
+         "SETUP_FINALLY", "SETUP_WITH",
+         # 3.11 pseudo / new jumps (pycodegen311.py), direction fixed by normalize_jumps
+         "JUMP", "JUMP_NO_INTERRUPT", "POP_JUMP_IF_NONE", "POP_JUMP_IF_NOT_NONE", "SETUP_CLEANUP", "SEND"}
+UNCOND = {"JUMP_ABSOLUTE", "JUMP_FORWARD", "JUMP", "JUMP_NO_INTERRUPT"}
+SETUPS = {"SETUP_FINALLY", "SETUP_WITH", "SETUP_CLEANUP"}
 EXITS = {"RETURN_VALUE", "RAISE_VARARGS", "RERAISE"}
 
 
@@ -388,7 +391,8 @@ def _analyze(s, bound):
 # ---------------------------------------------------------------- CFG
 
 class Block:
-    __slots__ = ("instrs", "next", "idx", "exit", "nofall", "preds", "label", "depth")
+    __slots__ = ("instrs", "next", "idx", "exit", "nofall", "preds", "label", "depth",
+                 "visited", "exc", "lasti")  # the last three: 3.11 exception labelling
 
     def __init__(self, idx):
         self.instrs = []     # [opname, arg, target Block | None, lineno]
@@ -399,6 +403,9 @@ class Block:
         self.preds = 0
         self.label = None
         self.depth = -1
+        self.visited = False
+        self.exc = None
+        self.lasti = False
 
 
 def _is_jump(ins):
@@ -415,7 +422,8 @@ class FBlock:
 class Unit:
     """One code object being compiled (compiler_unit)."""
 
-    def __init__(self, scope, name, qualname, firstlineno, kind):
+    def __init__(self, scope, name, qualname, firstlineno, kind, minor=10):
+        self.minor = minor
         self.scope = scope
         self.name = name
         self.qualname = qualname
@@ -523,9 +531,11 @@ def _truthy(c):
 # ---------------------------------------------------------------- the compiler
 
 class Compiler:
+    MINORS = (10,)
+
     def __init__(self, source, filename="<corpus>", minor=10):
-        if minor != 10:
-            raise CompileError("pycodegen targets CPython 3.10 bytecode")
+        if minor not in self.MINORS:
+            raise CompileError(f"{type(self).__name__} targets CPython 3.{self.MINORS[0]} bytecode")
         self.minor = minor
         self.filename = filename
         tree = ast.parse(source, filename)
@@ -539,9 +549,12 @@ class Compiler:
         self.stack = []
 
     # ------------------------------------------------------------ units
+    def _new_unit(self, scope, name, qual, firstlineno, kind):
+        return Unit(scope, name, qual, firstlineno, kind)
+
     def compile_module(self):
         s = self.scopes[id(self.tree)]
-        self.u = Unit(s, "<module>", "<module>", 1, "module")
+        self.u = self._new_unit(s, "<module>", "<module>", 1, "module")
         body = self.tree.body
         if body:
             self.u.lineno = body[0].lineno
@@ -562,7 +575,7 @@ class Compiler:
                 else:
                     qual = f"{parent.qualname}.{name}"
         self.stack.append(self.u)
-        self.u = Unit(scope, name, qual, firstlineno, kind)
+        self.u = self._new_unit(scope, name, qual, firstlineno, kind)
         return self.u
 
     def _exit(self):
@@ -1875,10 +1888,11 @@ def _eliminate_empty(u):
             b.instrs[-1][2] = _first_nonempty(b.instrs[-1][2])
 
 
-def _optimize(u):
+def _optimize(u, optimize_block=None):
+    optimize_block = optimize_block or _optimize_block
     _normalize(u)
     for b in _chain(u.entry):
-        _optimize_block(u, b)
+        optimize_block(u, b)
         _clean(b, -1)
     for b in sorted(u.blocks, key=lambda x: -x.idx):
         _extend_block(b)
@@ -1908,7 +1922,7 @@ def _optimize(u):
     _mark_reachable(u)
     live = [b for b in _chain(u.entry)]
     for b in sorted(live, key=lambda x: -x.idx):
-        if b.instrs and b.instrs[-1][0] in JUMPS and b.instrs[-1][0] not in ("SETUP_FINALLY", "SETUP_WITH"):
+        if b.instrs and b.instrs[-1][0] in JUMPS and b.instrs[-1][0] not in SETUPS:
             t = b.instrs[-1][2]
             if t.exit and t.instrs[0][3] < 0 and t.preds > 1:
                 nb = u.new_block()
@@ -1924,6 +1938,8 @@ def _optimize(u):
     for b in _chain(u.entry):
         while b.next is not None and not b.next.instrs:
             b.next = b.next.next
+    if u.minor >= 11:
+        return  # jump directions are chosen by normalize_jumps (pycodegen311.py)
     # relative jumps must point forward
     pos = {}
     k = 0

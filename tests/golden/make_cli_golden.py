@@ -40,7 +40,8 @@ MODS = ["classes/class_inherit_kw", "comprehensions/nested_listcomp", "control/f
 def _trees():
     with open(os.path.join(HERE, "c2.jsonl")) as f:
         recs = [json.loads(line) for line in f]
-    by = {r["case"][len("c2-3.10-"):]: codejson.from_json(r["tree"]) for r in recs if not r.get("style")}
+    by = {r["case"][len("c2-3.10-"):]: codejson.from_json(r["tree"]) for r in recs
+          if not r.get("style") and r["minor"] == 10}
     return [(m.split("/")[1], by[m]) for m in MODS]
 
 

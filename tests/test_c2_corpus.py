@@ -22,7 +22,8 @@ def test_c2_fixture_inputs_pinned():
     from paper_2403_13839_b200.synth import codejson
 
     recs = _recs()
-    assert len(recs) == 110 and all(r["status"] == "ok" for r in recs)
+    assert len(recs) == 220 and all(r["status"] == "ok" for r in recs)
+    assert sorted({r["minor"] for r in recs}) == [10, 11]
     for r, co in zip(recs, inputs(recs)):
         assert codejson.to_json(co) == r["tree"]
         h = hashlib.sha256()
@@ -99,3 +100,27 @@ def test_codegen_closures_and_class_cell():
     assert cls.cellvars == ("__class__",)
     m = next(c.value for c in cls.consts if c.kind == "code")
     assert m.freevars == ("__class__",)
+
+
+def test_codegen311_try_except_layout_and_exception_table():
+    # CPython 3.11: handler entered with PUSH_EXC_INFO / CHECK_EXC_MATCH, the
+    # `as` name cleaned up in an artificial block, `COPY 3; POP_EXCEPT;
+    # RERAISE 1` cleanup, zero-cost exception table with depth / lasti
+    from paper_2403_13839_b200._optables import TABLES
+    from paper_2403_13839_b200.synth import pycodegen311
+
+    mod = pycodegen311.compile_source("def f(d, k):\n    try:\n        return d[k]\n    except KeyError as exc:\n"
+                                      "        return 'missing:' + repr(exc.args[0])\n")
+    fn = mod.consts[0].value
+    code = fn.code
+    ops = []
+    i = 0
+    while i < len(code):
+        name, _, _, caches = TABLES[11][code[i]]
+        ops.append((name, code[i + 1]))
+        i += 2 * (1 + caches)
+    assert ops[:5] == [("RESUME", 0), ("NOP", 0), ("LOAD_FAST", 0), ("LOAD_FAST", 1), ("BINARY_SUBSCR", 0)]
+    assert ("POP_JUMP_FORWARD_IF_FALSE", 39) in ops and ops[-3:] == [("COPY", 3), ("POP_EXCEPT", 0), ("RERAISE", 1)]
+    assert ("LOAD_GLOBAL", 3) in ops  # NULL + repr
+    # entries (start, size, target, depth<<1|lasti) in code units, varint encoded
+    assert fn.exceptiontable == bytes([0x82, 7, 10, 0, 0x8a, 10, 59, 3, 0x94, 28, 54, 3, 0xb0, 1, 59, 3, 0xb6, 5, 59, 3])
