@@ -16,6 +16,7 @@ POOLS = {
     # tests/golden/c2.jsonl, made by make_c2_golden.py); roots are modules
     "c2_310": {"gen": "c2", "minor": 10, "size": 110},
     "c2_311": {"gen": "c2", "minor": 11, "size": 110},
+    "c2_39": {"gen": "c2", "minor": 9, "size": 110},
 }
 
 

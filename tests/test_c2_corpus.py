@@ -22,8 +22,8 @@ def test_c2_fixture_inputs_pinned():
     from paper_2403_13839_b200.synth import codejson
 
     recs = _recs()
-    assert len(recs) == 220 and all(r["status"] == "ok" for r in recs)
-    assert sorted({r["minor"] for r in recs}) == [10, 11]
+    assert len(recs) == 330 and all(r["status"] == "ok" for r in recs)
+    assert sorted({r["minor"] for r in recs}) == [9, 10, 11]
     for r, co in zip(recs, inputs(recs)):
         assert codejson.to_json(co) == r["tree"]
         h = hashlib.sha256()
@@ -124,3 +124,18 @@ def test_codegen311_try_except_layout_and_exception_table():
     assert ("LOAD_GLOBAL", 3) in ops  # NULL + repr
     # entries (start, size, target, depth<<1|lasti) in code units, varint encoded
     assert fn.exceptiontable == bytes([0x82, 7, 10, 0, 0x8a, 10, 59, 3, 0x94, 28, 54, 3, 0xb0, 1, 59, 3, 0xb6, 5, 59, 3])
+
+
+def test_codegen39_leading_test_while_loop():
+    # CPython 3.9: test at the top, JUMP_ABSOLUTE back to it, byte-offset jump args
+    from paper_2403_13839_b200._optables import TABLES
+    from paper_2403_13839_b200.synth import pycodegen39
+
+    mod = pycodegen39.compile_source("def f(n):\n    total = 0\n    while n > 0:\n        total += n\n"
+                                     "        n -= 1\n    return total\n")
+    code = next(c.value for c in mod.consts if c.kind == "code").code
+    ops = [(TABLES[9][code[i]][0], code[i + 1]) for i in range(0, len(code), 2)]
+    assert ops == [("LOAD_CONST", 1), ("STORE_FAST", 1), ("LOAD_FAST", 0), ("LOAD_CONST", 1), ("COMPARE_OP", 4),
+                   ("POP_JUMP_IF_FALSE", 30), ("LOAD_FAST", 1), ("LOAD_FAST", 0), ("INPLACE_ADD", 0),
+                   ("STORE_FAST", 1), ("LOAD_FAST", 0), ("LOAD_CONST", 2), ("INPLACE_SUBTRACT", 0),
+                   ("STORE_FAST", 0), ("JUMP_ABSOLUTE", 4), ("LOAD_FAST", 1), ("RETURN_VALUE", 0)]
