@@ -17,6 +17,7 @@ POOLS = {
     "c2_310": {"gen": "c2", "minor": 10, "size": 110},
     "c2_311": {"gen": "c2", "minor": 11, "size": 110},
     "c2_39": {"gen": "c2", "minor": 9, "size": 110},
+    "c2_38": {"gen": "c2", "minor": 8, "size": 110},
 }
 
 

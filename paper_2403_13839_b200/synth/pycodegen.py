@@ -1980,8 +1980,22 @@ def _effect(op, arg, jump):
         return (arg & 0xFF) + (arg >> 8)
     if op == "FOR_ITER":
         return -1 if jump else 1
-    if op in ("BUILD_TUPLE", "BUILD_LIST", "BUILD_SET", "BUILD_STRING"):
+    if op in ("BUILD_TUPLE", "BUILD_LIST", "BUILD_SET", "BUILD_STRING",
+              # 3.8 (pycodegen38.py)
+              "BUILD_TUPLE_UNPACK", "BUILD_LIST_UNPACK", "BUILD_SET_UNPACK", "BUILD_MAP_UNPACK",
+              "BUILD_TUPLE_UNPACK_WITH_CALL", "BUILD_MAP_UNPACK_WITH_CALL"):
         return 1 - arg
+    # 3.8 finally machinery (Python/compile.c 3.8 stack_effect)
+    if op == "BEGIN_FINALLY":
+        return 6
+    if op in ("END_FINALLY", "POP_FINALLY"):
+        return -6 if op == "END_FINALLY" else 0
+    if op == "CALL_FINALLY":
+        return 1 if jump else 0
+    if op == "WITH_CLEANUP_START":
+        return 2
+    if op == "WITH_CLEANUP_FINISH":
+        return -3
     if op == "BUILD_MAP":
         return 1 - 2 * arg
     if op == "BUILD_CONST_KEY_MAP":

@@ -1,7 +1,7 @@
 """C2 golden vectors (BASELINE.json configs[1]): the
 reference's syntax corpus `pkg/corpus/<category>/*.py` (110 modules) compiled
-to CPython 3.9, 3.10 and 3.11 code objects by the in-repo code generators
-(paper_2403_13839_b200/synth/pycodegen39.py, pycodegen.py, pycodegen311.py), then decompiled by the REAL
+to CPython 3.8-3.11 code objects by the in-repo code generators
+(paper_2403_13839_b200/synth/pycodegen38.py, pycodegen39.py, pycodegen.py, pycodegen311.py), then decompiled by the REAL
 reference (unpyre.decompile_source, imported from /root/reference/pkg/src).
 Run in the build container:
 
@@ -29,7 +29,8 @@ from unpyre.pyc import load_pyc  # noqa: E402
 from helpers import code_key_sha  # noqa: E402
 from make_golden import input_sha, run_ref  # noqa: E402
 from paper_2403_13839_b200 import arena  # noqa: E402
-from paper_2403_13839_b200.synth import codejson, marshal, pycodegen, pycodegen39, pycodegen311  # noqa: E402
+from paper_2403_13839_b200.synth import (codejson, marshal, pycodegen, pycodegen38, pycodegen39,  # noqa: E402
+                                         pycodegen311)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CORPUS = "/root/reference/pkg/corpus"
@@ -49,7 +50,8 @@ def main():
     path = os.path.join(HERE, "c2.jsonl")
     n_ok = n = 0
     with open(path, "w") as f:
-        for minor, compile_source in ((9, pycodegen39.compile_source), (10, pycodegen.compile_source),
+        for minor, compile_source in ((8, pycodegen38.compile_source), (9, pycodegen39.compile_source),
+                                     (10, pycodegen.compile_source),
                                      (11, pycodegen311.compile_source)):
             for fn in files:
                 rel = os.path.relpath(fn, CORPUS)
@@ -66,7 +68,7 @@ def main():
                     f.write(json.dumps(rec) + "\n")
                     n += 1
                     n_ok += status == "ok"
-    print(f"c2: {n} cases ({len(files)} modules x 3 versions x {len(STYLES)} styles), {n_ok} ok -> {path}")
+    print(f"c2: {n} cases ({len(files)} modules x 4 versions x {len(STYLES)} styles), {n_ok} ok -> {path}")
 
 
 if __name__ == "__main__":

@@ -22,8 +22,8 @@ def test_c2_fixture_inputs_pinned():
     from paper_2403_13839_b200.synth import codejson
 
     recs = _recs()
-    assert len(recs) == 330 and all(r["status"] == "ok" for r in recs)
-    assert sorted({r["minor"] for r in recs}) == [9, 10, 11]
+    assert len(recs) == 440 and all(r["status"] == "ok" for r in recs)
+    assert sorted({r["minor"] for r in recs}) == [8, 9, 10, 11]
     for r, co in zip(recs, inputs(recs)):
         assert codejson.to_json(co) == r["tree"]
         h = hashlib.sha256()
@@ -139,3 +139,19 @@ def test_codegen39_leading_test_while_loop():
                    ("POP_JUMP_IF_FALSE", 30), ("LOAD_FAST", 1), ("LOAD_FAST", 0), ("INPLACE_ADD", 0),
                    ("STORE_FAST", 1), ("LOAD_FAST", 0), ("LOAD_CONST", 2), ("INPLACE_SUBTRACT", 0),
                    ("STORE_FAST", 0), ("JUMP_ABSOLUTE", 4), ("LOAD_FAST", 1), ("RETURN_VALUE", 0)]
+
+
+def test_codegen38_finally_and_exception_match():
+    # CPython 3.8: BEGIN_FINALLY / END_FINALLY / CALL_FINALLY finally machinery,
+    # COMPARE_OP 10 (exception match), BUILD_LIST_UNPACK for starred displays
+    from paper_2403_13839_b200._optables import TABLES
+    from paper_2403_13839_b200.synth import pycodegen38
+
+    mod = pycodegen38.compile_source("def f(a, xs):\n    try:\n        return g(a)\n    except KeyError:\n"
+                                     "        pass\n    finally:\n        h()\n    return [*xs, 1]\n")
+    code = next(c.value for c in mod.consts if c.kind == "code").code
+    names = [TABLES[8][code[i]][0] for i in range(0, len(code), 2)]
+    for op in ("SETUP_FINALLY", "CALL_FINALLY", "BEGIN_FINALLY", "END_FINALLY", "POP_EXCEPT",
+               "BUILD_LIST_UNPACK"):
+        assert op in names, op
+    assert ("COMPARE_OP", 10) in [(TABLES[8][code[i]][0], code[i + 1]) for i in range(0, len(code), 2)]
