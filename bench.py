@@ -210,7 +210,6 @@ def main():
     ap.add_argument("--slots", type=int, default=0)
     ap.add_argument("--arena-bytes", type=int, default=0)
     ap.add_argument("--tpb", type=int, default=0)
-    ap.add_argument("--schedule", type=int, default=None, help="decompile-kernel schedule (0 queue, 1 lockstep)")
     ap.add_argument("--verify-stride", type=int, default=0, help="check every k-th output (0: 1, c5: 16)")
     ap.add_argument("--pyc", type=int, default=1, help="also time the .pyc-bytes end-to-end path (0: skip)")
     args = ap.parse_args()
@@ -246,7 +245,7 @@ def main():
     t_gen = time.time() - t_gen
     n_roots = arena.n_roots
     da = DeviceArena(arena, device=f"cuda:{local}", slots=args.slots, arena_bytes=args.arena_bytes,
-                     threads_per_block=args.tpb, schedule=args.schedule)
+                     threads_per_block=args.tpb)
     da.upload()
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
@@ -358,8 +357,7 @@ def main():
                    "python": POOLS[pool_name]["minor"], "code_bytes_per_gpu": code_bytes,
                    "instructions_per_gpu": n_instr,
                    "l2": f"inputs larger than L2 ({h2d / 1e9:.2f} GB arena + {12 * n_instr / 1e9:.2f} GB records)",
-                   "parallelism": f"shard roots x{world}", "gen_seconds": round(t_gen, 1),
-                   "schedule": int(da.opts.schedule)},
+                   "parallelism": f"shard roots x{world}", "gen_seconds": round(t_gen, 1)},
         "bytecode_gbs": code_bytes * world / (ms_step / 1000.0) / 1e9,
         "kernel_ms": {"decode": dec_sum / args.steps, "decompile": st_sum / args.steps},
         "parity": {"checked": n_checked, "mismatches": n_bad, "against": "reference SHA-256 (pools.json)"},
@@ -404,7 +402,7 @@ def pyc_e2e(pool, reps, local, args, pool_name, n_pool, barrier):
         t0 = time.perf_counter()
         arena, per_file = load_pyc_buffer(buf, offs, sizes, pinned=True)
         t1 = time.perf_counter()
-        da = DeviceArena(arena, device=f"cuda:{local}", schedule=args.schedule)
+        da = DeviceArena(arena, device=f"cuda:{local}")
         da.upload()
         da.run()
         res = da.fetch()

@@ -86,8 +86,7 @@ typedef struct {
   uint64_t arena_bytes;      /* bytes per slot arena; 0 = auto from max_code_len */
   int32_t decode_only;       /* 1: run only the decode kernel */
   int32_t skip_decode;       /* 1: reuse the records of a previous decode_only call on the same workspace */
-  int32_t schedule;          /* 0: each thread takes the next root; 1: a warp takes 32 roots and runs
-                                the pipeline stages in lockstep */
+  int32_t schedule;          /* reserved, must be 0 (one decompile schedule: each thread takes the next root) */
 } upy_options;
 
 /* Per-root results (device pointers, caller-allocated). */

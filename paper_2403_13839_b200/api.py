@@ -21,9 +21,6 @@ from .arena import Arena, pack
 from .errors import RETRYABLE, ST_OK, DeviceCapacityError, make_exception
 
 
-# decompile-kernel schedule (upy_options.schedule): 0 = per-thread root queue,
-# 1 = warp-lockstep stages
-DEFAULT_SCHEDULE = int(os.environ.get("UPY_SCHEDULE", "0"))
 
 
 def _torch():
@@ -62,7 +59,7 @@ class DeviceArena:
     `run()` on HBM-resident inputs and `upload()+run()+fetch()` end to end)."""
 
     def __init__(self, arena: Arena, style=None, device=None, text_cap=None, arena_bytes=0, slots=0,
-                 threads_per_block=0, pinned=None, schedule=None):
+                 threads_per_block=0, pinned=None):
         torch = _torch()
         self.torch = torch
         self.lib = _lib.load()
@@ -74,8 +71,7 @@ class DeviceArena:
         self.dev = torch.empty(self.host.numel(), dtype=torch.uint8, device=self.device)
         self.A = _abi.arena_struct(arena, self.dev.data_ptr())
         self.opts = _abi.options(style, arena_bytes=arena_bytes, slots=slots,
-                                 threads_per_block=threads_per_block,
-                                 schedule=DEFAULT_SCHEDULE if schedule is None else schedule)
+                                 threads_per_block=threads_per_block)
         ws = C.c_size_t(0)
         _lib.check(self.lib.upy_query_workspace(C.byref(self.A), C.byref(self.opts), C.byref(ws)),
                    "upy_query_workspace")

@@ -119,7 +119,7 @@ HD NOINL bool load_instructions(Dc* C, Code* K, u32 oi) {
   const upy_ins* src = C->ins_all + (K->o->code_off >> 1);
   for (i32 i = 0; i < n; i++) {
     const upy_ins& r = src[i];
-    u32 e = optab(K->minor, r.opcode);
+    u32 e = optab_div(K->minor, r.opcode);
     Ins& x = K->ins[i];
     x.offset = r.offset;
     x.arg = r.arg;
@@ -315,7 +315,7 @@ HD NOINL Vec<TryRegion>* match_try_regions(Dc* C, const Code* K, const Vec<ExcEn
 HD inline void link(Dc* C, Cfg* G, i32 src, u32 dst_off, u8 kind) {
   i32 dst = block_at(G, dst_off);
   if (dst < 0) {
-    py_error(C, UPY_ST_PY_KEY_ERROR, "block_at lookup");
+    py_key_error(C, dst_off);  // cfg.py:100 block_at[dst_offset]
     return;
   }
   vpush(C, G->blocks[src].succ, dst);

@@ -61,6 +61,18 @@ static const char* const UPY_CMPOP_HOST[UPY_NCMP_ALL] = UPY_CMPOP_INIT;
 #endif
 
 HD inline u32 optab(int minor, u32 opcode) { return T_OPTABLE[minor - 8][opcode & 0xFF]; }
+#if defined(UPY_SMEM_OPTAB) && defined(__CUDACC__)
+// The decompile kernel stages the opcode tables in shared memory: per-thread
+// objects make the lookups divergent, and divergent __constant__ reads serialize.
+__shared__ u32 upy_s_optab[4][256];
+#endif
+HD inline u32 optab_div(int minor, u32 opcode) {
+#if defined(UPY_SMEM_OPTAB) && defined(__CUDA_ARCH__)
+  return upy_s_optab[minor - 8][opcode & 0xFF];
+#else
+  return optab(minor, opcode);
+#endif
+}
 HD inline const char* opname_of(int op) { return T_OPNAMES[op]; }
 
 HD inline size_t cstrlen(const char* s) {
@@ -154,6 +166,9 @@ HD inline void zero16(void* p, u64 bytes) {
 #ifdef __CUDA_ARCH__
   uint4* q = (uint4*)p;
   const uint4 z = make_uint4(0, 0, 0, 0);
+  // not unrolled: inlined at ~2000 call sites, unrolled copies were 29% of the
+  // kernel's SASS and the instruction-cache misses they caused its top stall
+#pragma unroll 1
   for (u64 i = 0, n = bytes >> 4; i < n; i++) q[i] = z;
 #else
   memset(p, 0, bytes);
@@ -163,6 +178,7 @@ HD inline void copy16(void* dst, const void* src, u64 bytes) {  // both 16-align
 #ifdef __CUDA_ARCH__
   uint4* d = (uint4*)dst;
   const uint4* s = (const uint4*)src;
+#pragma unroll 1
   for (u64 i = 0, n = (bytes + 15) >> 4; i < n; i++) d[i] = s[i];
 #else
   memcpy(dst, src, bytes);
@@ -173,21 +189,31 @@ HD inline void copy16(void* dst, const void* src, u64 bytes) {  // both 16-align
 #ifndef UPY_ALLOC_HOOK
 #define UPY_ALLOC_HOOK(bytes)
 #endif
+#if !defined(UPY_INLINE_SLOW) && defined(__CUDA_ARCH__)
+// Cold paths live out of line: every helper below is inlined at thousands of
+// call sites, and their rarely taken branches (overflow handling, vector growth,
+// message formatting) were most of the decompile kernel's 8 MB of SASS.
+#define SLOWPATH NOINL inline
+#else
+#define SLOWPATH inline
+#endif
+HD SLOWPATH void* alloc_overflow(Dc* C, u64 bytes) {
+  if (!C->err) {
+    C->err = UPY_ST_ARENA_OVERFLOW;
+    C->aux0 = (i64)C->used;
+    C->aux1 = (i64)bytes;
+  }
+  u64 z = bytes < SINK_BYTES ? bytes : SINK_BYTES;
+  zero16(C->sink, z);
+  return C->sink;
+}
 HD inline void* alloc_raw(Dc* C, u64 bytes, bool zero) {
   bytes = (bytes + 15) & ~(u64)15;
   UPY_ALLOC_HOOK(bytes);
-  if (C->used + bytes > C->top) {
-    if (!C->err) {
-      C->err = UPY_ST_ARENA_OVERFLOW;
-      C->aux0 = (i64)C->used;
-      C->aux1 = (i64)bytes;
-    }
-    u64 z = bytes < SINK_BYTES ? bytes : SINK_BYTES;
-    zero16(C->sink, z);
-    return C->sink;
-  }
-  void* p = C->base + C->used;
-  C->used += bytes;
+  const u64 u = C->used;
+  if (u + bytes > C->top) return alloc_overflow(C, bytes);
+  void* p = C->base + u;
+  C->used = u + bytes;
   if (zero) zero16(p, bytes);
   return p;
 }
@@ -235,7 +261,7 @@ HD inline Vec<T>* vnew(Dc* C, u32 cap = 0) {
   return v;
 }
 template <class T>
-HD inline bool vgrow(Dc* C, Vec<T>* v, u32 need) {
+HD SLOWPATH bool vgrow(Dc* C, Vec<T>* v, u32 need) {
   if (need <= v->cap) return true;
   if (C->err) return false;
   u32 nc = v->cap ? v->cap * 2 : 4;
@@ -259,9 +285,12 @@ HD inline Vec<T>* vcopy(Dc* C, const Vec<T>* src, u32 lo = 0, u32 hi = 0xFFFFFFF
   if (lo > hi) lo = hi;
   Vec<T>* v = vnew<T>(C, hi - lo);
   if (C->err) return v;
-  if (lo == 0 && hi) copy16(v->d, src->d, (u64)hi * sizeof(T));
-  else
+  if (lo == 0 && hi) {
+    copy16(v->d, src->d, (u64)hi * sizeof(T));
+  } else {
+#pragma unroll 1
     for (u32 i = lo; i < hi; i++) v->d[i - lo] = src->d[i];
+  }
   v->n = hi - lo;
   return v;
 }
@@ -270,7 +299,8 @@ HD inline void vextend(Dc* C, Vec<T>* dst, const Vec<T>* src, u32 lo = 0, u32 hi
   if (!src) return;
   if (hi > src->n) hi = src->n;
   if (lo >= hi) return;
-  if (!vgrow(C, dst, dst->n + (hi - lo))) return;
+  if (dst->n + (hi - lo) > dst->cap && !vgrow(C, dst, dst->n + (hi - lo))) return;
+#pragma unroll 1
   for (u32 i = lo; i < hi; i++) dst->d[dst->n++] = src->d[i];
 }
 template <class T>
@@ -281,8 +311,12 @@ struct Text {
   char* d;
   u32 n, cap;
 };
+HD SLOWPATH bool t_grow_slow(Dc* C, Text* t, u32 need);
 HD inline bool t_grow(Dc* C, Text* t, u32 need) {
   if (need <= t->cap) return true;
+  return t_grow_slow(C, t, need);
+}
+HD SLOWPATH bool t_grow_slow(Dc* C, Text* t, u32 need) {
   if (C->err) return false;
   u32 nc = t->cap ? t->cap * 2 : 256;
   while (nc < need) nc *= 2;
@@ -297,6 +331,7 @@ HD inline void t_putn(Dc* C, Text* t, const char* p, u32 n) {
   if (!n) return;
   if (!t_grow(C, t, t->n + n)) return;
   char* d = t->d + t->n;
+#pragma unroll 1
   for (u32 i = 0; i < n; i++) d[i] = p[i];
   t->n += n;
 }
@@ -351,12 +386,13 @@ HD inline void fail_end(Dc* C, Text* t) {
   C->msg_len = t->n;
 }
 // Message appenders that work after err is set (fixed buffer, truncating).
-HD inline void m_putn(Dc* C, Text* t, const char* p, u32 n) {
+HD SLOWPATH void m_putn(Dc* C, Text* t, const char* p, u32 n) {
+#pragma unroll 1
   for (u32 i = 0; i < n && t->n < t->cap; i++) t->d[t->n++] = p[i];
 }
 HD inline void m_puts(Dc* C, Text* t, const char* s) { m_putn(C, t, s, (u32)cstrlen(s)); }
 HD inline void m_str(Dc* C, Text* t, Str s) { m_putn(C, t, s.p, s.n); }
-HD inline void m_i64(Dc* C, Text* t, i64 v) {
+HD SLOWPATH void m_i64(Dc* C, Text* t, i64 v) {
   char buf[24];
   int k = 0;
   u64 m = v < 0 ? (u64)(-(v + 1)) + 1 : (u64)v;
@@ -379,6 +415,13 @@ HD inline void fail_msg(Dc* C, int status, const char* m, i64 a0 = 0, i64 a1 = 0
   fail_end(C, &t);
 }
 HD inline void py_error(Dc* C, int status, const char* what) { fail_msg(C, status, what); }
+// KeyError on an int-keyed dict: str(KeyError(k)) is repr(k)
+HD inline void py_key_error(Dc* C, i64 key) {
+  Text t;
+  if (!fail_begin(C, UPY_ST_PY_KEY_ERROR, 0, 0, &t)) return;
+  m_i64(C, &t, key);
+  fail_end(C, &t);
+}
 
 // StackUnderflow(offset, opname)  errors.py:69-72
 HD inline void fail_underflow(Dc* C, const Ins* ins) {

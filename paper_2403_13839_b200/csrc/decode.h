@@ -14,6 +14,10 @@
 #include "common.h"
 
 #define EXT_OP 144
+// extra bits of the opcode-table entries the decode kernel stages in shared memory
+#define ENT_JUMP_BIT 31
+#define ENT_EXT_BIT 30
+#define ENT_PAD (1u << 29)
 
 // error aux conventions (consumed by cfg.h load_instructions):
 //   UNKNOWN_OPCODE: aux0 opcode, aux1 offset
@@ -188,15 +192,17 @@ __device__ __forceinline__ int decode_chunk(const u8* __restrict__ code, u32 len
   const u32 words[4] = {w.x, w.y, w.z, w.w};
 #define UNIT_OP(q) ((words[(q) >> 1] >> (16 * ((q) & 1))) & 0xFFu)
 #define UNIT_ARG(q) ((words[(q) >> 1] >> (16 * ((q) & 1) + 8)) & 0xFFu)
+  // staged entries carry two extra bits (decode_kernel.cu): ENT_JUMP (jump kinds)
+  // and ENT_EXT (EXTENDED_ARG); ENT_PAD marks units past the end (defined, inert)
   u32 ent[8];
-  u32 ext_mask = 0, unknown_mask = 0;
+#pragma unroll
+  for (int q = 0; q < 8; q++) ent[q] = (u32)q < nu ? tab[UNIT_OP(q)] : ENT_PAD;
+  u32 ext_mask = 0, unknown_mask = 0, jump_mask = 0;
 #pragma unroll
   for (int q = 0; q < 8; q++) {
-    ent[q] = (u32)q < nu ? tab[UNIT_OP(q)] : 0;
-    if ((u32)q < nu) {
-      if (UNIT_OP(q) == EXT_OP) ext_mask |= 1u << q;
-      if (!ent[q]) unknown_mask |= 1u << q;
-    }
+    unknown_mask |= (ent[q] == 0 ? 1u : 0u) << q;
+    ext_mask |= ((ent[q] >> ENT_EXT_BIT) & 1u) << q;
+    jump_mask |= (ent[q] >> ENT_JUMP_BIT) << q;
   }
   // first unknown opcode of the chunk (reference order) stops the object
   u32 has_unknown = __ballot_sync(0xffffffffu, unknown_mask != 0);
@@ -221,7 +227,6 @@ __device__ __forceinline__ int decode_chunk(const u8* __restrict__ code, u32 len
   ExtRun inc = {0, 0, 0};
   if (fast) {
     total = units - base < 256 ? units - base : 256;
-    const bool no_ext_obj = units <= 256;
     uint4* st4 = reinterpret_cast<uint4*>(stage) + 6 * lane;
 #pragma unroll
     for (int g = 0; g < 2; g++) {  // 4 records = 12 words = 3 uint4 per group
@@ -229,17 +234,23 @@ __device__ __forceinline__ int decode_chunk(const u8* __restrict__ code, u32 len
 #pragma unroll
       for (int r = 0; r < 4; r++) {
         const int q = 4 * g + r;
-        u32 u = u0 + q;
-        u32 e = ent[q];
-        u32 has_arg = UPY_ENT_HASARG(e) ? 1u : 0u;
-        u32 arg = has_arg ? UNIT_ARG(q) : 0u;
-        wr[3 * r] = 2 * u;
-        wr[3 * r + 1] = arg;
+        const u32 has_arg = UPY_ENT_HASARG(ent[q]);
+        wr[3 * r] = 2 * (u0 + q);
+        wr[3 * r + 1] = has_arg ? UNIT_ARG(q) : 0u;
         wr[3 * r + 2] = UNIT_OP(q) | (has_arg << 24);
-        u32 kind = UPY_ENT_KIND(e);
-        if ((u32)q < nu && my_bad < 0 && (kind == K_JUMP_REL || kind == K_JUMP_ABS || kind == K_JUMP_BACK)) {
+      }
+#pragma unroll
+      for (int k = 0; k < 3; k++) st4[3 * g + k] = make_uint4(wr[4 * k], wr[4 * k + 1], wr[4 * k + 2], wr[4 * k + 3]);
+    }
+    if (jump_mask) {  // straight-line code skips the jump checks entirely
+      const bool no_ext_obj = units <= 256;
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        if (((jump_mask >> q) & 1) && my_bad < 0) {
+          const u32 u = u0 + q;
+          const u32 arg = UPY_ENT_HASARG(ent[q]) ? UNIT_ARG(q) : 0u;
           bool okk;
-          i64 t = jump_target_u64(minor, kind, 2ull * u, arg, &okk);
+          i64 t = jump_target_u64(minor, UPY_ENT_KIND(ent[q]), 2ull * u, arg, &okk);
           bool valid = t >= 0 && t < (i64)len && !(t & 1) && (no_ext_obj || t == 0 || code[t - 2] != EXT_OP);
           if (!valid) {
             my_bad = st.n_before + 8 * lane + q;
@@ -248,8 +259,6 @@ __device__ __forceinline__ int decode_chunk(const u8* __restrict__ code, u32 len
           }
         }
       }
-#pragma unroll
-      for (int k = 0; k < 3; k++) st4[3 * g + k] = make_uint4(wr[4 * k], wr[4 * k + 1], wr[4 * k + 2], wr[4 * k + 3]);
     }
   } else {
     // lane summary of its 8 units

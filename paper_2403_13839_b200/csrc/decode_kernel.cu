@@ -64,14 +64,25 @@ __device__ __forceinline__ u32 n_chunks(u32 len, u32 minor) {
   return ((len >> 1) + 255) >> 8;
 }
 
-__global__ void __launch_bounds__(DWARPS * 32, 6) upy_decode_kernel(upy_arena A, upy_ins* __restrict__ ins,
+#ifndef DEC_MINB
+#define DEC_MINB 5  // 5 x 4 warps per SM at <= 96 registers (no spills): 0.712 ms vs 0.735 ms at 6
+#endif
+__global__ void __launch_bounds__(DWARPS * 32, DEC_MINB) upy_decode_kernel(upy_arena A, upy_ins* __restrict__ ins,
                                                                     upy_decoded* __restrict__ dec) {
   __shared__ u32 tab[3][256];  // 3.8-3.10 opcode tables
   __shared__ DecWarpSmem wsm[DWARPS];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   DecWarpSmem& S = wsm[wid];
-  for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) tab[i >> 8][i & 255] = UPY_OPTABLE_DEV[i >> 8][i & 255];
+  for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) {
+    u32 e = UPY_OPTABLE_DEV[i >> 8][i & 255];
+    if (e) {
+      const u32 k = UPY_ENT_KIND(e);
+      if (k == K_JUMP_REL || k == K_JUMP_ABS || k == K_JUMP_BACK) e |= 1u << ENT_JUMP_BIT;
+      if ((i & 255) == EXT_OP) e |= 1u << ENT_EXT_BIT;
+    }
+    tab[i >> 8][i & 255] = e;
+  }
   if (lane == 0) {
     for (int s = 0; s < DSTAGES; s++) mbar_init(&S.bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -152,6 +163,22 @@ __global__ void __launch_bounds__(DWARPS * 32, 6) upy_decode_kernel(upy_arena A,
       const u32 nch = n_chunks(len, minor);
       upy_ins* rec = ins + (off >> 1);
       if (nch == 0) {
+        if (minor == 11 && len && len <= (u32)sizeof(S.out)) {
+          // 3.11: instruction starts are a serial chain through the inline caches, so
+          // one lane walks it -- over a shared-memory copy of the code (coalesced
+          // 16-B loads by the warp) instead of dependent byte loads from global
+          // memory.  The record staging buffers hold the copy; their pending bulk
+          // stores must have read them first.
+          if (lane == 0) bulk_wait_all();
+          __syncwarp();
+          uint4* buf = reinterpret_cast<uint4*>(&S.out[0][0]);
+          const uint4* src = reinterpret_cast<const uint4*>(A.bytes + off);
+          for (u32 k = lane; k < (len + 15) / 16; k += 32) buf[k] = src[k];
+          __syncwarp();
+          if (lane == 0) decode_scalar(reinterpret_cast<const u8*>(buf), len, 11, rec, &dec[o]);
+          __syncwarp();
+          continue;
+        }
         if (lane == 0) {
           if (minor == 11 || ((minor >= 8 && minor <= 10) && (len == 0 || (len & 1)))) {
             decode_scalar(A.bytes + off, len, (int)minor, rec, &dec[o]);
@@ -220,7 +247,7 @@ __global__ void __launch_bounds__(DWARPS * 32, 6) upy_decode_kernel(upy_arena A,
 cudaError_t upy_decode_launch(const upy_arena* arena, upy_ins* ins, upy_decoded* dec, cudaStream_t s, int sms) {
   const i64 groups = (arena->n_objs + 31) / 32;
   i64 blocks = (groups + DWARPS - 1) / DWARPS;
-  const i64 max_blocks = (i64)sms * 6;
+  const i64 max_blocks = (i64)sms * DEC_MINB;
   if (blocks > max_blocks) blocks = max_blocks;
   upy_decode_kernel<<<(unsigned)blocks, DWARPS * 32, 0, s>>>(*arena, ins, dec);
   return cudaGetLastError();

@@ -9,6 +9,7 @@
 //                          then the text is appended to the flat output buffer.
 #include <cuda_runtime.h>
 #include <stdio.h>
+#define UPY_SMEM_OPTAB 1
 #include "pipeline.h"
 
 // decode_kernel.cu
@@ -32,7 +33,6 @@ struct KParams {
   u32* next_root;
   int header;
   int max_depth;
-  int schedule;  // 0: per-thread root queue, 1: warp-lockstep stages
   int indent_len, tool_len;
   char indent[64];
   char tool[64];
@@ -97,47 +97,27 @@ __global__ void __launch_bounds__(128, UPY_MINB) upy_decompile_kernel(KParams P)
   opt.header = P.header != 0;
   opt.indent = Str{P.indent, (u32)P.indent_len};
   opt.tool = Str{P.tool, (u32)P.tool_len};
-  // The per-thread context (arena cursor, sticky status, depth guard) is read
-  // after nearly every call; keeping it in shared memory instead of the local
-  // stack takes those accesses off the L1/L2/DRAM path.
+#ifndef UPY_DC_SHARED
+  // The per-thread context lives on the thread's stack: the shared-memory copy
+  // (17 KB per block, 139 KB per SM at 8 blocks) cost more in L1 capacity for the
+  // arena than it saved (C3 278.6 -> 261.4 ms with the context in local memory).
+  Dc C_local;
+  Dc& C = C_local;
+#else
   __shared__ Dc dcs[128];
   Dc& C = dcs[threadIdx.x];
+#endif
+  for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) upy_s_optab[i >> 8][i & 255] = UPY_OPTABLE_DEV[i >> 8][i & 255];
+  __syncthreads();
   const u64 n_roots = (u64)P.A.n_roots;
-  if (P.schedule == 0) {
-    // each thread takes the next root from the global queue
-    while (true) {
-      u32 r = atomicAdd(P.next_root, 1u);
-      if (r >= n_roots) break;
-      dc_reset(C, P, base);
-      Text out = {nullptr, 0, 0};
-      decompile_source(&C, (u32)P.A.roots[r], &opt, &out);
-      emit_result(P, C, r, out);
-    }
-  } else {
-    // warp lockstep: a warp takes 32 consecutive roots and runs each stage of
-    // decompile_source for all of them before the next stage, so the lanes
-    // execute the same code (instruction cache, SIMT efficiency)
-    const int lane = threadIdx.x & 31;
-    while (true) {
-      u32 b0 = 0;
-      if (lane == 0) b0 = atomicAdd(P.next_root, 32u);
-      b0 = __shfl_sync(0xffffffffu, b0, 0);
-      if (b0 >= n_roots) break;
-      u32 r = b0 + lane;
-      bool have = r < n_roots;
-      dc_reset(C, P, base);
-      Text out = {nullptr, 0, 0};
-      SourceJob S;
-      S.oi = have ? (u32)P.A.roots[r] : 0;
-      S.opt = &opt;
-      S.out = &out;
-      for (int st = 0; st < DS_STAGES; st++) {
-        if (have) ds_stage(&C, &S, st);
-        __syncwarp();
-      }
-      if (have) emit_result(P, C, r, out);
-      __syncwarp();
-    }
+  // each thread takes the next root from the global queue
+  while (true) {
+    u32 r = atomicAdd(P.next_root, 1u);
+    if (r >= n_roots) break;
+    dc_reset(C, P, base);
+    Text out = {nullptr, 0, 0};
+    decompile_source(&C, (u32)P.A.roots[r], &opt, &out);
+    emit_result(P, C, r, out);
   }
 }
 
@@ -155,8 +135,7 @@ static int sm_count() {
   return n;
 }
 
-// threads per block: <= 128 (shared Dc array), whole warps (the lockstep
-// schedule shuffles across all 32 lanes)
+// threads per block: <= 128 (shared Dc array), whole warps
 static int eff_tpb(const upy_options* o) {
   int tpb = o && o->threads_per_block > 0 && o->threads_per_block < 128 ? o->threads_per_block : 128;
   return tpb < 32 ? 32 : tpb & ~31;
@@ -173,6 +152,12 @@ static WsLayout layout(const upy_arena* a, const upy_options* o) {
   // measured peaks: C3 (400 B code) ~25 KB, C4 (19 KB code) ~2.2 MB => ~115 B per code byte
   u64 sb = o && o->arena_bytes ? o->arena_bytes : (u64)(64u << 10) + (u64)a->max_code_len * 160u;
   sb = (sb + SLOT_HEADER + 255) & ~(u64)255;
+#ifdef UPY_SLOT_STAGGER
+  // slot stride off the power-of-two grid: every thread starts allocating at the
+  // same offset of its slot, so a 2^k stride lines the hot lines of all slots up
+  // on the same L2 sets / DRAM banks
+  sb += UPY_SLOT_STAGGER;
+#endif
   L.slot_bytes = sb;
   u64 slots;
   if (o && o->slots > 0) {
@@ -277,7 +262,6 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
   P.slot_bytes = L.slot_bytes;
   P.next_root = ctr;
   P.max_depth = 600;
-  P.schedule = opt ? opt->schedule : 0;
   if (opt) {
     P.header = opt->header;
     P.indent_len = opt->indent_len > 64 ? 64 : opt->indent_len;

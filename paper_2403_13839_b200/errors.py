@@ -193,6 +193,12 @@ def make_exception(status, message, aux):
         ST_PY_VALUE_ERROR: ValueError,
         ST_PY_RECURSION_ERROR: RecursionError,
     }.get(status)
+    if py is KeyError:
+        # the device formats the missing key as repr(key); KeyError(key) has str == repr(key)
+        try:
+            return KeyError(int(message))
+        except ValueError:
+            return KeyError(message)
     if py is not None:
         return py(message)
     return DeviceCapacityError(f"device status {status}: {message}")

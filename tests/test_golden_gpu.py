@@ -33,24 +33,6 @@ def test_gpu_single_decompile_raises_reference_class():
     assert ei.value.offset == 0
 
 
-@pytest.mark.parametrize("gset", ["c2", "c4", "fuzz", "mutant", "snippets"])
-def test_gpu_lockstep_schedule_matches_reference(gset, monkeypatch):
-    """The warp-lockstep schedule (upy_options.schedule = 1) runs the same stages
-    in a different order across threads; results must be identical."""
-    from paper_2403_13839_b200 import api
-
-    monkeypatch.setattr(api, "DEFAULT_SCHEDULE", 1)
-    recs = golden_cases([gset])
-    by_style = {}
-    for r in recs:
-        by_style.setdefault(repr(r.get("style")), []).append(r)
-    bad = []
-    for _, group in by_style.items():
-        got = [outcome(v) for v in api.decompile_many(inputs(group), style_of(group[0]))]
-        bad += mismatches(group, got)
-    assert not bad, bad[:3]
-
-
 def test_gpu_c2_from_pyc_images_matches_reference():
     """C2 modules as .pyc images (synth/marshal.py) through the native loader and
     the kernels: same text as the reference decompiling the compiled tree."""
