@@ -44,6 +44,20 @@ WORKLOADS = {
 }
 
 
+def measured_traffic(workload, kernel):
+    """DRAM bytes (read + write) per launch of `kernel` on `workload`, from the
+    committed ncu capture of the same bench command (profiles/traffic.json, made by
+    tools/traffic_json.py from `ncu --metrics dram__bytes_read.sum,...`); None when
+    this configuration was not captured."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    v = d.get(workload, {}).get(kernel)
+    return None if v is None else float(v["bytes_per_launch"])
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -362,10 +376,12 @@ def main():
         "kernel_ms": {"decode": dec_sum / args.steps, "decompile": st_sum / args.steps},
         "parity": {"checked": n_checked, "mismatches": n_bad, "against": "reference SHA-256 (pools.json)"},
         "roofline": {"bound": "hbm", "kernel": "upy_decompile_kernel", "achieved": ach_struct, "peak": peak,
-                     "unit": "GB/s", "frac": ach_struct / peak, "traffic": None,
+                     "unit": "GB/s", "frac": ach_struct / peak,
+                     "traffic": measured_traffic(args.workload, "upy_decompile_kernel"),
                      "algorithmic_bytes_per_launch": alg_struct, "peak_source": peak_src},
         "roofline_decode": {"bound": "hbm", "kernel": "upy_decode_kernel", "achieved": ach_dec, "peak": peak,
-                            "unit": "GB/s", "frac": ach_dec / peak, "traffic": None,
+                            "unit": "GB/s", "frac": ach_dec / peak,
+                            "traffic": measured_traffic(args.workload, "upy_decode_kernel"),
                             "algorithmic_bytes_per_launch": alg_dec},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "objects/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

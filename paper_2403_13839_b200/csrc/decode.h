@@ -181,9 +181,14 @@ __device__ __forceinline__ void chunk_state_init(ChunkState& st) {
 // version's opcode table in shared memory; stage: 256 records of shared
 // memory the chunk's records are written to (the caller stores them out).
 // Returns the number of records, or -1 after an UnknownOpcode (res written).
+// 3.11 (decode_kernel.cu): `skip` marks this lane's units that lie inside an
+// instruction's inline-cache span (neither instructions nor EXTENDED_ARG), and
+// `xs` is the object's extent-start bitmap for jump validation (nullptr: the
+// <=3.10 rule "in range and the previous unit is not EXTENDED_ARG").
 __device__ __forceinline__ int decode_chunk(const u8* __restrict__ code, u32 len, int minor, u32 base,
                                             const u32* __restrict__ tab, upy_ins* stage, uint4 w,
-                                            ChunkState& st, upy_decoded* res) {
+                                            ChunkState& st, upy_decoded* res, u32 skip = 0,
+                                            const u32* __restrict__ xs = nullptr) {
   const int lane = threadIdx.x & 31;
   const u32 units = len >> 1;
   const u32 u0 = base + 8 * lane;
@@ -204,6 +209,9 @@ __device__ __forceinline__ int decode_chunk(const u8* __restrict__ code, u32 len
     ext_mask |= ((ent[q] >> ENT_EXT_BIT) & 1u) << q;
     jump_mask |= (ent[q] >> ENT_JUMP_BIT) << q;
   }
+  unknown_mask &= ~skip;
+  ext_mask &= ~skip;
+  jump_mask &= ~skip;
   // first unknown opcode of the chunk (reference order) stops the object
   u32 has_unknown = __ballot_sync(0xffffffffu, unknown_mask != 0);
   if (has_unknown) {
@@ -221,7 +229,10 @@ __device__ __forceinline__ int decode_chunk(const u8* __restrict__ code, u32 len
   // every unit is one instruction, lane L's records start at 8*L and need no
   // scans; a single-chunk object with no EXTENDED_ARG also has every even
   // in-range offset as an extent start.
-  const bool fast = __ballot_sync(0xffffffffu, ext_mask != 0) == 0 && st.carry.len == 0;
+  // (the fast path stores 8 records per lane -- also past the end of the object --
+  // as whole uint4 groups: only into a shared-memory staging area, xs == nullptr)
+  const bool fast = xs == nullptr && __ballot_sync(0xffffffffu, (ext_mask | skip) != 0) == 0 &&
+                    st.carry.len == 0;
   u32 total;
   i64 my_bad = -1, my_bad_off = 0, my_bad_tgt = 0;
   ExtRun inc = {0, 0, 0};
@@ -237,7 +248,7 @@ __device__ __forceinline__ int decode_chunk(const u8* __restrict__ code, u32 len
         const u32 has_arg = UPY_ENT_HASARG(ent[q]);
         wr[3 * r] = 2 * (u0 + q);
         wr[3 * r + 1] = has_arg ? UNIT_ARG(q) : 0u;
-        wr[3 * r + 2] = UNIT_OP(q) | (has_arg << 24);
+        wr[3 * r + 2] = UNIT_OP(q) | (UPY_ENT_CACHE(ent[q]) << 16) | (has_arg << 24);
       }
 #pragma unroll
       for (int k = 0; k < 3; k++) st4[3 * g + k] = make_uint4(wr[4 * k], wr[4 * k + 1], wr[4 * k + 2], wr[4 * k + 3]);
@@ -251,7 +262,9 @@ __device__ __forceinline__ int decode_chunk(const u8* __restrict__ code, u32 len
           const u32 arg = UPY_ENT_HASARG(ent[q]) ? UNIT_ARG(q) : 0u;
           bool okk;
           i64 t = jump_target_u64(minor, UPY_ENT_KIND(ent[q]), 2ull * u, arg, &okk);
-          bool valid = t >= 0 && t < (i64)len && !(t & 1) && (no_ext_obj || t == 0 || code[t - 2] != EXT_OP);
+          bool valid = t >= 0 && t < (i64)len && !(t & 1) &&
+                       (xs ? ((xs[t >> 6] >> ((t >> 1) & 31)) & 1u) != 0
+                           : (no_ext_obj || t == 0 || code[t - 2] != EXT_OP));
           if (!valid) {
             my_bad = st.n_before + 8 * lane + q;
             my_bad_off = 2 * u;
@@ -292,7 +305,7 @@ __device__ __forceinline__ int decode_chunk(const u8* __restrict__ code, u32 len
     if (lane == 0) excl = ExtRun{1, 0, 0};
     excl = ext_combine(st.carry, excl);
     // instruction slots: non-EXT units before this lane
-    u32 my_ins = (u32)__popc((~ext_mask) & (nu >= 8 ? 0xFF : ((1u << nu) - 1)));
+    u32 my_ins = (u32)__popc((~(ext_mask | skip)) & (nu >= 8 ? 0xFF : ((1u << nu) - 1)));
     u32 pre = my_ins;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -307,6 +320,7 @@ __device__ __forceinline__ int decode_chunk(const u8* __restrict__ code, u32 len
     for (int q = 0; q < 8; q++) {
       if ((u32)q >= nu) continue;
       u32 u = u0 + q;
+      if ((skip >> q) & 1) continue;  // inline cache unit (3.11)
       if ((ext_mask >> q) & 1) {
         run_val = (run_val << 8) | UNIT_ARG(q);
         run_len++;
@@ -322,12 +336,14 @@ __device__ __forceinline__ int decode_chunk(const u8* __restrict__ code, u32 len
       u32 off = 2 * (u - run_len);
       sw[0] = off;
       sw[1] = big ? 0xFFFFFFFFu : (u32)arg;
-      sw[2] = UNIT_OP(q) | ((run_len > 255 ? 255u : run_len) << 8) | (((has_arg ? 1u : 0u) | (big ? 2u : 0u)) << 24);
+      sw[2] = UNIT_OP(q) | ((run_len > 255 ? 255u : run_len) << 8) | (UPY_ENT_CACHE(e) << 16) |
+              (((has_arg ? 1u : 0u) | (big ? 2u : 0u)) << 24);
       u32 kind = UPY_ENT_KIND(e);
       if (my_bad < 0 && (kind == K_JUMP_REL || kind == K_JUMP_ABS || kind == K_JUMP_BACK)) {
         bool okk;
         i64 t = jump_target_u64(minor, kind, 2ull * u, arg, &okk);
-        bool valid = !big && t >= 0 && t < (i64)len && !(t & 1) && (t == 0 || code[t - 2] != EXT_OP);
+        bool valid = !big && t >= 0 && t < (i64)len && !(t & 1) &&
+                     (xs ? ((xs[t >> 6] >> ((t >> 1) & 31)) & 1u) != 0 : (t == 0 || code[t - 2] != EXT_OP));
         if (!valid) {
           my_bad = idx;
           my_bad_off = off;

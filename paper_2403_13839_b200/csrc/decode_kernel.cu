@@ -23,9 +23,13 @@
 #define DSTAGES 4
 #define DWARPS 4  // warps per block
 
+#define X11_UNITS 3072  // 3.11 objects up to 6 KB of code take the warp path
+
 struct __align__(128) DecWarpSmem {
   uint4 in[DSTAGES][32];    // DSTAGES x 512 B of code
-  upy_ins out[2][256];      // 2 x 3 KB of records
+  upy_ins out[2][256];      // 2 x 3 KB of records (3.11: the object's code copy)
+  u32 cov[X11_UNITS / 32];  // 3.11: units inside an inline-cache span
+  u32 xs[X11_UNITS / 32];   // 3.11: extent starts (jump targets)
   unsigned long long bar[DSTAGES];
 };
 
@@ -67,14 +71,143 @@ __device__ __forceinline__ u32 n_chunks(u32 len, u32 minor) {
 #ifndef DEC_MINB
 #define DEC_MINB 5  // 5 x 4 warps per SM at <= 96 registers (no spills): 0.712 ms vs 0.735 ms at 6
 #endif
+// 3.11: inline caches make instruction starts a serial chain.  The warp copies the
+// code into shared memory (coalesced), marks cache-covered units and extent starts
+// in two bitmaps with a speculative warp prefix-max scan over cache-span ends
+// (pass 1), then decodes the object 256 units at a time with decode_chunk,
+// skipping covered units, folding EXTENDED_ARG with the scans and validating jumps
+// against the extent-start bitmap; records go straight to global memory.  Any
+// decode error or failed speculation sends the object to the scalar
+// reference-order decoder (same shared-memory copy), so error semantics are
+// decode_scalar's.
+__device__ __noinline__ void decode311_warp(const u8* __restrict__ gcode, u32 len, upy_ins* __restrict__ rec,
+                                            upy_decoded* res, const u32* __restrict__ tab, DecWarpSmem& S) {
+  const int lane = threadIdx.x & 31;
+  const u32 units = len >> 1;
+  if (lane == 0) bulk_wait_all();  // the staging buffers are about to hold the code
+  __syncwarp();
+  uint4* buf = reinterpret_cast<uint4*>(&S.out[0][0]);
+  const uint4* src = reinterpret_cast<const uint4*>(gcode);
+  for (u32 k = lane; k < (len + 15) / 16; k += 32) buf[k] = src[k];
+  const u32 nwords = (units + 31) / 32;
+  for (u32 k = lane; k < nwords; k += 32) S.cov[k] = S.xs[k] = 0;
+  __syncwarp();
+  const u8* code = reinterpret_cast<const u8*>(buf);
+  // Pass 1 (warp-parallel, speculative): every unit's span end = u + cache(op(u));
+  // a unit is covered iff an earlier unit's span reaches it (warp prefix-max scan,
+  // carried across chunks).  Exact when no covered unit has caches of its own
+  // (real cache slots hold CACHE = 0); anything else -- such a conflict, an
+  // unknown opcode, caches or an EXTENDED_ARG run past the end -- goes to the
+  // scalar decoder, which reports errors in reference order.
+  int ok = 1;
+  int cmax = -1;          // max span end of earlier chunks
+  u32 prev_ext = 0;       // last unit of the previous chunk is an uncovered EXTENDED_ARG
+  for (u32 base = 0; base < units; base += 256) {
+    const u32 u0 = base + 8 * lane;
+    u32 nu = 0;
+    if (u0 < units) nu = units - u0 < 8 ? units - u0 : 8;
+    const uint4 w = u0 < units ? buf[u0 >> 3] : make_uint4(0, 0, 0, 0);
+    const u32 words[4] = {w.x, w.y, w.z, w.w};
+    int se[8];
+    u32 ent[8];
+    int lane_max = -1;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const u32 op = (words[q >> 1] >> (16 * (q & 1))) & 0xFFu;
+      ent[q] = (u32)q < nu ? tab[op] : ENT_PAD;
+      se[q] = (u32)q < nu ? (int)(u0 + q + UPY_ENT_CACHE(ent[q])) : -1;
+      lane_max = se[q] > lane_max ? se[q] : lane_max;
+    }
+    int inc = lane_max;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int o = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc = o > inc ? o : inc;
+    }
+    int run = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane == 0) run = -1;
+    run = run > cmax ? run : cmax;
+    u32 cov_bits = 0, xs_bits = 0, bad = 0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      if ((u32)q >= nu) continue;
+      const int u = (int)(u0 + q);
+      const bool covered = run >= u;
+      if (covered) {
+        cov_bits |= 1u << q;
+        if (se[q] > u) bad = 1;                              // a cache slot with caches
+      } else {
+        if (!ent[q]) bad = 1;                                // unknown opcode
+        if (se[q] >= (int)units) bad = 1;                    // caches past the end
+      }
+      run = se[q] > run ? se[q] : run;
+    }
+    // extent starts: uncovered units not preceded by an uncovered EXTENDED_ARG
+    const u32 ext_bits = [&] {
+      u32 m = 0;
+#pragma unroll
+      for (int q = 0; q < 8; q++)
+        if ((u32)q < nu && !((cov_bits >> q) & 1u) && ((ent[q] >> ENT_EXT_BIT) & 1u)) m |= 1u << q;
+      return m;
+    }();
+    u32 prev_last = __shfl_up_sync(0xffffffffu, (ext_bits >> 7) & 1u, 1);
+    if (lane == 0) prev_last = prev_ext;
+    const u32 prev_of = ((ext_bits << 1) | prev_last) & 0xFFu;  // bit q: unit q-1 is an uncovered EXT
+    xs_bits = ~cov_bits & ~prev_of & (nu >= 8 ? 0xFFu : ((1u << nu) - 1));
+    if (u0 < units) {
+      reinterpret_cast<u8*>(S.cov)[u0 >> 3] = (u8)cov_bits;
+      reinterpret_cast<u8*>(S.xs)[u0 >> 3] = (u8)xs_bits;
+    }
+    if (__ballot_sync(0xffffffffu, bad)) {
+      ok = 0;
+      break;
+    }
+    cmax = __shfl_sync(0xffffffffu, inc, 31);
+    prev_ext = __shfl_sync(0xffffffffu, (ext_bits >> 7) & 1u, 31);
+  }
+  // an EXTENDED_ARG run reaching the end of the code: the scalar decoder's error
+  __syncwarp();
+  if (ok) {
+    const u32 last = units - 1;
+    const bool end_ext = !((S.cov[last >> 5] >> (last & 31)) & 1u) && code[2 * last] == EXT_OP;
+    if (end_ext) ok = 0;
+  }
+  __syncwarp();
+  if (!ok) {
+    if (lane == 0) decode_scalar(code, len, 11, rec, res);
+    __syncwarp();
+    return;
+  }
+  ChunkState st;
+  chunk_state_init(st);
+  for (u32 base = 0; base < units; base += 256) {
+    const u32 u0 = base + 8 * lane;
+    uint4 w = make_uint4(0, 0, 0, 0);
+    u32 skip = 0;
+    if (u0 < units) {
+      w = buf[u0 >> 3];
+      skip = (S.cov[u0 >> 5] >> (u0 & 31)) & 0xFFu;
+    }
+    const int total = decode_chunk(code, len, 11, base, tab, rec + st.n_before, w, st, res, skip, S.xs);
+    if (total < 0) {  // cannot happen after pass 1 (unknown opcodes are caught there)
+      if (lane == 0) decode_scalar(code, len, 11, rec, res);
+      __syncwarp();
+      return;
+    }
+    st.n_before += (u32)total;
+  }
+  if (lane == 0) chunk_finish(len, st, res);
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(DWARPS * 32, DEC_MINB) upy_decode_kernel(upy_arena A, upy_ins* __restrict__ ins,
                                                                     upy_decoded* __restrict__ dec) {
-  __shared__ u32 tab[3][256];  // 3.8-3.10 opcode tables
+  __shared__ u32 tab[4][256];  // 3.8-3.11 opcode tables
   __shared__ DecWarpSmem wsm[DWARPS];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   DecWarpSmem& S = wsm[wid];
-  for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) {
+  for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) {
     u32 e = UPY_OPTABLE_DEV[i >> 8][i & 255];
     if (e) {
       const u32 k = UPY_ENT_KIND(e);
@@ -163,20 +296,8 @@ __global__ void __launch_bounds__(DWARPS * 32, DEC_MINB) upy_decode_kernel(upy_a
       const u32 nch = n_chunks(len, minor);
       upy_ins* rec = ins + (off >> 1);
       if (nch == 0) {
-        if (minor == 11 && len && len <= (u32)sizeof(S.out)) {
-          // 3.11: instruction starts are a serial chain through the inline caches, so
-          // one lane walks it -- over a shared-memory copy of the code (coalesced
-          // 16-B loads by the warp) instead of dependent byte loads from global
-          // memory.  The record staging buffers hold the copy; their pending bulk
-          // stores must have read them first.
-          if (lane == 0) bulk_wait_all();
-          __syncwarp();
-          uint4* buf = reinterpret_cast<uint4*>(&S.out[0][0]);
-          const uint4* src = reinterpret_cast<const uint4*>(A.bytes + off);
-          for (u32 k = lane; k < (len + 15) / 16; k += 32) buf[k] = src[k];
-          __syncwarp();
-          if (lane == 0) decode_scalar(reinterpret_cast<const u8*>(buf), len, 11, rec, &dec[o]);
-          __syncwarp();
+        if (minor == 11 && len && !(len & 1) && len <= 2 * X11_UNITS) {
+          decode311_warp(A.bytes + off, len, rec, &dec[o], tab[3], S);
           continue;
         }
         if (lane == 0) {

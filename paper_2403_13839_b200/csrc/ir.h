@@ -172,7 +172,7 @@ static constexpr NodeSizeTable NODE_SIZES;
 #endif
 HD inline u32 node_bytes(u8 k) { return NODE_SIZES.v[k]; }
 
-HD inline Node* mk(Dc* C, u8 k) {
+HD ALLOCFN Node* mk(Dc* C, u8 k) {
   Node* n = (Node*)zalloc(C, node_bytes(k));
   n->k = k;
   if (k == E_FUNC || k == E_BUILDCLASS) C->n_defs++;

@@ -9,7 +9,6 @@
 //                          then the text is appended to the flat output buffer.
 #include <cuda_runtime.h>
 #include <stdio.h>
-#define UPY_SMEM_OPTAB 1
 #include "pipeline.h"
 
 // decode_kernel.cu
@@ -107,8 +106,6 @@ __global__ void __launch_bounds__(128, UPY_MINB) upy_decompile_kernel(KParams P)
   __shared__ Dc dcs[128];
   Dc& C = dcs[threadIdx.x];
 #endif
-  for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) upy_s_optab[i >> 8][i & 255] = UPY_OPTABLE_DEV[i >> 8][i & 255];
-  __syncthreads();
   const u64 n_roots = (u64)P.A.n_roots;
   // each thread takes the next root from the global queue
   while (true) {
@@ -241,6 +238,12 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
   }
   if (opt && opt->decode_only) return 0;
   if (arena->n_roots == 0) return 0;
+  static bool carveout_set = false;
+  if (!carveout_set) {
+    // no shared memory: give the whole L1/shared pool to L1 (arena + stack hit rate)
+    cudaFuncSetAttribute(upy_decompile_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+    carveout_set = true;
+  }
   static size_t stack_set = 0;
   size_t want = 48 * 1024;
   if (stack_set != want) {

@@ -71,6 +71,19 @@ def run(arena, style=None, arena_bytes=256 << 20, text_cap=None):
     return out
 
 
+def decode(arena):
+    """decode_scalar on the host for every object: (records, decoded) arrays laid
+    out like the device workspace (records at code_off/2)."""
+    from .arena import INS_DTYPE
+
+    L = lib()
+    A = _abi.arena_struct(arena, arena.blob.ctypes.data)
+    ins = np.zeros(arena.total_code_units + 1, dtype=INS_DTYPE)
+    dec = np.zeros(arena.n_objs, dtype=DECODED_DTYPE)
+    L.upyh_decode(C.byref(A), ins.ctypes.data_as(C.c_void_p), dec.ctypes.data_as(C.c_void_p))
+    return ins, dec
+
+
 def decompile_many(codes, style=None):
     from .arena import pack
     res = run(pack(codes), style)

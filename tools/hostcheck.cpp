@@ -63,3 +63,14 @@ extern "C" int upyh_decompile(const upy_arena* A, int header, const char* indent
   }
   return 0;
 }
+
+// decode_instructions only (the reference-order scalar decoder) for every object:
+// records at ins_out[code_off/2 + i], statuses in dec_out -- the oracle the
+// device decode kernel's records are compared with (tests/test_decode_gpu.py).
+extern "C" int upyh_decode(const upy_arena* A, upy_ins* ins_out, upy_decoded* dec_out) {
+  for (int64_t o = 0; o < A->n_objs; o++) {
+    const upy_obj* ob = &A->objs[o];
+    decode_scalar(A->bytes + ob->code_off, ob->code_len, (int)ob->minor, ins_out + (ob->code_off >> 1), &dec_out[o]);
+  }
+  return 0;
+}
