@@ -412,6 +412,7 @@ def pyc_e2e(pool, reps, local, args, pool_name, n_pool, barrier):
     buf = np.frombuffer(one * reps, dtype=np.uint8)
     n = len(sizes)
     t_load, t_all = [], []
+    parts = {"init": [], "upload_run": [], "fetch": []}
     res = None
     for k in range(1 + args.steps):  # first step is warm-up
         barrier()
@@ -419,19 +420,26 @@ def pyc_e2e(pool, reps, local, args, pool_name, n_pool, barrier):
         arena, per_file = load_pyc_buffer(buf, offs, sizes, pinned=True)
         t1 = time.perf_counter()
         da = DeviceArena(arena, device=f"cuda:{local}")
+        ti = time.perf_counter()
         da.upload()
         da.run()
+        torch.cuda.synchronize()
+        tr = time.perf_counter()
         res = da.fetch()
         barrier()
         t2 = time.perf_counter()
         if k:
             t_load.append(t1 - t0)
             t_all.append(t2 - t0)
+            parts["init"].append(ti - t1)
+            parts["upload_run"].append(tr - ti)
+            parts["fetch"].append(t2 - tr)
         del da, arena
     n_checked, n_bad = verify(res, pool_name, n_pool, 1)
     step = sum(t_all) / len(t_all)
     return {"value": n / step, "unit": "objects/s", "files_per_step": n, "pyc_bytes_per_step": int(len(buf)),
             "load_ms": 1000 * sum(t_load) / len(t_load), "step_ms": 1000 * step,
+            "breakdown_ms": {k: round(1000 * sum(v) / len(v), 2) for k, v in parts.items()},
             "loader_threads": os.cpu_count(), "parity": {"checked": n_checked, "mismatches": n_bad},
             "timing": "wall clock, synchronized, mean of --steps after 1 warm-up"}
 

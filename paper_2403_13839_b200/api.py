@@ -37,11 +37,11 @@ class BatchResult:
     text_off: np.ndarray    # uint64
     text_len: np.ndarray    # uint32
     aux: np.ndarray         # int64 [n_roots, 2]
-    text: bytes             # flat UTF-8 buffer
+    text: np.ndarray        # flat UTF-8 buffer (uint8; a view of page-locked host memory)
 
     def item(self, i):
         s = self.text[int(self.text_off[i]):int(self.text_off[i]) + int(self.text_len[i])]
-        return int(self.status[i]), s.decode("utf-8", "surrogatepass")
+        return int(self.status[i]), bytes(s).decode("utf-8", "surrogatepass")
 
     def values(self):
         out = []
@@ -119,7 +119,14 @@ class DeviceArena:
         aux = meta[64 + 8 * n:64 + 24 * n].view(np.int64).reshape(n, 2).copy()
         ln = meta[64 + 24 * n:64 + 28 * n].view(np.uint32).copy()
         st = meta[64 + 28 * n:64 + 32 * n].view(np.int32).copy()
-        text = self.text[:used].cpu().numpy().tobytes() if used else b""
+        if used:
+            # page-locked destination (torch's caching host allocator reuses it across
+            # calls): a direct DMA instead of a pageable copy plus a bytes() copy
+            host = self.torch.empty(used, dtype=self.torch.uint8, pin_memory=True)
+            host.copy_(self.text[:used])
+            text = host.numpy()
+        else:
+            text = np.zeros(0, dtype=np.uint8)
         return BatchResult(st, off, ln, aux, text)
 
 
@@ -145,7 +152,7 @@ def run_arena(arena: Arena, style=None, device=None, retries=3) -> BatchResult:
         r2 = db.fetch()
         # splice retried results back
         base = len(res.text)
-        res.text = res.text + r2.text
+        res.text = np.concatenate([res.text, r2.text])
         for j, i in enumerate(redo):
             res.status[i] = r2.status[j]
             res.text_off[i] = base + int(r2.text_off[j])

@@ -27,7 +27,7 @@ def parse(path):
         unit = r.get("Metric Unit", "")
         v = float(r["Metric Value"].replace(",", ""))
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-                 "msecond": 1e-3}.get(unit, 1)
+                 "msecond": 1e-3, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(unit, 1)
         per[key][r["Metric Name"]] += v * scale
     out = collections.defaultdict(list)
     for (_, name), m in per.items():
