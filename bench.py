@@ -425,6 +425,7 @@ def pyc_e2e(pool, reps, local, args, pool_name, n_pool, barrier):
         da.run()
         torch.cuda.synchronize()
         tr = time.perf_counter()
+        res = None  # return the previous step's page-locked text buffer to the cache first
         res = da.fetch()
         barrier()
         t2 = time.perf_counter()

@@ -114,7 +114,7 @@ HD NOINL bool load_instructions(Dc* C, Code* K, u32 oi) {
   }
   i32 n = d.n_instrs;
   K->n_ins = n;
-  K->ins = (Ins*)zalloc(C, (u64)n * sizeof(Ins));
+  K->ins = (Ins*)ualloc(C, (u64)n * sizeof(Ins));  // every field is written below
   CKR(C, false);
   const upy_ins* src = C->ins_all + (K->o->code_off >> 1);
   for (i32 i = 0; i < n; i++) {

@@ -164,7 +164,11 @@ struct Dc {
 
 // 16-byte-granular zero / copy for 16-aligned arena blocks (device memset /
 // memcpy on generic pointers compile to byte loops).
+#ifndef UPY_ZERO_HOOK
+#define UPY_ZERO_HOOK(bytes)
+#endif
 HD inline void zero16(void* p, u64 bytes) {
+  UPY_ZERO_HOOK(bytes);
 #ifdef __CUDA_ARCH__
   uint4* q = (uint4*)p;
   const uint4 z = make_uint4(0, 0, 0, 0);
