@@ -98,16 +98,43 @@ def load_pyc(data: bytes):
     return code.version, code
 
 
-def decompile_pyc_many(blobs, style=None, device=None, n_threads=0):
+def decompile_pyc_many(blobs, style=None, device=None, n_threads=0, chunk_files=1 << 18):
     """Decompile a batch of .pyc images on the GPU: one entry per file, the text
-    or the exception the reference's `load_pyc` + `decompile_source` raise."""
+    or the exception the reference's `load_pyc` + `decompile_source` raise.
+
+    Large batches run as a pipeline of sub-batches of `chunk_files` files: the
+    native loader (all host threads) parses sub-batch i+1 while the device
+    decompiles sub-batch i."""
+    blobs = [bytes(b) for b in blobs]
+    out = []
+    for lo, per_file, res in decompile_pyc_chunks(
+            lambda a, b: load_pyc_batch(blobs[a:b], n_threads, pinned=True), len(blobs), style, device,
+            chunk_files):
+        vals = res.values() if res is not None else []
+        for v in per_file:
+            out.append(v if isinstance(v, BaseException) else vals[v])
+    return out
+
+
+def decompile_pyc_chunks(load, n_files, style=None, device=None, chunk_files=1 << 18):
+    """Pipelined driver: `load(lo, hi)` -> (arena, per_file) for files [lo, hi) runs
+    on a worker thread (the native loader releases the GIL and uses every host
+    core) one sub-batch ahead of the device.  Yields (lo, per_file, BatchResult or
+    None) in order."""
+    from concurrent.futures import ThreadPoolExecutor
+
     from .api import run_arena
 
-    arena, per_file = load_pyc_batch(blobs, n_threads, pinned=True)
-    out = list(per_file)
-    if arena.n_roots:
-        vals = run_arena(arena, style, device).values()
-        for i, v in enumerate(per_file):
-            if not isinstance(v, BaseException):
-                out[i] = vals[v]
-    return out
+    chunk_files = max(1, int(chunk_files))
+    bounds = [(lo, min(n_files, lo + chunk_files)) for lo in range(0, n_files, chunk_files)]
+    if not bounds:
+        return
+    with ThreadPoolExecutor(1) as ex:
+        fut = ex.submit(load, *bounds[0])
+        for i, (lo, _hi) in enumerate(bounds):
+            arena, per_file = fut.result()
+            if i + 1 < len(bounds):
+                fut = ex.submit(load, *bounds[i + 1])
+            res = run_arena(arena, style, device) if arena.n_roots else None
+            del arena
+            yield lo, per_file, res

@@ -106,10 +106,15 @@ dist.destroy_process_group()
 
 
 def test_gloo_world_size_2(tmp_path):
+    import socket
+
     script = tmp_path / "w.py"
     script.write_text(GLOO_WORKER)
+    with socket.socket() as sk:  # a free port (a fixed one can still be in TIME_WAIT from a previous run)
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr", "127.0.0.1", "--master-port", "29533", str(script), ROOT]
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(script), ROOT]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
     assert out.stdout.count("ok ") == 2
