@@ -100,7 +100,8 @@ mx = shard.max_over_ranks([float(r + 1), float(hi - lo)])
 tot = shard.sum_over_ranks([hi - lo])
 assert mx[0] == w, mx
 assert tot[0] == 100, tot
-print("ok", r, lo, hi, mx, tot)
+with open(os.path.join(sys.argv[2], f"ok_{r}"), "w") as f:  # files, not interleaved stdout
+    f.write(f"{lo} {hi} {mx} {tot}")
 dist.destroy_process_group()
 """
 
@@ -114,7 +115,7 @@ def test_gloo_world_size_2(tmp_path):
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr", "127.0.0.1", "--master-port", str(port), str(script), ROOT]
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(script), ROOT, str(tmp_path)]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
-    assert out.stdout.count("ok ") == 2
+    assert sorted(p.name for p in tmp_path.glob("ok_*")) == ["ok_0", "ok_1"]
