@@ -434,7 +434,9 @@ def pyc_e2e(pool, reps, local, args, pool_name, n_pool, barrier):
     offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.uint64)
     buf = np.frombuffer(one * reps, dtype=np.uint8)
     n = len(sizes)
-    chunk = max(1, n // 4)  # 4 sub-batches: host parsing of one overlaps the device work of the previous
+    # up to 4 sub-batches of >= 65,536 files: host parsing of one overlaps the device work
+    # of the previous (small batches stay one batch: per-batch fixed costs dominate there)
+    chunk = max(65536, (n + 3) // 4)
 
     def load(lo, hi):
         return load_pyc_buffer(buf, offs[lo:hi], sizes[lo:hi], pinned=True)

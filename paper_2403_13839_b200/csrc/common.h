@@ -338,7 +338,14 @@ HD SLOWPATH bool t_grow_slow(Dc* C, Text* t, u32 need) {
   t->cap = nc;
   return true;
 }
-HD inline void t_putn(Dc* C, Text* t, const char* p, u32 n) {
+// Inlined: out of line these were 12% less SASS but 1.7% slower on C3 (same-session
+// A/B, 255.5 vs 251.3 ms) -- they sit on the emitter's hot path.
+#ifdef UPY_TEXT_OOL
+#define TEXTFN SLOWPATH
+#else
+#define TEXTFN inline
+#endif
+HD TEXTFN void t_putn(Dc* C, Text* t, const char* p, u32 n) {
   if (!n) return;
   if (!t_grow(C, t, t->n + n)) return;
   char* d = t->d + t->n;
@@ -350,7 +357,7 @@ HD inline void t_put(Dc* C, Text* t, char ch) {
   if (t->n >= t->cap && !t_grow(C, t, t->n + 1)) return;
   t->d[t->n++] = ch;
 }
-HD inline void t_puts(Dc* C, Text* t, const char* s) { t_putn(C, t, s, (u32)cstrlen(s)); }
+HD TEXTFN void t_puts(Dc* C, Text* t, const char* s) { t_putn(C, t, s, (u32)cstrlen(s)); }
 HD inline void t_str(Dc* C, Text* t, Str s) { t_putn(C, t, s.p, s.n); }
 HD inline void t_u32(Dc* C, Text* t, u32 v) {
   char buf[10];
@@ -401,7 +408,7 @@ HD SLOWPATH void m_putn(Dc* C, Text* t, const char* p, u32 n) {
 #pragma unroll 1
   for (u32 i = 0; i < n && t->n < t->cap; i++) t->d[t->n++] = p[i];
 }
-HD inline void m_puts(Dc* C, Text* t, const char* s) { m_putn(C, t, s, (u32)cstrlen(s)); }
+HD SLOWPATH void m_puts(Dc* C, Text* t, const char* s) { m_putn(C, t, s, (u32)cstrlen(s)); }
 HD inline void m_str(Dc* C, Text* t, Str s) { m_putn(C, t, s.p, s.n); }
 HD SLOWPATH void m_i64(Dc* C, Text* t, i64 v) {
   char buf[24];

@@ -425,7 +425,7 @@ struct Sim {
     }
   }
 
-  HD void binop(NV* st, const Ins* ins, u8 op, bool inplace) {
+  HD FORCEINL void binop(NV* st, const Ins* ins, u8 op, bool inplace) {
     Node* r = pop_value(st, ins);
     CK(C);
     Node* l = pop_value(st, ins);
@@ -615,32 +615,80 @@ HD FORCEINL int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out) {
       return 0;
     }
     // ------------------------------------------------ arithmetic (:455-484, 927-944)
-    case OP_BINARY_ADD: binop(st, ins, BO_ADD, false); return 0;
-    case OP_BINARY_SUBTRACT: binop(st, ins, BO_SUB, false); return 0;
-    case OP_BINARY_MULTIPLY: binop(st, ins, BO_MUL, false); return 0;
-    case OP_BINARY_TRUE_DIVIDE: binop(st, ins, BO_TRUEDIV, false); return 0;
-    case OP_BINARY_FLOOR_DIVIDE: binop(st, ins, BO_FLOORDIV, false); return 0;
-    case OP_BINARY_MODULO: binop(st, ins, BO_MOD, false); return 0;
-    case OP_BINARY_POWER: binop(st, ins, BO_POW, false); return 0;
-    case OP_BINARY_LSHIFT: binop(st, ins, BO_LSHIFT, false); return 0;
-    case OP_BINARY_RSHIFT: binop(st, ins, BO_RSHIFT, false); return 0;
-    case OP_BINARY_AND: binop(st, ins, BO_AND, false); return 0;
-    case OP_BINARY_OR: binop(st, ins, BO_OR, false); return 0;
-    case OP_BINARY_XOR: binop(st, ins, BO_XOR, false); return 0;
-    case OP_BINARY_MATRIX_MULTIPLY: binop(st, ins, BO_MATMUL, false); return 0;
-    case OP_INPLACE_ADD: binop(st, ins, BO_ADD, true); return 0;
-    case OP_INPLACE_SUBTRACT: binop(st, ins, BO_SUB, true); return 0;
-    case OP_INPLACE_MULTIPLY: binop(st, ins, BO_MUL, true); return 0;
-    case OP_INPLACE_TRUE_DIVIDE: binop(st, ins, BO_TRUEDIV, true); return 0;
-    case OP_INPLACE_FLOOR_DIVIDE: binop(st, ins, BO_FLOORDIV, true); return 0;
-    case OP_INPLACE_MODULO: binop(st, ins, BO_MOD, true); return 0;
-    case OP_INPLACE_POWER: binop(st, ins, BO_POW, true); return 0;
-    case OP_INPLACE_LSHIFT: binop(st, ins, BO_LSHIFT, true); return 0;
-    case OP_INPLACE_RSHIFT: binop(st, ins, BO_RSHIFT, true); return 0;
-    case OP_INPLACE_AND: binop(st, ins, BO_AND, true); return 0;
-    case OP_INPLACE_OR: binop(st, ins, BO_OR, true); return 0;
-    case OP_INPLACE_XOR: binop(st, ins, BO_XOR, true); return 0;
-    case OP_INPLACE_MATRIX_MULTIPLY: binop(st, ins, BO_MATMUL, true); return 0;
+    // the 26 binary / in-place operator cases share one inlined binop
+    case OP_BINARY_ADD:
+    case OP_BINARY_SUBTRACT:
+    case OP_BINARY_MULTIPLY:
+    case OP_BINARY_TRUE_DIVIDE:
+    case OP_BINARY_FLOOR_DIVIDE:
+    case OP_BINARY_MODULO:
+    case OP_BINARY_POWER:
+    case OP_BINARY_LSHIFT:
+    case OP_BINARY_RSHIFT:
+    case OP_BINARY_AND:
+    case OP_BINARY_OR:
+    case OP_BINARY_XOR:
+    case OP_BINARY_MATRIX_MULTIPLY:
+    case OP_INPLACE_ADD:
+    case OP_INPLACE_SUBTRACT:
+    case OP_INPLACE_MULTIPLY:
+    case OP_INPLACE_TRUE_DIVIDE:
+    case OP_INPLACE_FLOOR_DIVIDE:
+    case OP_INPLACE_MODULO:
+    case OP_INPLACE_POWER:
+    case OP_INPLACE_LSHIFT:
+    case OP_INPLACE_RSHIFT:
+    case OP_INPLACE_AND:
+    case OP_INPLACE_OR:
+    case OP_INPLACE_XOR:
+    case OP_INPLACE_MATRIX_MULTIPLY:
+    {
+      u8 bo = BO_ADD;
+      switch (in.op) {
+        case OP_BINARY_ADD: bo = BO_ADD; break;
+        case OP_BINARY_SUBTRACT: bo = BO_SUB; break;
+        case OP_BINARY_MULTIPLY: bo = BO_MUL; break;
+        case OP_BINARY_TRUE_DIVIDE: bo = BO_TRUEDIV; break;
+        case OP_BINARY_FLOOR_DIVIDE: bo = BO_FLOORDIV; break;
+        case OP_BINARY_MODULO: bo = BO_MOD; break;
+        case OP_BINARY_POWER: bo = BO_POW; break;
+        case OP_BINARY_LSHIFT: bo = BO_LSHIFT; break;
+        case OP_BINARY_RSHIFT: bo = BO_RSHIFT; break;
+        case OP_BINARY_AND: bo = BO_AND; break;
+        case OP_BINARY_OR: bo = BO_OR; break;
+        case OP_BINARY_XOR: bo = BO_XOR; break;
+        case OP_BINARY_MATRIX_MULTIPLY: bo = BO_MATMUL; break;
+        case OP_INPLACE_ADD: bo = BO_ADD; break;
+        case OP_INPLACE_SUBTRACT: bo = BO_SUB; break;
+        case OP_INPLACE_MULTIPLY: bo = BO_MUL; break;
+        case OP_INPLACE_TRUE_DIVIDE: bo = BO_TRUEDIV; break;
+        case OP_INPLACE_FLOOR_DIVIDE: bo = BO_FLOORDIV; break;
+        case OP_INPLACE_MODULO: bo = BO_MOD; break;
+        case OP_INPLACE_POWER: bo = BO_POW; break;
+        case OP_INPLACE_LSHIFT: bo = BO_LSHIFT; break;
+        case OP_INPLACE_RSHIFT: bo = BO_RSHIFT; break;
+        case OP_INPLACE_AND: bo = BO_AND; break;
+        case OP_INPLACE_OR: bo = BO_OR; break;
+        case OP_INPLACE_XOR: bo = BO_XOR; break;
+        case OP_INPLACE_MATRIX_MULTIPLY: bo = BO_MATMUL; break;
+        default: break;
+      }
+      const bool inplace = in.op == OP_INPLACE_ADD ||
+                           in.op == OP_INPLACE_SUBTRACT ||
+                           in.op == OP_INPLACE_MULTIPLY ||
+                           in.op == OP_INPLACE_TRUE_DIVIDE ||
+                           in.op == OP_INPLACE_FLOOR_DIVIDE ||
+                           in.op == OP_INPLACE_MODULO ||
+                           in.op == OP_INPLACE_POWER ||
+                           in.op == OP_INPLACE_LSHIFT ||
+                           in.op == OP_INPLACE_RSHIFT ||
+                           in.op == OP_INPLACE_AND ||
+                           in.op == OP_INPLACE_OR ||
+                           in.op == OP_INPLACE_XOR ||
+                           in.op == OP_INPLACE_MATRIX_MULTIPLY;
+      binop(st, ins, bo, inplace);
+      return 0;
+    }
     case OP_BINARY_OP: {
       u64 arg = (in.flags & 2) ? 0xFFFFFFFFull : in.arg;
       bool inplace = arg >= 13;
@@ -1386,9 +1434,14 @@ HD NOINL BlockResult Sim::simulate(const Block* b, const NV* entry) {
   NV* out = vnew<Node*>(C);
   R.stmts = out;
   i32 i = b->lo;
-  while (i < b->hi) {
+  // loop invariants held in registers (the compiler must assume the arena stores of
+  // every step may alias *K / *b and would reload them per instruction)
+  const i32 hi_ = b->hi;
+  const Ins* const ins_base = K->ins;
+  const i64 depth_limit = K->o->stacksize + 6;
+  while (i < hi_) {
     CKR(C, R);
-    const Ins* ins = &K->ins[i];
+    const Ins* ins = &ins_base[i];
     u8 op = ins->op;
     if (is_async_op(op)) {
       fail_unsupported(C, opname_of(op), ins->offset);
@@ -1488,10 +1541,10 @@ HD NOINL BlockResult Sim::simulate(const Block* b, const NV* entry) {
       R.term = i;
       return R;
     }
-    int consumed = step(ins, i, b->hi, st, out);
+    int consumed = step(ins, i, hi_, st, out);
     CKR(C, R);
     i += 1 + consumed;
-    if ((i64)st->n > K->o->stacksize + 6) {
+    if ((i64)st->n > depth_limit) {
       fail_depth(C, b->id, st->n, 0, false);
       return R;
     }

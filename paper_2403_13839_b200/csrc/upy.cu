@@ -35,6 +35,7 @@ struct KParams {
   int indent_len, tool_len;
   char indent[64];
   char tool[64];
+  int lane_stride;  // 1: every thread takes roots; 32: one root-taking thread per warp
 };
 
 #ifndef UPY_MINB
@@ -90,7 +91,12 @@ __device__ __forceinline__ void emit_result(const KParams& P, Dc& C, u32 r, cons
 }
 
 __global__ void __launch_bounds__(128, UPY_MINB) upy_decompile_kernel(KParams P) {
-  const u64 slot = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  // Small batches (fewer roots than resident warps) run one root-taking thread per
+  // warp: a lone thread issues without divergence serialisation, and the roots
+  // spread over all SMs instead of packing into a few blocks -- latency, not
+  // throughput, is what a small batch measures.
+  if (P.lane_stride > 1 && (threadIdx.x & 31)) return;
+  const u64 slot = ((u64)blockIdx.x * blockDim.x + threadIdx.x) / (u64)P.lane_stride;
   u8* base = P.slots_base + slot * P.slot_bytes;
   EmitOpts opt;
   opt.header = P.header != 0;
@@ -122,6 +128,7 @@ __global__ void __launch_bounds__(128, UPY_MINB) upy_decompile_kernel(KParams P)
 struct WsLayout {
   u64 ins_off, dec_off, ctr_off, slots_off, total;
   u64 slots, slot_bytes;
+  int lane_stride;
 };
 static u64 al(u64 x) { return (x + 255) & ~(u64)255; }
 
@@ -168,7 +175,14 @@ static WsLayout layout(const upy_arena* a, const upy_options* o) {
   if (slots > (u64)a->n_roots) slots = (u64)a->n_roots;
   if (slots < 1) slots = 1;
   int tpb = eff_tpb(o);
-  slots = (slots + tpb - 1) / tpb * tpb;
+  L.lane_stride = 1;
+  if (!(o && o->slots > 0) && (u64)a->n_roots <= (u64)sm_count() * (4 * UPY_MINB)) {
+    L.lane_stride = 32;  // one root-taking thread per warp (see the kernel)
+    const u64 wpb = (u64)tpb / 32;
+    slots = (slots + wpb - 1) / wpb * wpb;
+  } else {
+    slots = (slots + tpb - 1) / tpb * tpb;
+  }
   L.slots = slots;
   L.total = L.slots_off + slots * sb;
   if (o && o->decode_only) L.total = L.slots_off;
@@ -277,8 +291,9 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
     P.tool_len = 6;
     memcpy(P.tool, "unpyre", 6);
   }
+  P.lane_stride = L.lane_stride;
   int tpb = eff_tpb(opt);
-  unsigned blocks = (unsigned)(L.slots / tpb);
+  unsigned blocks = (unsigned)(L.slots * L.lane_stride / tpb);
   upy_decompile_kernel<<<blocks, tpb, 0, s>>>(P);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
