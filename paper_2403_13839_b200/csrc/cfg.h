@@ -117,10 +117,12 @@ HD NOINL bool load_instructions(Dc* C, Code* K, u32 oi) {
   K->ins = (Ins*)ualloc(C, (u64)n * sizeof(Ins));  // every field is written below
   CKR(C, false);
   const upy_ins* src = C->ins_all + (K->o->code_off >> 1);
+  Ins* const dst = K->ins;      // loop invariants in registers (the stores below
+  const int minor = K->minor;   // could alias *K as far as the compiler knows)
   for (i32 i = 0; i < n; i++) {
     const upy_ins& r = src[i];
-    u32 e = optab_div(K->minor, r.opcode);
-    Ins& x = K->ins[i];
+    u32 e = optab_div(minor, r.opcode);
+    Ins& x = dst[i];
     x.offset = r.offset;
     x.arg = r.arg;
     x.op = UPY_ENT_OP(e);
@@ -249,8 +251,9 @@ HD inline bool is_as_cleanup(const Code* K, i32 idx) {  // structurer.py:154-160
 HD NOINL Vec<TryRegion>* match_try_regions(Dc* C, const Code* K, const Vec<ExcEntry>* exc) {
   Vec<TryRegion>* out = vnew<TryRegion>(C);
   const Ins* I = K->ins;
+  const i32 n_ins = K->n_ins;
   if (K->minor <= 10) {  // _regions_legacy (structurer.py:69-88)
-    for (i32 i = 0; i < K->n_ins; i++) {
+    for (i32 i = 0; i < n_ins; i++) {
       if (I[i].op != OP_SETUP_FINALLY && I[i].op != OP_SETUP_WITH) continue;
       TryRegion r;
       r.start = ins_end(I[i]);

@@ -34,14 +34,26 @@ struct Code {
   Vec<Str>* kwnames;
 };
 
-HD FORCEINL Str argval_name(Dc* C, const Code* K, const Ins& in) {
+// The read-only part of Code the per-instruction transfer functions use, passed by
+// value into the force-inlined step: the fields live in registers for the whole
+// block instead of being reloaded through K after every arena store (which the
+// compiler must assume may alias *K).
+struct StepCtx {
+  u32 oi;
+  int minor;
+  const upy_obj* o;
+};
+
+template <class KK>
+HD FORCEINL Str argval_name(Dc* C, const KK* K, const Ins& in) {
   // kind == name (disasm.py:134-138)
   u64 idx = in.arg;
   if (K->minor >= 11 && in.op == OP_LOAD_GLOBAL) idx = in.arg >> 1;
   if ((in.flags & 2) || idx >= K->o->n_names) return Snone();
   return obj_tab(C, K->o->names_off, (u32)idx);
 }
-HD FORCEINL Str argval_local(Dc* C, const Code* K, const Ins& in) {
+template <class KK>
+HD FORCEINL Str argval_local(Dc* C, const KK* K, const Ins& in) {
   if (in.flags & 2) return Snone();
   if (K->minor <= 10) {
     if (in.arg >= K->o->n_varnames) return Snone();
@@ -51,17 +63,20 @@ HD FORCEINL Str argval_local(Dc* C, const Code* K, const Ins& in) {
   Str s = obj_localsplus(C, K->oi, in.arg, &ok);
   return ok ? s : Snone();
 }
-HD FORCEINL Str argval_free(Dc* C, const Code* K, const Ins& in) {
+template <class KK>
+HD FORCEINL Str argval_free(Dc* C, const KK* K, const Ins& in) {
   if (in.flags & 2) return Snone();
   bool ok;
   Str s = obj_deref_name(C, K->oi, in.arg, &ok);
   return ok ? s : Snone();
 }
-HD FORCEINL u32 argval_const(Dc* C, const Code* K, const Ins& in) {
+template <class KK>
+HD FORCEINL u32 argval_const(Dc* C, const KK* K, const Ins& in) {
   if ((in.flags & 2) || in.arg >= K->o->n_consts) return CID_INVALID;
   return obj_const_id(C, K->oi, in.arg);
 }
-HD inline u8 argval_cmp(Dc* C, const Code* K, const Ins& in) {
+template <class KK>
+HD inline u8 argval_cmp(Dc* C, const KK* K, const Ins& in) {
   if ((in.flags & 2) || (int)in.arg >= T_NCMP[K->minor - 8]) return CO_NONE;
   return (u8)in.arg;
 }
@@ -256,11 +271,12 @@ struct Sim {
       default: return SC_DEREF;
     }
   }
-  HD Str store_name(const Ins& in) {
+  template <class KK>
+  HD FORCEINL Str store_name(const Ins& in, const KK* KX) {
     switch (in.op) {
-      case OP_STORE_FAST: return argval_local(C, K, in);
-      case OP_STORE_DEREF: return argval_free(C, K, in);
-      default: return argval_name(C, K, in);
+      case OP_STORE_FAST: return argval_local(C, KX, in);
+      case OP_STORE_DEREF: return argval_free(C, KX, in);
+      default: return argval_name(C, KX, in);
     }
   }
 
@@ -378,7 +394,7 @@ struct Sim {
       int k = 0;
       while (idx + 1 + k < hi && is_scalar_store(K->ins[idx + 1 + k].op) && st->n && !blocks_batch(vlast(st))) {
         const Ins* nxt = &K->ins[idx + 1 + k];
-        Node* t2 = mk_name(C, store_name(*nxt), store_scope(nxt->op));
+        Node* t2 = mk_name(C, store_name(*nxt, K), store_scope(nxt->op));
         Node* u = pop(st, nxt);
         CKR(C, 0);
         vpush(C, bt, t2);
@@ -521,7 +537,7 @@ struct Sim {
   }
 
   // dispatch of one non-terminator instruction; returns consumed following instrs
-  HD int step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out);
+  HD int step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out, const StepCtx& X);
 
   HD BlockResult simulate(const Block* b, const NV* entry);
 };
@@ -530,20 +546,20 @@ struct Sim {
 
 // Inlined into simulate() (its only caller): as a call, its register save/restore
 // was ~30% of the kernel's local-memory traffic (ncu source page, round 1).
-HD FORCEINL int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out) {
+HD FORCEINL int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out, const StepCtx& X) {
   const Ins& in = *ins;
   switch (in.op) {
     // ------------------------------------------------ loads (symexec.py:239-268)
-    case OP_LOAD_CONST: BR_PUSH(mk_const(C, argval_const(C, K, in))); return 0;
-    case OP_LOAD_FAST: BR_PUSH(mk_name(C, argval_local(C, K, in), SC_FAST)); return 0;
+    case OP_LOAD_CONST: BR_PUSH(mk_const(C, argval_const(C, &X, in))); return 0;
+    case OP_LOAD_FAST: BR_PUSH(mk_name(C, argval_local(C, &X, in), SC_FAST)); return 0;
     case OP_LOAD_GLOBAL:
-      if (K->minor >= 11 && (in.arg & 1)) BR_PUSH(mk(C, E_NULL));
-      BR_PUSH(mk_name(C, argval_name(C, K, in), SC_GLOBAL));
+      if (X.minor >= 11 && (in.arg & 1)) BR_PUSH(mk(C, E_NULL));
+      BR_PUSH(mk_name(C, argval_name(C, &X, in), SC_GLOBAL));
       return 0;
-    case OP_LOAD_NAME: BR_PUSH(mk_name(C, argval_name(C, K, in), SC_NAME)); return 0;
+    case OP_LOAD_NAME: BR_PUSH(mk_name(C, argval_name(C, &X, in), SC_NAME)); return 0;
     case OP_LOAD_DEREF:
-    case OP_LOAD_CLASSDEREF: BR_PUSH(mk_name(C, argval_free(C, K, in), SC_DEREF)); return 0;
-    case OP_LOAD_CLOSURE: BR_PUSH(mk_name(C, argval_free(C, K, in), SC_CELL)); return 0;
+    case OP_LOAD_CLASSDEREF: BR_PUSH(mk_name(C, argval_free(C, &X, in), SC_DEREF)); return 0;
+    case OP_LOAD_CLOSURE: BR_PUSH(mk_name(C, argval_free(C, &X, in), SC_CELL)); return 0;
     case OP_LOAD_ASSERTION_ERROR: BR_PUSH(mk_name(C, S("AssertionError"), SC_GLOBAL)); return 0;
     case OP_LOAD_BUILD_CLASS: BR_PUSH(mk(C, E_BUILDCLASS)); return 0;
     case OP_PUSH_NULL: BR_PUSH(mk(C, E_NULL)); return 0;
@@ -552,12 +568,12 @@ HD FORCEINL int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out) {
     case OP_STORE_NAME:
     case OP_STORE_GLOBAL:
     case OP_STORE_DEREF:
-      return store(ins, st, out, idx, hi, mk_name(C, store_name(in), store_scope(in.op)));
+      return store(ins, st, out, idx, hi, mk_name(C, store_name(in, &X), store_scope(in.op)));
     case OP_STORE_ATTR: {
       Node* obj = pop(st, ins);
       CKR(C, 0);
       Node* t = mk1(C, E_ATTR, obj);
-      t->s = argval_name(C, K, in);
+      t->s = argval_name(C, &X, in);
       return store(ins, st, out, idx, hi, t);
     }
     case OP_STORE_SUBSCR: {
@@ -585,8 +601,8 @@ HD FORCEINL int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out) {
     case OP_DELETE_NAME:
     case OP_DELETE_GLOBAL:
     case OP_DELETE_DEREF: {
-      Str nm = in.op == OP_DELETE_FAST ? argval_local(C, K, in)
-               : in.op == OP_DELETE_DEREF ? argval_free(C, K, in) : argval_name(C, K, in);
+      Str nm = in.op == OP_DELETE_FAST ? argval_local(C, &X, in)
+               : in.op == OP_DELETE_DEREF ? argval_free(C, &X, in) : argval_name(C, &X, in);
       u8 sc = in.op == OP_DELETE_FAST ? SC_FAST : in.op == OP_DELETE_NAME ? SC_NAME
               : in.op == OP_DELETE_GLOBAL ? SC_GLOBAL : SC_DEREF;
       Node* d = mk(C, S_DELETE);
@@ -598,7 +614,7 @@ HD FORCEINL int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out) {
       Node* o = pop(st, ins);
       CKR(C, 0);
       Node* t = mk1(C, E_ATTR, o);
-      t->s = argval_name(C, K, in);
+      t->s = argval_name(C, &X, in);
       Node* d = mk(C, S_DELETE);
       d->l1 = nv1(C, t);
       vpush(C, out, d);
@@ -715,7 +731,7 @@ HD FORCEINL int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out) {
       CKR(C, 0);
       Node* l = pop_value(st, ins);
       CKR(C, 0);
-      u8 cmp = in.op == OP_COMPARE_OP ? argval_cmp(C, K, in)
+      u8 cmp = in.op == OP_COMPARE_OP ? argval_cmp(C, &X, in)
                : in.op == OP_IS_OP ? (in.arg ? CO_ISNOT : CO_IS) : (in.arg ? CO_NOTIN : CO_IN);
       BR_PUSH(mk_compare(C, l, cmp, r));
       return 0;
@@ -1054,7 +1070,7 @@ HD FORCEINL int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out) {
       Node* v = pop_value(st, ins);
       CKR(C, 0);
       Node* t = mk1(C, E_ATTR, v);
-      t->s = argval_name(C, K, in);
+      t->s = argval_name(C, &X, in);
       BR_PUSH(t);
       return 0;
     }
@@ -1062,14 +1078,14 @@ HD FORCEINL int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out) {
       Node* v = pop_value(st, ins);
       CKR(C, 0);
       Node* t = mk1(C, E_ATTR, v);
-      t->s = argval_name(C, K, in);
+      t->s = argval_name(C, &X, in);
       BR_PUSH(t);
       BR_PUSH(mk(C, E_METHSELF));
       return 0;
     }
     // ------------------------------------------------ calls (:722-785)
     case OP_KW_NAMES: {
-      Vec<Str>* kw = const_str_tuple(argval_const(C, K, in));
+      Vec<Str>* kw = const_str_tuple(argval_const(C, &X, in));
       CKR(C, 0);
       K->kwnames = kw;
       K->has_kwnames = true;
@@ -1128,7 +1144,7 @@ HD FORCEINL int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out) {
       CKR(C, 0);
       Node* func = pop(st, ins);
       CKR(C, 0);
-      if (K->minor >= 11 && st->n && is_k(vlast(st), E_NULL)) st->n--;
+      if (X.minor >= 11 && st->n && is_k(vlast(st), E_NULL)) st->n--;
       NV* args = spread(C, posargs, false);
       CKR(C, 0);
       NV* kws = vnew<Node*>(C);
@@ -1164,7 +1180,7 @@ HD FORCEINL int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out) {
     // ------------------------------------------------ functions (:789-822)
     case OP_MAKE_FUNCTION: {
       u32 flags = in.arg;
-      if (K->minor <= 10) {
+      if (X.minor <= 10) {
         pop(st, ins);
         CKR(C, 0);
       }
@@ -1249,7 +1265,7 @@ HD FORCEINL int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out) {
       Node* level = pop(st, ins);
       CKR(C, 0);
       Node* n = mk(C, E_IMPORT);
-      n->s = argval_name(C, K, in);
+      n->s = argval_name(C, &X, in);
       u32 fc = const_of(fromlist);
       CKR(C, 0);
       if (fc == CID_INVALID) { py_error(C, UPY_ST_PY_ATTRIBUTE_ERROR, "'NoneType' object has no attribute 'kind'"); return 0; }
@@ -1269,7 +1285,7 @@ HD FORCEINL int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out) {
       Node* top = py_index(C, st, -1);
       CKR(C, 0);
       Node* n = mk1(C, E_IMPORTFROM, top);
-      n->s = argval_name(C, K, in);
+      n->s = argval_name(C, &X, in);
       BR_PUSH(n);
       return 0;
     }
@@ -1314,7 +1330,7 @@ HD FORCEINL int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out) {
       return 0;
     }
     case OP_POP_EXCEPT: {
-      int n = K->minor >= 11 ? 1 : 3;
+      int n = X.minor >= 11 ? 1 : 3;
       for (int q = 0; q < n; q++)
         if (st->n) st->n--;
       return 0;
@@ -1439,6 +1455,7 @@ HD NOINL BlockResult Sim::simulate(const Block* b, const NV* entry) {
   const i32 hi_ = b->hi;
   const Ins* const ins_base = K->ins;
   const i64 depth_limit = K->o->stacksize + 6;
+  const StepCtx X = {K->oi, K->minor, K->o};
   while (i < hi_) {
     CKR(C, R);
     const Ins* ins = &ins_base[i];
@@ -1541,7 +1558,7 @@ HD NOINL BlockResult Sim::simulate(const Block* b, const NV* entry) {
       R.term = i;
       return R;
     }
-    int consumed = step(ins, i, hi_, st, out);
+    int consumed = step(ins, i, hi_, st, out, X);
     CKR(C, R);
     i += 1 + consumed;
     if ((i64)st->n > depth_limit) {
