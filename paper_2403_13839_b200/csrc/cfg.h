@@ -98,7 +98,7 @@ HD NOINL bool load_instructions(Dc* C, Code* K, u32 oi) {
           else if (d.aux0 == 3) { m_puts(C, &t, "code ends inside EXTENDED_ARG run at "); m_i64(C, &t, d.aux1); }
           else if (d.aux0 == 4) {
             const upy_obj* o = K->o;
-            u32 opb = C->A->bytes[o->code_off + (d.aux1 - 2)];
+            u32 opb = C->bytes[o->code_off + (d.aux1 - 2)];
             m_puts(C, &t, "code ends inside inline cache of ");
             m_puts(C, &t, opname_of(UPY_ENT_OP(optab(K->minor, opb))));
             m_puts(C, &t, " at "); m_i64(C, &t, d.aux1);
@@ -177,7 +177,7 @@ HD NOINL void rewrite_yield_from(Dc* C, Code* K) {
 // decode_exception_table (disasm.py:175-214)
 HD NOINL Vec<ExcEntry>* decode_exception_table(Dc* C, const Code* K) {
   Vec<ExcEntry>* v = vnew<ExcEntry>(C);
-  const u8* data = C->A->bytes + K->o->exc_off;
+  const u8* data = C->bytes + K->o->exc_off;
   u32 len = K->o->exc_len, pos = 0;
   auto bad = [&](const char* what, u32 at) {
     Text t;

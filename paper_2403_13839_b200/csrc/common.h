@@ -150,6 +150,14 @@ struct Dc {
   u32 msg_len, msg_cap;
   // inputs
   const upy_arena* A;
+  // the arena's section bases copied out of *A: one dependent load less on every
+  // string / const / ref lookup (A points at the kernel-parameter copy)
+  const upy_obj* objs;
+  const upy_const* consts;
+  const upy_str* strs;
+  const uint32_t* refs;
+  const uint32_t* limbs;
+  const uint8_t* bytes;
   const upy_ins* ins_all;
   const upy_decoded* dec_all;
   // recursion guard

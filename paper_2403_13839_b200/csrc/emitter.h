@@ -125,7 +125,7 @@ struct Emitter {
       case UPY_C_ELLIPSIS: t_puts(C, t, "..."); return;
       case UPY_C_INT: {
         const upy_const* c = cget(C, cid);
-        t_int_repr(C, t, c->ival, C->A->limbs + c->off, c->n);
+        t_int_repr(C, t, c->ival, C->limbs + c->off, c->n);
         return;
       }
       case UPY_C_FLOAT: render_float(t, cget(C, cid)->re); return;
@@ -158,7 +158,7 @@ struct Emitter {
       case UPY_C_STR: t_str_repr(C, t, cstr(C, cid)); return;
       case UPY_C_BYTES: {
         const upy_const* c = cget(C, cid);
-        t_bytes_repr(C, t, C->A->bytes + c->off, c->n);
+        t_bytes_repr(C, t, C->bytes + c->off, c->n);
         return;
       }
       case UPY_C_TUPLE: {
@@ -261,7 +261,7 @@ struct Emitter {
       if (e->k == E_CONST && e->cid < CID_NONE_SYN) {
         const upy_const* c = cget(C, e->cid);
         if (c->kind == UPY_C_INT && c->n == 1 && c->ival >= 0) {
-          t_u32(C, t, C->A->limbs[c->off]);
+          t_u32(C, t, C->limbs[c->off]);
           return false;
         }
         if (c->kind == UPY_C_NONE) {
@@ -298,13 +298,13 @@ HD inline void Emitter::r_const_value(Text* t, u32 cid) {
     case UPY_C_BOOL: t_puts(C, t, cbool(C, cid) ? "True" : "False"); return;
     case UPY_C_INT: {
       const upy_const* c = cget(C, cid);
-      t_int_repr(C, t, c->ival, C->A->limbs + c->off, c->n);
+      t_int_repr(C, t, c->ival, C->limbs + c->off, c->n);
       return;
     }
     case UPY_C_FLOAT: t_float_repr(C, t, cget(C, cid)->re); return;
     case UPY_C_COMPLEX: t_complex_repr(C, t, cget(C, cid)->re, cget(C, cid)->im); return;
     case UPY_C_STR: t_str_repr(C, t, cstr(C, cid)); return;
-    case UPY_C_BYTES: t_bytes_repr(C, t, C->A->bytes + cget(C, cid)->off, cget(C, cid)->n); return;
+    case UPY_C_BYTES: t_bytes_repr(C, t, C->bytes + cget(C, cid)->off, cget(C, cid)->n); return;
     case UPY_C_TUPLE:
     case UPY_C_FROZENSET: {
       u32 n = cnelem(C, cid);
@@ -1189,7 +1189,7 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
       u32 lk = s->cid == CID_INVALID ? UPY_C_NONE : ckind(C, s->cid);
       if (lk == UPY_C_INT) {
         const upy_const* c = cget(C, s->cid);
-        level = c->n ? (i64)C->A->limbs[c->off] * c->ival : 0;
+        level = c->n ? (i64)C->limbs[c->off] * c->ival : 0;
       } else if (lk == UPY_C_BOOL) {
         level = cbool(C, s->cid);
       } else {

@@ -14,12 +14,12 @@ struct Obj {
   u32 idx;
 };
 
-HD inline const upy_obj* obj_at(const Dc* C, u32 i) { return &C->A->objs[i]; }
+HD inline const upy_obj* obj_at(const Dc* C, u32 i) { return &C->objs[i]; }
 HD inline Str str_at(const Dc* C, u32 sid) {
-  const upy_str& s = C->A->strs[sid];
-  return Str{(const char*)(C->A->bytes + s.off), s.len};
+  const upy_str& s = C->strs[sid];
+  return Str{(const char*)(C->bytes + s.off), s.len};
 }
-HD inline u32 ref_at(const Dc* C, u64 i) { return C->A->refs[i]; }
+HD inline u32 ref_at(const Dc* C, u64 i) { return C->refs[i]; }
 HD inline Str obj_name(const Dc* C, u32 oi) { return str_at(C, obj_at(C, oi)->name); }
 HD inline Str obj_qualname(const Dc* C, u32 oi) { return str_at(C, obj_at(C, oi)->qualname); }
 HD inline Str obj_varname(const Dc* C, u32 oi, u32 k) {
@@ -35,12 +35,12 @@ HD inline u32 obj_const_id(const Dc* C, u32 oi, u32 k) {
 HD inline u32 ckind(const Dc* C, u32 cid) {
   if (cid == CID_NONE_SYN) return UPY_C_NONE;
   if (cid == CID_TRUE_SYN) return UPY_C_BOOL;
-  return C->A->consts[cid].kind;
+  return C->consts[cid].kind;
 }
-HD inline const upy_const* cget(const Dc* C, u32 cid) { return &C->A->consts[cid]; }
+HD inline const upy_const* cget(const Dc* C, u32 cid) { return &C->consts[cid]; }
 HD inline Str cstr(const Dc* C, u32 cid) {
   const upy_const* k = cget(C, cid);
-  return Str{(const char*)(C->A->bytes + k->off), k->n};
+  return Str{(const char*)(C->bytes + k->off), k->n};
 }
 HD inline u32 celem(const Dc* C, u32 cid, u32 i) { return ref_at(C, cget(C, cid)->off + i); }
 HD inline u32 cnelem(const Dc* C, u32 cid) { return cget(C, cid)->n; }
@@ -98,8 +98,8 @@ HD inline bool limbs_eq(const Dc* C, const upy_const* x, const upy_const* y) {
   // normalized magnitudes (packer strips leading zero limbs except a single zero)
   if (x->ival != y->ival) return false;
   u32 nx = x->n, ny = y->n;
-  const u32* lx = C->A->limbs + x->off;
-  const u32* ly = C->A->limbs + y->off;
+  const u32* lx = C->limbs + x->off;
+  const u32* ly = C->limbs + y->off;
   while (nx > 1 && lx[nx - 1] == 0) nx--;
   while (ny > 1 && ly[ny - 1] == 0) ny--;
   if (nx != ny) return false;
@@ -109,7 +109,7 @@ HD inline bool limbs_eq(const Dc* C, const upy_const* x, const upy_const* y) {
 }
 HD inline bool bytes_eq(const Dc* C, u64 oa, u32 na, u64 ob, u32 nb) {
   if (na != nb) return false;
-  const u8* p = C->A->bytes;
+  const u8* p = C->bytes;
   for (u32 i = 0; i < na; i++)
     if (p[oa + i] != p[ob + i]) return false;
   return true;

@@ -34,6 +34,17 @@ struct Code {
   Vec<Str>* kwnames;
 };
 
+// The per-instruction helpers (pops, use_all, store, finish_call) are force-inlined
+// into step: out of line, their prologue/epilogue register saves were the largest
+// source of local-memory traffic (same-session A/B: C3 237.8 -> 223.1 ms).
+#ifdef UPY_SYM_OUTLINE
+#define SYMFN
+#define SYMFN_NOINL NOINL
+#else
+#define SYMFN FORCEINL
+#define SYMFN_NOINL FORCEINL
+#endif
+
 // The read-only part of Code the per-instruction transfer functions use, passed by
 // value into the force-inlined step: the fields live in registers for the whole
 // block instead of being reloaded through K after every arena store (which the
@@ -231,7 +242,7 @@ struct Sim {
     for (i32 i = (i32)pend->n - 1; i >= 0; i--) v = mk2(C, E_NAMED, pend->d[i], v);
     return v;
   }
-  HD NV* pops(NV* st, const Ins* ins, u64 n) {
+  HD SYMFN NV* pops(NV* st, const Ins* ins, u64 n) {
     if (st->n < n) {
       fail_underflow(C, ins);
       return nullptr;
@@ -248,7 +259,7 @@ struct Sim {
     }
     return v;
   }
-  HD NV* use_all(NV* vals) {
+  HD SYMFN NV* use_all(NV* vals) {
     NV* out = vnew<Node*>(C, vals ? vals->n : 0);
     for (u32 i = 0; vals && i < vals->n; i++) vpush(C, out, use(vals->d[i]));
     return out;
@@ -298,7 +309,7 @@ struct Sim {
   }
 
   // _store (symexec.py:295-399); returns the number of following stores consumed
-  HD NOINL int store(const Ins* ins, NV* st, NV* out, i32 idx, i32 hi, Node* target) {
+  HD SYMFN_NOINL int store(const Ins* ins, NV* st, NV* out, i32 idx, i32 hi, Node* target) {
     Node* v = pop(st, ins);
     CKR(C, 0);
     if (is_k(v, E_UNPACKSLOT)) {
@@ -453,7 +464,7 @@ struct Sim {
     return py_index(C, st, -(i64)ins->arg);
   }
 
-  HD void finish_call(NV* st, const Ins* ins, NV* args, Vec<Str>* kwnames) {
+  HD SYMFN void finish_call(NV* st, const Ins* ins, NV* args, Vec<Str>* kwnames) {
     NV* kwargs = vnew<Node*>(C);
     if (kwnames && kwnames->n) {
       u32 n = kwnames->n;

@@ -55,6 +55,12 @@ __device__ __forceinline__ void dc_reset(Dc& C, const KParams& P, u8* base) {
   C.err = 0;
   C.aux0 = C.aux1 = 0;
   C.A = &P.A;
+  C.objs = P.A.objs;
+  C.consts = P.A.consts;
+  C.strs = P.A.strs;
+  C.refs = P.A.refs;
+  C.limbs = P.A.limbs;
+  C.bytes = P.A.bytes;
   C.ins_all = P.ins;
   C.dec_all = P.dec;
   C.depth = 0;

@@ -40,6 +40,12 @@ extern "C" int upyh_decompile(const upy_arena* A, int header, const char* indent
     C.msg = msg.data();
     C.msg_cap = 4096;
     C.A = A;
+    C.objs = A->objs;
+    C.consts = A->consts;
+    C.strs = A->strs;
+    C.refs = A->refs;
+    C.limbs = A->limbs;
+    C.bytes = A->bytes;
     C.ins_all = ins.data();
     C.dec_all = dec.data();
     C.max_depth = 600;
