@@ -251,7 +251,7 @@ struct Sim {
     st->n -= (u32)n;
     return vals;
   }
-  HD SYMFN Node* use(Node* v) {  // symexec.py:571-577
+  HD Node* use(Node* v) {  // symexec.py:571-577
     NV* pend = v ? v->pend : nullptr;
     if (pend && pend->n) {
       v->pend = nullptr;
@@ -264,9 +264,9 @@ struct Sim {
     for (u32 i = 0; vals && i < vals->n; i++) vpush(C, out, use(vals->d[i]));
     return out;
   }
-  HD SYMFN void push(NV* st, Node* x) { vpush(C, st, x); }
+  HD void push(NV* st, Node* x) { vpush(C, st, x); }
 
-  HD SYMFN bool in_comprehension() {
+  HD bool in_comprehension() {
     Str n = obj_name(C, K->oi);
     return s_eqc(n, "<listcomp>") || s_eqc(n, "<setcomp>") || s_eqc(n, "<dictcomp>");
   }
@@ -460,7 +460,7 @@ struct Sim {
     push(st, mk_binop(C, op, l, r, inplace));
   }
 
-  HD SYMFN Node* display_target(NV* st, const Ins* ins) {
+  HD Node* display_target(NV* st, const Ins* ins) {
     return py_index(C, st, -(i64)ins->arg);
   }
 
@@ -539,7 +539,7 @@ struct Sim {
     }
     return v;
   }
-  HD SYMFN u32 const_of(Node* e) {  // `e.const` of a ConstE, AttributeError otherwise
+  HD u32 const_of(Node* e) {  // `e.const` of a ConstE, AttributeError otherwise
     if (!is_k(e, E_CONST)) {
       py_attr_error(C, e, "const");
       return CID_INVALID;
