@@ -233,8 +233,10 @@ struct Emitter {
     if (none && j.bad < 0) j.bad = j.i;
     j.i++;
   }
-  HD void join_end(const Join& j) {  // str.join: items are all evaluated first
-    if (j.bad < 0) return;
+  HD FORCEINL void join_end(const Join& j) {  // str.join: items are all evaluated first
+    if (j.bad >= 0) join_fail(j);
+  }
+  HD NOINL void join_fail(const Join& j) {
     Text m;
     if (fail_begin(C, UPY_ST_PY_TYPE_ERROR, 0, 0, &m)) {
       m_puts(C, &m, "sequence item ");
