@@ -172,12 +172,35 @@ static constexpr NodeSizeTable NODE_SIZES;
 #endif
 HD inline u32 node_bytes(u8 k) { return NODE_SIZES.v[k]; }
 
+#ifndef UPY_MK_TABLE
+// The size comes from the constexpr switch, so at the (inlined) call sites with a
+// literal kind it folds to a constant, and the node is cleared with straight-line
+// 16-B stores (predicated when the kind is only known at run time) instead of a
+// __constant__ table read followed by a loop.
+HD FORCEINL Node* mk(Dc* C, u8 k) {
+  const u32 r = (node_bytes_sw(k) + 15) & ~15u;
+  Node* n = (Node*)alloc_raw(C, r, false);
+#ifdef __CUDA_ARCH__
+  uint4* q = (uint4*)n;
+  const uint4 z = make_uint4(0, 0, 0, 0);
+#pragma unroll
+  for (u32 i = 0; i < (sizeof(Node) + 15) / 16; i++)
+    if (i * 16 < r) q[i] = z;
+#else
+  memset(n, 0, r);
+#endif
+  n->k = k;
+  if (k == E_FUNC || k == E_BUILDCLASS) C->n_defs++;
+  return n;
+}
+#else
 HD ALLOCFN Node* mk(Dc* C, u8 k) {
   Node* n = (Node*)zalloc(C, node_bytes(k));
   n->k = k;
   if (k == E_FUNC || k == E_BUILDCLASS) C->n_defs++;
   return n;
 }
+#endif
 HD inline Node* mk_const(Dc* C, u32 cid) {
   Node* n = mk(C, E_CONST);
   n->cid = cid;
