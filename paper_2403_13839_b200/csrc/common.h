@@ -254,9 +254,33 @@ template <class T>
 HD inline T* sarr(Dc* C, u64 n, bool zero = true) {
   return (T*)salloc(C, n * sizeof(T) + 16, zero);
 }
+// Clear of a compile-time-sized block: straight-line 16-B stores (no loop) up to
+// 256 bytes -- vector headers and the other small records take one to a few stores.
+template <u64 R>
+HD FORCEINL void zero_const(void* p) {
+#ifdef __CUDA_ARCH__
+  if (R <= 256) {
+    uint4* q = (uint4*)p;
+    const uint4 z = make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (u64 i = 0; i < R / 16; i++) q[i] = z;
+  } else {
+    zero16(p, R);
+  }
+#else
+  memset(p, 0, R);
+#endif
+}
 template <class T>
 HD inline T* anew(Dc* C) {
+#ifndef UPY_ANEW_LOOP
+  constexpr u64 r = (sizeof(T) + 15) & ~(u64)15;
+  T* p = (T*)alloc_raw(C, r, false);
+  zero_const<r>(p);
+  return p;
+#else
   return (T*)zalloc(C, sizeof(T));
+#endif
 }
 
 // ------------------------------------------------------------------ vectors
