@@ -20,3 +20,4 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:upy_
 ncu -i /tmp/ncu/decode.ncu-rep --page raw --csv > gpurun_out/ncu_decode_raw.csv 2>&1
 ncu -i /tmp/ncu/decode.ncu-rep --page details --csv > gpurun_out/ncu_decode_details.csv 2>&1
 ls -la gpurun_out
+timeout 900 python bench.py --workload c5 --steps 2 --warmup 3 --no-cpu --pyc 0 > gpurun_out/bench_c5.log 2>&1; tail -1 gpurun_out/bench_c5.log > gpurun_out/bench_c5.json
