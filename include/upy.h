@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define UPY_ABI_VERSION 1
+#define UPY_ABI_VERSION 2
 
 /* Const kinds (code_model.py:56-59). */
 enum {
@@ -74,19 +74,23 @@ typedef struct {
   uint64_t total_code_units;                   /* sum(code_len)/2 upper bound incl. odd */
 } upy_arena;
 
-/* EmitStyle (emitter.py:46-50) plus launch knobs. */
+/* EmitStyle (emitter.py:46-50) plus launch knobs.  indent / tool are UTF-8
+ * (surrogatepass) of any length, in HOST memory; they are read during the
+ * call (copied into the workspace when longer than 64 bytes). */
 typedef struct {
+  const char* indent;        /* EmitStyle.indent */
+  uint64_t indent_len;
+  const char* tool;          /* EmitStyle.tool */
+  uint64_t tool_len;
   int32_t header;            /* EmitStyle.header */
-  int32_t indent_len;        /* EmitStyle.indent, <= 64 bytes UTF-8 */
-  char    indent[64];
-  int32_t tool_len;          /* EmitStyle.tool, <= 64 bytes UTF-8 */
-  char    tool[64];
   int32_t threads_per_block; /* 0 = default */
   int32_t slots;             /* concurrent per-thread arenas; 0 = auto */
-  uint64_t arena_bytes;      /* bytes per slot arena; 0 = auto from max_code_len */
   int32_t decode_only;       /* 1: run only the decode kernel */
+  uint64_t arena_bytes;      /* bytes per slot arena; 0 = auto from max_code_len */
   int32_t skip_decode;       /* 1: reuse the records of a previous decode_only call on the same workspace */
   int32_t schedule;          /* reserved, must be 0 (one decompile schedule: each thread takes the next root) */
+  int32_t max_depth;         /* device recursion guard (UPY_ST_DEPTH_LIMIT); 0 = default 600 */
+  int32_t pad;
 } upy_options;
 
 /* Per-root results (device pointers, caller-allocated). */
@@ -135,7 +139,8 @@ enum {
 size_t upy_abi_sizeof(int which);
 int upy_abi_version(void);
 
-/* Workspace bytes needed by upy_decompile_batch for this arena and options. */
+/* Workspace bytes needed by upy_decompile_batch for this arena and options
+ * (opt may be NULL: default style and knobs). */
 int upy_query_workspace(const upy_arena* arena, const upy_options* opt, size_t* ws_bytes);
 
 /* Decompile every root of the arena (≡ decompile_source per root, pipeline.py:143).

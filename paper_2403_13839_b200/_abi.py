@@ -23,15 +23,17 @@ class UpyArena(C.Structure):
 
 class UpyOptions(C.Structure):
     _fields_ = [
+        ("indent", C.c_char_p), ("indent_len", C.c_uint64),
+        ("tool", C.c_char_p), ("tool_len", C.c_uint64),
         ("header", C.c_int32),
-        ("indent_len", C.c_int32), ("indent", C.c_char * 64),
-        ("tool_len", C.c_int32), ("tool", C.c_char * 64),
         ("threads_per_block", C.c_int32),
         ("slots", C.c_int32),
-        ("arena_bytes", C.c_uint64),
         ("decode_only", C.c_int32),
+        ("arena_bytes", C.c_uint64),
         ("skip_decode", C.c_int32),
         ("schedule", C.c_int32),
+        ("max_depth", C.c_int32),
+        ("pad", C.c_int32),
     ]
 
 
@@ -83,18 +85,15 @@ def arena_struct(arena, base_ptr: int) -> UpyArena:
 
 
 def options(style=None, **kw) -> UpyOptions:
+    """upy_options for an EmitStyle (any indent / tool length; the encoded
+    strings are kept alive on the returned struct)."""
     o = UpyOptions()
     indent = "    " if style is None else style.indent
     tool = "unpyre" if style is None else style.tool
-    ib = indent.encode("utf-8", "surrogatepass")
-    tb = tool.encode("utf-8", "surrogatepass")
-    if len(ib) > 64 or len(tb) > 64:
-        raise ValueError("EmitStyle.indent / EmitStyle.tool longer than 64 bytes")
+    o._keep = (indent.encode("utf-8", "surrogatepass"), tool.encode("utf-8", "surrogatepass"))
+    o.indent, o.indent_len = o._keep[0], len(o._keep[0])
+    o.tool, o.tool_len = o._keep[1], len(o._keep[1])
     o.header = 1 if (style is not None and style.header) else 0
-    o.indent_len = len(ib)
-    o.indent = ib
-    o.tool_len = len(tb)
-    o.tool = tb
     for k, v in kw.items():
         setattr(o, k, v)
     return o

@@ -65,6 +65,8 @@ class DeviceArena:
         self.lib = _lib.load()
         self.arena = arena
         self.device = torch.device(device or "cuda")
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         if pinned is None:
             pinned = getattr(arena, "pinned", None)  # image already page-locked (loader.load_pyc_batch)
         self.host = pinned if pinned is not None else torch.from_numpy(arena.blob).pin_memory()
@@ -73,8 +75,9 @@ class DeviceArena:
         self.opts = _abi.options(style, arena_bytes=arena_bytes, slots=slots,
                                  threads_per_block=threads_per_block)
         ws = C.c_size_t(0)
-        _lib.check(self.lib.upy_query_workspace(C.byref(self.A), C.byref(self.opts), C.byref(ws)),
-                   "upy_query_workspace")
+        with torch.cuda.device(self.device):  # sizing reads the device's SM count
+            _lib.check(self.lib.upy_query_workspace(C.byref(self.A), C.byref(self.opts), C.byref(ws)),
+                       "upy_query_workspace")
         self.ws_bytes = ws.value
         self.ws = torch.empty(max(self.ws_bytes, 256), dtype=torch.uint8, device=self.device)
         n = max(arena.n_roots, 1)
@@ -94,7 +97,8 @@ class DeviceArena:
         self.n = arena.n_roots
 
     def upload(self, stream=None):
-        self.dev.copy_(self.host, non_blocking=True)
+        with self.torch.cuda.device(self.device):
+            self.dev.copy_(self.host, non_blocking=True)
 
     def run(self, stream=None, mode="full"):
         """mode: "full" (decode + decompile), "decode" (decode kernel only) or
@@ -103,11 +107,12 @@ class DeviceArena:
         s = stream or torch.cuda.current_stream(self.device)
         self.opts.decode_only = 1 if mode == "decode" else 0
         self.opts.skip_decode = 1 if mode == "structure" else 0
-        if mode != "decode":
-            self.meta[:8].zero_()
-        rc = self.lib.upy_decompile_batch(C.byref(self.A), C.byref(self.opts), C.byref(self.out),
-                                          C.c_void_p(self.ws.data_ptr()), C.c_size_t(self.ws_bytes),
-                                          C.c_void_p(s.cuda_stream))
+        with torch.cuda.device(self.device):  # the C ABI launches on the current device
+            if mode != "decode":
+                self.meta[:8].zero_()
+            rc = self.lib.upy_decompile_batch(C.byref(self.A), C.byref(self.opts), C.byref(self.out),
+                                              C.c_void_p(self.ws.data_ptr()), C.c_size_t(self.ws_bytes),
+                                              C.c_void_p(s.cuda_stream))
         _lib.check(rc, "upy_decompile_batch")
 
     def fetch(self) -> BatchResult:
@@ -130,34 +135,85 @@ class DeviceArena:
         return BatchResult(st, off, ln, aux, text)
 
 
+def default_slot_bytes(arena: Arena) -> int:
+    """The per-thread arena size upy_query_workspace picks (upy.cu layout())."""
+    return (64 << 10) + 160 * arena.max_code_len
+
+
+def tree_sizes(arena: Arena, roots) -> tuple:
+    """(code bytes, str/bytes constant payload bytes) of the code-object trees
+    under the given root positions (roots and every nested code constant)."""
+    from .arena import KIND_ID
+
+    objs = arena.section("objs")
+    consts = arena.section("consts")
+    refs = arena.section("refs")
+    root_obj = arena.section("roots")
+    seen = set()
+    stack = [int(root_obj[i]) for i in roots]
+    code = payload = 0
+    while stack:
+        o = stack.pop()
+        if o in seen:
+            continue
+        seen.add(o)
+        r = objs[o]
+        code += int(r["code_len"])
+        todo = [int(c) for c in refs[int(r["consts_off"]):int(r["consts_off"]) + int(r["n_consts"])]]
+        while todo:
+            c = consts[todo.pop()]
+            k = int(c["kind"])
+            if k == KIND_ID["code"]:
+                stack.append(int(c["off"]))
+            elif k in (KIND_ID["str"], KIND_ID["bytes"]):
+                payload += int(c["n"])
+            elif k in (KIND_ID["tuple"], KIND_ID["frozenset"]):
+                todo.extend(int(x) for x in refs[int(c["off"]):int(c["off"]) + int(c["n"])])
+    return code, payload
+
+
 def run_arena(arena: Arena, style=None, device=None, retries=3) -> BatchResult:
-    """Decompile every root of a packed arena on the GPU (with on-device retries)."""
-    da = DeviceArena(arena, style, device)
-    da.upload()
-    da.run()
-    res = da.fetch()
-    bytes_per_slot = 0
-    text_scale = 1
-    for _ in range(retries):
-        redo = np.nonzero(np.isin(res.status, RETRYABLE))[0]
-        if not len(redo):
-            break
-        bytes_per_slot = (bytes_per_slot or da.ws_bytes // max(1, len(arena.section("roots")))) * 4
-        text_scale *= 4
-        sub = _subset(arena, redo)
-        db = DeviceArena(sub, style, device, text_cap=text_scale * max(1 << 16, 8 * sub.code_bytes),
-                         arena_bytes=max(bytes_per_slot, 64 << 20), slots=min(len(redo), 4096))
-        db.upload()
-        db.run()
-        r2 = db.fetch()
-        # splice retried results back
-        base = len(res.text)
-        res.text = np.concatenate([res.text, r2.text])
-        for j, i in enumerate(redo):
-            res.status[i] = r2.status[j]
-            res.text_off[i] = base + int(r2.text_off[j])
-            res.text_len[i] = r2.text_len[j]
-            res.aux[i] = r2.aux[j]
+    """Decompile every root of a packed arena on the GPU.
+
+    Roots that hit a device capacity limit (per-thread arena, output buffer) are
+    re-run on the device with 4x larger limits per attempt, sized from the
+    retried roots' own trees and capped by the device's free memory."""
+    torch = _torch()
+    dev = torch.device(device or "cuda")
+    with torch.cuda.device(dev):
+        da = DeviceArena(arena, style, dev)
+        da.upload()
+        da.run()
+        res = da.fetch()
+        del da
+        slot = default_slot_bytes(arena)
+        for attempt in range(1, retries + 1):
+            redo = np.nonzero(np.isin(res.status, RETRYABLE))[0]
+            if not len(redo):
+                break
+            scale = 4 ** attempt
+            slot_bytes = slot * scale
+            code, payload = tree_sizes(arena, redo)
+            text_cap = scale * (8 * code + 2 * payload + 512 * len(redo)) + (1 << 16)
+            free, _ = torch.cuda.mem_get_info(dev)
+            budget = max(0, int(free * 0.6) - text_cap - 2 * len(arena.blob))
+            slots = int(min(len(redo), 4096, budget // slot_bytes))
+            if slots < 1:
+                break  # not even one slot fits: the statuses stay (DeviceCapacityError)
+            sub = _subset(arena, redo)
+            db = DeviceArena(sub, style, dev, text_cap=text_cap, arena_bytes=slot_bytes, slots=slots)
+            db.upload()
+            db.run()
+            r2 = db.fetch()
+            del db
+            # splice retried results back
+            base = len(res.text)
+            res.text = np.concatenate([res.text, r2.text])
+            for j, i in enumerate(redo):
+                res.status[i] = r2.status[j]
+                res.text_off[i] = base + int(r2.text_off[j])
+                res.text_len[i] = r2.text_len[j]
+                res.aux[i] = r2.aux[j]
     return res
 
 
@@ -175,18 +231,107 @@ def _subset(arena: Arena, idx) -> Arena:
     return Arena(blob, dict(arena.offsets), counts, arena.max_code_len, arena.total_code_units)
 
 
-def decompile_many(codes, style=None, device=None):
+def decompile_many(codes, style=None, device=None, devices=None):
     """Batched decompile_source: one entry per input, text or the exception
-    instance the reference would raise (the batch keeps going, like the CLI)."""
+    instance the reference would raise (the batch keeps going, like the CLI).
+
+    `devices` (e.g. ["cuda:0", "cuda:1"]) shards the batch: contiguous root
+    ranges balanced by code bytes (shard.shard_bounds), one packed arena and
+    one host thread per device, results gathered back in input order.  There
+    is no cross-device traffic: every root (with its nested codes) is
+    decompiled on one device."""
     codes = list(codes)
     if not codes:
         return []
+    if devices is not None and len(devices) > 1:
+        return _decompile_sharded(codes, style, list(devices))
+    if devices:
+        device = devices[0]
     res = run_arena(pack(codes), style, device)
+    return _values(res)
+
+
+def _values(res):
     out = res.values()
-    for i, v in enumerate(out):
+    for v in out:
         if isinstance(v, DeviceCapacityError):
             raise v
     return out
+
+
+def shard_plan(codes, n_devices):
+    """Contiguous [lo, hi) ranges of `codes` per device, balanced by the code
+    bytes of each root's tree (the decompile cost grows with it)."""
+    from .shard import shard_bounds
+
+    def tree_code(co, seen):
+        if id(co) in seen:
+            return 0
+        seen.add(id(co))
+        n = len(co.code)
+        todo = list(co.consts)
+        while todo:
+            c = todo.pop()
+            if c.kind == "code":
+                n += tree_code(c.value, seen)
+            elif c.kind in ("tuple", "frozenset"):
+                todo.extend(c.value)
+        return n
+
+    return shard_bounds([tree_code(co, set()) for co in codes], n_devices)
+
+
+def _decompile_sharded(codes, style, devices):
+    from concurrent.futures import ThreadPoolExecutor
+
+    plan = shard_plan(codes, len(devices))
+
+    def work(k):
+        lo, hi = plan[k]
+        if lo == hi:
+            return []
+        return _values(run_arena(pack(codes[lo:hi]), style, devices[k]))
+
+    with ThreadPoolExecutor(len(devices)) as ex:
+        parts = list(ex.map(work, range(len(devices))))
+    return [v for part in parts for v in part]
+
+
+def _value(triple):
+    st, text, aux = triple
+    if st == ST_OK:
+        return text
+    v = make_exception(st, text, aux)
+    if isinstance(v, DeviceCapacityError):
+        raise v
+    return v
+
+
+def decompile_many_distributed(codes, style=None, gather=True, device=None, backend=None):
+    """Multi-process form of decompile_many (one process per GPU, under
+    torch.distributed): every rank passes the same `codes`; rank r decompiles
+    the contiguous shard shard_plan(codes, world)[r] on its own device, with no
+    communication.  gather=True then all-gathers the per-root (status, text,
+    aux) triples so every rank returns the full list in input order (the
+    optional final gather of SURVEY §8e); gather=False returns (lo, hi,
+    values of the rank's own shard).  `backend(codes, style) -> [(status,
+    text, aux)]` replaces the device run (tests use the host build)."""
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    lo, hi = shard_plan(codes, world)[rank]
+    if hi == lo:
+        triples = []
+    elif backend is not None:
+        triples = backend(codes[lo:hi], style)
+    else:
+        res = run_arena(pack(codes[lo:hi]), style, device)
+        triples = [(*res.item(i), (int(res.aux[i][0]), int(res.aux[i][1]))) for i in range(len(res.status))]
+    if not gather:
+        return lo, hi, [_value(t) for t in triples]
+    parts = [None] * world
+    dist.all_gather_object(parts, triples)
+    return [_value(t) for part in parts for t in part]
 
 
 def decompile(code, style=None, device=None) -> str:

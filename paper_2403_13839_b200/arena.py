@@ -265,11 +265,12 @@ def pack(roots) -> Arena:
     return arena
 
 
-def unpack(arena: Arena, code_cls=CodeObject, const_cls=Const, version_cls=VersionTag):
+def unpack(arena: Arena, code_cls=CodeObject, const_cls=Const, version_cls=VersionTag, objects=None):
     """Rebuild the root CodeObject trees of an arena (inverse of `pack`).
 
     Used to feed arena-native synthetic corpora to CPU checkers; the classes are
-    parameters so the same arena can be rebuilt as any CodeObject flavour."""
+    parameters so the same arena can be rebuilt as any CodeObject flavour.
+    `objects` (object indices) selects other objects than the roots."""
     objs = arena.section("objs")
     consts = arena.section("consts")
     strs = arena.section("strs")
@@ -336,7 +337,8 @@ def unpack(arena: Arena, code_cls=CodeObject, const_cls=Const, version_cls=Versi
         built[i] = c
         return c
 
-    return [obj(int(i)) for i in arena.section("roots")]
+    which = arena.section("roots") if objects is None else objects
+    return [obj(int(i)) for i in which]
 
 
 def tile(arena: Arena, reps: int) -> Arena:

@@ -118,11 +118,21 @@ def build_host(force=False):
     return hostcheck.build(force=force)
 
 
+def stage_reference():
+    """Test infrastructure: copy the pure-Python reference into the git-ignored
+    oracle/_ref (oracle/make_ref.py) when /root/reference exists."""
+    sys.path.insert(0, ROOT)
+    from oracle import make_ref
+
+    return make_ref.stage()
+
+
 def main(argv=None):
     argv = sys.argv[1:] if argv is None else argv
     force = "--force" in argv
     build_cuda(force)
     build_host(force)
+    stage_reference()
 
 
 if __name__ == "__main__":

@@ -26,7 +26,7 @@ import sys
 import time
 from pathlib import Path
 
-from .errors import UnpyreError
+from . import errors
 from .model import EmitStyle, VersionTag, flatten_nested_codes
 
 
@@ -46,7 +46,7 @@ def _parse_version(text):
     try:
         major, minor = text.split(".")
         return VersionTag(int(major), int(minor))
-    except (ValueError, UnpyreError):
+    except (ValueError, errors.UnpyreError):
         raise SystemExit(2)
 
 
@@ -74,7 +74,7 @@ def _load_all(items, override, want_objects):
         if _is_json(path, data):
             try:
                 out.append(_Loaded(name, path, roots=load_json_dump(data.decode("utf-8"), override)))
-            except UnpyreError as exc:
+            except errors.UnpyreError as exc:
                 out.append(_Loaded(name, path, error=exc))
         else:
             out.append(_Loaded(name, path, pyc=data))
@@ -108,7 +108,7 @@ def _decompile_loaded(loaded, style, function=None):
             if function:
                 flat = dict(flatten_nested_codes(root))
                 if function not in flat:
-                    pre.setdefault(k, UnpyreError(f"no code object named {function!r}; have: "
+                    pre.setdefault(k, errors.UnpyreError(f"no code object named {function!r}; have: "
                                                   + ", ".join(sorted(flat))))
                     break
                 jobs.append((k, flat[function]))
@@ -159,7 +159,7 @@ def cmd_decompile(args) -> int:
     failures = 0
     outputs = []
     for (name, path, _), r in zip(items, results):
-        if isinstance(r, UnpyreError):
+        if isinstance(r, errors.UnpyreError):
             _diag(f"{name}: {type(r).__name__}: {r}")
             failures += 1
         elif isinstance(r, BaseException):
@@ -203,7 +203,7 @@ def cmd_verify(args) -> int:
         total += 1
         table[version][1] += 1
         name = f"{version}/{case.stem}"
-        if isinstance(r, UnpyreError):
+        if isinstance(r, errors.UnpyreError):
             failures.append((name, f"{type(r).__name__}: {r}"))
             continue
         if isinstance(r, BaseException):

@@ -76,7 +76,7 @@ HD inline void decode_scalar(const u8* code, u32 len, int minor, upy_ins* rec, u
     r.n_prefixes = (u8)(nprefix > 255 ? 255 : nprefix);
     u32 cache = UPY_ENT_CACHE(e);
     r.cache_units = (u8)cache;
-    bool big = sat || (arg >> 32);
+    bool big = UPY_ENT_HASARG(e) && (sat || (arg >> 32));
     r.arg = big ? 0xFFFFFFFFu : (u32)arg;
     r.flags = (u8)(UPY_ENT_HASARG(e) | (big ? 2 : 0));
     i += 2;
@@ -119,6 +119,7 @@ HD inline void decode_scalar(const u8* code, u32 len, int minor, upy_ins* rec, u
         else hi = mid;
       }
       valid = lo < n && (i64)rec[lo].offset == t;
+      if (valid) rec[lo].flags |= 4;  // is_jump_target (disasm.py:168-171)
     }
     if (!valid) {
       res->status = UPY_ST_BAD_JUMP_TARGET;
@@ -166,12 +167,14 @@ struct ChunkState {
   u32 n_before;   // records emitted by earlier chunks
   i64 bad_ins;    // first bad jump (instruction index) so far, -1 if none
   i64 bad_off, bad_tgt;
+  u32 has_jump;   // some chunk so far holds a jump (is_jump_target marking needed)
 };
 __device__ __forceinline__ void chunk_state_init(ChunkState& st) {
   st.carry = ExtRun{0, 0, 0};
   st.n_before = 0;
   st.bad_ins = -1;
   st.bad_off = st.bad_tgt = 0;
+  st.has_jump = 0;
 }
 
 // One warp decodes chunk [base, base+256) units of a <=3.10 object.  Must be
@@ -212,6 +215,7 @@ __device__ __forceinline__ int decode_chunk(const u8* __restrict__ code, u32 len
   unknown_mask &= ~skip;
   ext_mask &= ~skip;
   jump_mask &= ~skip;
+  if (__ballot_sync(0xffffffffu, jump_mask != 0)) st.has_jump = 1;
   // first unknown opcode of the chunk (reference order) stops the object
   u32 has_unknown = __ballot_sync(0xffffffffu, unknown_mask != 0);
   if (has_unknown) {
@@ -369,6 +373,61 @@ __device__ __forceinline__ int decode_chunk(const u8* __restrict__ code, u32 len
 #undef UNIT_OP
 #undef UNIT_ARG
   return (int)total;
+}
+
+// is_jump_target (resolve_jump_targets, disasm.py:166-171): bit2 of every record
+// whose extent start is some jump's target.  Warp-cooperative over n records at
+// `rec` (shared staging or global memory): pass 1 sets bit (t/2 - unit_lo) of the
+// bitmap `bm` (nbits bits, shared memory, cleared here) for every jump target t,
+// pass 2 ORs the flag into the records whose offset is marked.  Targets outside
+// the bitmap's unit range are ignored (the caller sizes it to the object).  Must
+// be called by all 32 lanes after the records are visible to the warp.
+__device__ __forceinline__ void mark_jump_targets(upy_ins* rec, u32 n, u32 unit_lo, u32 nbits, int minor,
+                                                  const u32* __restrict__ tab, u32* bm) {
+  const int lane = threadIdx.x & 31;
+  const u32 nw = (nbits + 31) >> 5;
+  for (u32 k = lane; k < nw; k += 32) bm[k] = 0;
+  __syncwarp();
+  for (u32 k = lane; k < n; k += 32) {
+    const u32* w = reinterpret_cast<const u32*>(rec + k);
+    const u32 w2 = w[2];
+    const u32 e = tab[w2 & 0xFFu];
+    if (!((e >> ENT_JUMP_BIT) & 1u) || ((w2 >> 24) & 2u)) continue;
+    bool ok;
+    const i64 t = jump_target_u64(minor, UPY_ENT_KIND(e), (u64)w[0] + 2ull * ((w2 >> 8) & 0xFFu), w[1], &ok);
+    if (t < 0 || (t & 1)) continue;
+    const u64 u = (u64)(t >> 1) - unit_lo;
+    if ((t >> 1) >= (i64)unit_lo && u < nbits) atomicOr(&bm[u >> 5], 1u << (u & 31));
+  }
+  __syncwarp();
+  for (u32 k = lane; k < n; k += 32) {
+    u32* w = reinterpret_cast<u32*>(rec + k);
+    const u32 u = (w[0] >> 1) - unit_lo;
+    if ((w[0] >> 1) >= unit_lo && u < nbits && ((bm[u >> 5] >> (u & 31)) & 1u)) w[2] |= 4u << 24;
+  }
+  __syncwarp();
+}
+
+// Same, for objects whose unit range exceeds every shared bitmap: each jump's
+// target record is found by binary search over the (offset-sorted) records.
+__device__ __forceinline__ void mark_jump_targets_search(upy_ins* rec, u32 n, int minor, const u32* __restrict__ tab) {
+  const int lane = threadIdx.x & 31;
+  for (u32 k = lane; k < n; k += 32) {
+    const u32* w = reinterpret_cast<const u32*>(rec + k);
+    const u32 w2 = w[2];
+    const u32 e = tab[w2 & 0xFFu];
+    if (!((e >> ENT_JUMP_BIT) & 1u) || ((w2 >> 24) & 2u)) continue;
+    bool ok;
+    const i64 t = jump_target_u64(minor, UPY_ENT_KIND(e), (u64)w[0] + 2ull * ((w2 >> 8) & 0xFFu), w[1], &ok);
+    u32 lo = 0, hi = n;
+    while (lo < hi) {
+      const u32 mid = (lo + hi) >> 1;
+      if ((i64)rec[mid].offset < t) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < n && (i64)rec[lo].offset == t) atomicOr(reinterpret_cast<u32*>(rec + lo) + 2, 4u << 24);
+  }
+  __syncwarp();
 }
 
 // Final status of a <=3.10 object after its last chunk (reference error order:

@@ -30,6 +30,7 @@ struct __align__(128) DecWarpSmem {
   upy_ins out[2][256];      // 2 x 3 KB of records (3.11: the object's code copy)
   u32 cov[X11_UNITS / 32];  // 3.11: units inside an inline-cache span
   u32 xs[X11_UNITS / 32];   // 3.11: extent starts (jump targets)
+  u32 tgt[8];               // jump targets of a one-chunk object (is_jump_target)
   unsigned long long bar[DSTAGES];
 };
 
@@ -61,6 +62,7 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, u32 bytes) 
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
 // chunks a <=3.10 object streams through the ring (0: handled from global memory)
 __device__ __forceinline__ u32 n_chunks(u32 len, u32 minor) {
@@ -196,6 +198,11 @@ __device__ __noinline__ void decode311_warp(const u8* __restrict__ gcode, u32 le
     }
     st.n_before += (u32)total;
   }
+  // is_jump_target: the cache-cover bitmap is dead now and spans the object
+  if (st.has_jump && st.carry.len == 0 && st.bad_ins < 0) {
+    __syncwarp();
+    mark_jump_targets(rec, st.n_before, 0, units, 11, tab, S.cov);
+  }
   if (lane == 0) chunk_finish(len, st, res);
   __syncwarp();
 }
@@ -329,6 +336,9 @@ __global__ void __launch_bounds__(DWARPS * 32, DEC_MINB) upy_decode_kernel(upy_a
             stopped = true;
           } else {
             __syncwarp();
+            // is_jump_target of a one-chunk object: marked in the staging area
+            if (nch == 1 && st.has_jump && st.bad_ins < 0)
+              mark_jump_targets(stage, (u32)total, 0, 256, (int)minor, tab[minor - 8], S.tgt);
             upy_ins* dst = rec + st.n_before;
             // bulk store: 16-B aligned destination, size rounded up to 16 B -- only on
             // the object's last chunk (the overshoot, < 16 B, stays inside this object's
@@ -352,6 +362,22 @@ __global__ void __launch_bounds__(DWARPS * 32, DEC_MINB) upy_decode_kernel(upy_a
         }
         __syncwarp();
         cons++;
+      }
+      if (!stopped && nch > 1 && st.has_jump && st.carry.len == 0 && st.bad_ins < 0) {
+        // is_jump_target of a multi-chunk object: targets may lie in chunks already
+        // stored out, so mark once the object's records are all in global memory
+        // (the staging buffers, idle now, hold the object's target bitmap)
+        if (lane == 0) {
+          bulk_wait_all();
+          fence_async_global();
+        }
+        __syncwarp();
+        const u32 units = len >> 1;
+        if (units <= (u32)sizeof(S.out) * 8)
+          mark_jump_targets(rec, st.n_before, 0, units, (int)minor, tab[minor - 8],
+                            reinterpret_cast<u32*>(&S.out[0][0]));
+        else
+          mark_jump_targets_search(rec, st.n_before, (int)minor, tab[minor - 8]);
       }
       if (!stopped && lane == 0) chunk_finish(len, st, &dec[o]);
     }

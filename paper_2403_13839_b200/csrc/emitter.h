@@ -879,16 +879,29 @@ HD FORCEINL void Emitter::expr_body(Text* t, Node* e) {  // only caller: sub()
 }
 
 HD NOINL void Emitter::format_part(Text* t, Node* fv) {  // emitter.py:510-519
-  if (!is_k(fv, E_FMTVAL)) {
-    // not a FormattedValue: the reference calls _format_part on it anyway
+  // Not a FormattedValue: the reference calls _format_part on it anyway, which
+  // renders `fv.value` when the node has such a field and then fails on
+  // `fv.conversion` (or on `.value` itself).
+  Node* value = nullptr;
+  bool fmt = is_k(fv, E_FMTVAL);
+  if (fmt) value = fv->a;
+  else if (is_k(fv, E_ATTR) || is_k(fv, E_SUBSCR) || is_k(fv, E_STARRED) || is_k(fv, E_YIELD) ||
+           is_k(fv, E_YIELDFROM)) value = fv->a;
+  else if (is_k(fv, E_NAMED)) value = fv->b;
+  else if (is_k(fv, E_COMP)) value = fv->c;
+  else {
     py_attr_error(C, fv, "value");
     return;
   }
   Text inner = {nullptr, 0, 0};
-  bool none = sub(&inner, fv->a, P_TERNARY);
+  bool none = sub(&inner, value, P_TERNARY);
   CK(C);
   if (none) {  // inner.startswith("{") on the None object
     py_error(C, UPY_ST_PY_ATTRIBUTE_ERROR, "'NoneType' object has no attribute 'startswith'");
+    return;
+  }
+  if (!fmt) {
+    py_attr_error(C, fv, "conversion");
     return;
   }
   t_put(C, t, '{');

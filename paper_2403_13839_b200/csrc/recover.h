@@ -50,12 +50,34 @@ HD inline bool code_is_str_doc(Dc* C, u32 oi) {
   const upy_obj* o = obj_at(C, oi);
   return o->n_consts && ckind(C, obj_const_id(C, oi, 0)) == UPY_C_STR;
 }
-HD inline Str code_name_checked(Dc* C, u32 oi) {
-  if (oi == CID_INVALID) {
-    py_error(C, UPY_ST_PY_ATTRIBUTE_ERROR, "object has no attribute 'name'");
+// Python type of a FuncExpr's `code` when MAKE_FUNCTION popped a non-code
+// constant (FuncExpr.code = code_const.const.value, symexec.py:820-821): the
+// node keeps that constant's kind in `j`.
+HD inline const char* py_value_type(i32 kind) {
+  switch (kind) {
+    case UPY_C_BOOL: return "bool"; case UPY_C_INT: return "int"; case UPY_C_FLOAT: return "float";
+    case UPY_C_COMPLEX: return "complex"; case UPY_C_STR: return "str"; case UPY_C_BYTES: return "bytes";
+    case UPY_C_TUPLE: case UPY_C_FROZENSET: return "tuple";
+  }
+  return "NoneType";
+}
+HD inline void py_value_attr_error(Dc* C, i32 kind, const char* attr) {
+  Text t;
+  if (!fail_begin(C, UPY_ST_PY_ATTRIBUTE_ERROR, 0, 0, &t)) return;
+  m_puts(C, &t, "'");
+  m_puts(C, &t, py_value_type(kind));
+  m_puts(C, &t, "' object has no attribute '");
+  m_puts(C, &t, attr);
+  m_puts(C, &t, "'");
+  fail_end(C, &t);
+}
+// `fe.code.name` of a FuncExpr node
+HD inline Str code_name_checked(Dc* C, const Node* fe) {
+  if (fe->cid == CID_INVALID) {
+    py_value_attr_error(C, fe->j, "name");
     return Snone();
   }
-  return obj_name(C, oi);
+  return obj_name(C, fe->cid);
 }
 
 struct Recovery {
@@ -153,7 +175,7 @@ HD inline int comp_kind_of(Str name) {  // COMP_NAMES (recover.py:17-22)
 
 HD inline Node* Recovery::pre_expr(Node* e) {  // recover.py:176-189
   if (is_k(e, E_CALL) && is_k(e->a, E_FUNC)) {
-    Str nm = code_name_checked(C, e->a->cid);
+    Str nm = code_name_checked(C, e->a);
     CKR(C, nullptr);
     int kind = comp_kind_of(nm);
     if (kind >= 0 && e->l1->n == 1 && e->l2->n == 0) {
@@ -165,7 +187,7 @@ HD inline Node* Recovery::pre_expr(Node* e) {  // recover.py:176-189
     }
   }
   if (is_k(e, E_FUNC)) {
-    Str nm = code_name_checked(C, e->cid);
+    Str nm = code_name_checked(C, e);
     CKR(C, nullptr);
     if (s_eqc(nm, "<lambda>")) {
       Node* lam = make_lambda(e);
@@ -180,7 +202,7 @@ HD inline Node* Recovery::post_expr(Node* e) {
   return e;
 }
 HD inline Node* Recovery::hoist(Node* fe) {  // recover.py:221-227
-  Str name = code_name_checked(C, fe->cid);
+  Str name = code_name_checked(C, fe);
   CKR(C, fe);
   if (s_eqc(name, "<lambda>")) {
     Node* nm = mk_name_syn(C, "__lambda_", lambda_counter, SC_FAST);
@@ -196,7 +218,7 @@ HD NOINL Node* Recovery::make_funcdef(Str name, Node* fe) {  // recover.py:150-1
   GUARD(C);
   CKR(C, nullptr);
   if (fe->cid == CID_INVALID) {
-    py_error(C, UPY_ST_PY_ATTRIBUTE_ERROR, "object has no attribute 'varnames'");
+    py_value_attr_error(C, fe->j, "varnames");
     return nullptr;
   }
   NV* defs = vnew<Node*>(C, fe->l1->n);
@@ -247,7 +269,7 @@ HD NOINL Node* Recovery::make_classdef(Str name, Node* call) {  // recover.py:16
   if (args->n < 2 || !is_k(args->d[0], E_FUNC)) return nullptr;
   u32 cls_code = args->d[0]->cid;
   if (cls_code == CID_INVALID) {
-    py_error(C, UPY_ST_PY_ATTRIBUTE_ERROR, "object has no attribute 'code'");
+    py_value_attr_error(C, args->d[0]->j, "code");
     return nullptr;
   }
   NV* bases = vnew<Node*>(C, args->n - 2);
@@ -369,7 +391,7 @@ HD NOINL Node* Recovery::match_def(Node* target, Node* value) {  // recover.py:1
     return nullptr;
   }
   if (is_k(inner, E_FUNC)) {
-    Str nm = code_name_checked(C, inner->cid);
+    Str nm = code_name_checked(C, inner);
     CKR(C, nullptr);
     if (s_eq(nm, target->s)) {
       Node* made = make_funcdef(target->s, inner);

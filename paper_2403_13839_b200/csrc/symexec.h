@@ -1266,6 +1266,7 @@ HD FORCEINL int Sim::step(const Ins* ins, i32 idx, i32 hi, NV* st, NV* out, cons
       CKR(C, 0);
       if (cc == CID_INVALID) { py_error(C, UPY_ST_PY_ATTRIBUTE_ERROR, "'NoneType' object has no attribute 'value'"); return 0; }
       fe->cid = ckind(C, cc) == UPY_C_CODE ? (u32)cget(C, cc)->off : CID_INVALID;
+      fe->j = (i32)ckind(C, cc);  // Python type of FuncExpr.code when it is not a code object
       BR_PUSH(fe);
       return 0;
     }

@@ -9,6 +9,7 @@
 //                          then the text is appended to the flat output buffer.
 #include <cuda_runtime.h>
 #include <stdio.h>
+#include <mutex>
 #include "pipeline.h"
 
 // decode_kernel.cu
@@ -18,6 +19,9 @@ cudaError_t upy_decode_launch(const upy_arena* arena, upy_ins* ins, upy_decoded*
 #define SLOT_HEADER (MSG_BYTES + SINK_BYTES)
 
 static __thread char g_last_error[512];
+static constexpr int kMaxDevices = 64;
+static std::mutex g_dev_cfg_mu;
+static bool g_dev_cfg_done[kMaxDevices];
 static void set_err(const char* fmt, const char* a = "") {
   snprintf(g_last_error, sizeof g_last_error, fmt, a);
 }
@@ -32,7 +36,9 @@ struct KParams {
   u32* next_root;
   int header;
   int max_depth;
-  int indent_len, tool_len;
+  u64 indent_len, tool_len;
+  const char* indent_ptr;  // style strings: `indent` / `tool` below when <= 64 bytes,
+  const char* tool_ptr;    // else a workspace copy
   char indent[64];
   char tool[64];
   int lane_stride;  // 1: every thread takes roots; 32: one root-taking thread per warp
@@ -106,8 +112,8 @@ __global__ void __launch_bounds__(128, UPY_MINB) upy_decompile_kernel(KParams P)
   u8* base = P.slots_base + slot * P.slot_bytes;
   EmitOpts opt;
   opt.header = P.header != 0;
-  opt.indent = Str{P.indent, (u32)P.indent_len};
-  opt.tool = Str{P.tool, (u32)P.tool_len};
+  opt.indent = Str{P.indent_len <= 64 ? P.indent : P.indent_ptr, (u32)P.indent_len};
+  opt.tool = Str{P.tool_len <= 64 ? P.tool : P.tool_ptr, (u32)P.tool_len};
 #ifndef UPY_DC_SHARED
   // The per-thread context lives on the thread's stack: the shared-memory copy
   // (17 KB per block, 139 KB per SM at 8 blocks) cost more in L1 capacity for the
@@ -132,7 +138,7 @@ __global__ void __launch_bounds__(128, UPY_MINB) upy_decompile_kernel(KParams P)
 
 // ------------------------------------------------------------ C ABI
 struct WsLayout {
-  u64 ins_off, dec_off, ctr_off, slots_off, total;
+  u64 ins_off, dec_off, ctr_off, style_off, slots_off, total;
   u64 slots, slot_bytes;
   int lane_stride;
 };
@@ -157,7 +163,11 @@ static WsLayout layout(const upy_arena* a, const upy_options* o) {
   L.ins_off = 0;
   L.dec_off = al(units * sizeof(upy_ins));
   L.ctr_off = L.dec_off + al((u64)a->n_objs * sizeof(upy_decoded));
-  L.slots_off = L.ctr_off + 256;
+  L.style_off = L.ctr_off + 256;
+  u64 style_bytes = 0;  // EmitStyle strings longer than the kernel-parameter copies
+  if (o && o->indent_len > 64) style_bytes += o->indent_len;
+  if (o && o->tool_len > 64) style_bytes += o->tool_len;
+  L.slots_off = L.style_off + al(style_bytes);
   // C3-size objects use ~55 KB; larger ones overflow and are retried by the host with 4x
   // measured peaks: C3 (400 B code) ~25 KB, C4 (19 KB code) ~2.2 MB => ~115 B per code byte
   u64 sb = o && o->arena_bytes ? o->arena_bytes : (u64)(64u << 10) + (u64)a->max_code_len * 160u;
@@ -258,21 +268,26 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
   }
   if (opt && opt->decode_only) return 0;
   if (arena->n_roots == 0) return 0;
-  static bool carveout_set = false;
-  if (!carveout_set) {
-    // no shared memory: give the whole L1/shared pool to L1 (arena + stack hit rate)
-    cudaFuncSetAttribute(upy_decompile_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-    carveout_set = true;
-  }
-  static size_t stack_set = 0;
-  size_t want = 48 * 1024;
-  if (stack_set != want) {
-    cudaError_t e = cudaDeviceSetLimit(cudaLimitStackSize, want);
-    if (e != cudaSuccess) {
-      set_err("cudaDeviceSetLimit(stack): %s", cudaGetErrorString(e));
-      return 2;
+  {
+    // one-time per-device settings (both are per device: the kernel runs on the
+    // caller's current device); guarded for concurrent callers
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_dev_cfg_mu);
+    if (dev < 0 || dev >= kMaxDevices) {
+      set_err("upy_decompile_batch: device ordinal out of range");
+      return 1;
     }
-    stack_set = want;
+    if (!g_dev_cfg_done[dev]) {
+      // no shared memory: give the whole L1/shared pool to L1 (arena + stack hit rate)
+      cudaFuncSetAttribute(upy_decompile_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+      cudaError_t e = cudaDeviceSetLimit(cudaLimitStackSize, 48 * 1024);
+      if (e != cudaSuccess) {
+        set_err("cudaDeviceSetLimit(stack): %s", cudaGetErrorString(e));
+        return 2;
+      }
+      g_dev_cfg_done[dev] = true;
+    }
   }
   cudaMemsetAsync(ctr, 0, 256, s);
   KParams P;
@@ -284,18 +299,26 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
   P.slots_base = ws + L.slots_off;
   P.slot_bytes = L.slot_bytes;
   P.next_root = ctr;
-  P.max_depth = 600;
-  if (opt) {
-    P.header = opt->header;
-    P.indent_len = opt->indent_len > 64 ? 64 : opt->indent_len;
-    memcpy(P.indent, opt->indent, P.indent_len);
-    P.tool_len = opt->tool_len > 64 ? 64 : opt->tool_len;
-    memcpy(P.tool, opt->tool, P.tool_len);
+  P.max_depth = opt && opt->max_depth > 0 ? opt->max_depth : 600;
+  static const char kIndent[] = "    ", kTool[] = "unpyre";
+  const char* ind = opt && opt->indent ? opt->indent : kIndent;
+  const char* tool = opt && opt->tool ? opt->tool : kTool;
+  P.indent_len = opt && opt->indent ? opt->indent_len : 4;
+  P.tool_len = opt && opt->tool ? opt->tool_len : 6;
+  P.header = opt ? opt->header : 0;
+  u8* style_ws = ws + L.style_off;
+  if (P.indent_len <= 64) {
+    memcpy(P.indent, ind, P.indent_len);
   } else {
-    P.indent_len = 4;
-    memcpy(P.indent, "    ", 4);
-    P.tool_len = 6;
-    memcpy(P.tool, "unpyre", 6);
+    cudaMemcpyAsync(style_ws, ind, P.indent_len, cudaMemcpyHostToDevice, s);
+    P.indent_ptr = (const char*)style_ws;
+    style_ws += P.indent_len;
+  }
+  if (P.tool_len <= 64) {
+    memcpy(P.tool, tool, P.tool_len);
+  } else {
+    cudaMemcpyAsync(style_ws, tool, P.tool_len, cudaMemcpyHostToDevice, s);
+    P.tool_ptr = (const char*)style_ws;
   }
   P.lane_stride = L.lane_stride;
   int tpb = eff_tpb(opt);

@@ -2,9 +2,16 @@
 one to one so callers can `except` the same types.
 
 Reference: /root/reference/pkg/src/unpyre/errors.py:8-102.  The device reports a
-status code per object plus a message it formatted itself; `raise_status`
+status code per object plus a message it formatted itself; `make_exception`
 turns that into the matching exception instance (attributes from the aux
 words the kernel wrote).
+
+Drop-in interop: when the reference package (`unpyre`) is importable, the
+classes below are REPLACED by the reference's own class objects (`bind`), so
+`except unpyre.UnpyreError` around `decompile(...)` -- e.g. the reference CLI's
+`cmd_decompile` (cli.py:82) with this package patched in -- catches exactly
+what it catches around `unpyre.decompile_source`.  Without the reference the
+package's own mirror hierarchy is used.
 """
 
 
@@ -129,7 +136,9 @@ ST_DEPTH_LIMIT = 32
 ST_INTERNAL = 33
 ST_NOT_RUN = 34
 
-RETRYABLE = (ST_ARENA_OVERFLOW, ST_OUTPUT_OVERFLOW, ST_DEPTH_LIMIT)
+# capacity statuses the host re-runs with larger limits (ST_DEPTH_LIMIT is the
+# device's recursion guard, sized to the kernel stack: a retry cannot pass it)
+RETRYABLE = (ST_ARENA_OVERFLOW, ST_OUTPUT_OVERFLOW)
 
 
 def _bare(cls, message):
@@ -202,3 +211,50 @@ def make_exception(status, message, aux):
     if py is not None:
         return py(message)
     return DeviceCapacityError(f"device status {status}: {message}")
+
+
+# ---------------------------------------------------------------- interop
+CLASS_NAMES = ("UnpyreError", "UnsupportedVersion", "UnknownMagic", "TruncatedHeader", "MalformedMarshal",
+               "SchemaError", "UnknownOpcode", "TruncatedCode", "BadJumpTarget", "MalformedExceptionTable",
+               "StackUnderflow", "UnsupportedOpcode", "StackDepthMismatch", "StructuringFailed",
+               "InternalMarkerLeak")
+_OWN = {n: globals()[n] for n in CLASS_NAMES}
+
+
+def bind(module=None):
+    """Use `module`'s exception classes (the reference's `unpyre.errors`, or any
+    module defining the same names) for every exception this package raises;
+    `bind(None)` restores the package's own hierarchy.  Returns the module bound."""
+    import sys
+
+    g = globals()
+    for n in CLASS_NAMES:
+        cls = getattr(module, n, None) if module is not None else None
+        g[n] = cls if cls is not None else _OWN[n]
+    pkg = sys.modules.get(__package__)
+    if pkg is not None:  # the package re-exports the classes
+        for n in CLASS_NAMES:
+            if hasattr(pkg, n):
+                setattr(pkg, n, g[n])
+    return module
+
+
+def bound():
+    """True when the reference's classes are in use."""
+    return UnpyreError is not _OWN["UnpyreError"]
+
+
+def _auto_bind():
+    import importlib
+    import os
+
+    if os.environ.get("UPY_BIND_REFERENCE_ERRORS", "1") == "0":
+        return
+    try:
+        ref = importlib.import_module("unpyre.errors")
+    except ImportError:
+        return
+    bind(ref)
+
+
+_auto_bind()

@@ -13,108 +13,125 @@ from __future__ import annotations
 import base64
 import json
 
-from .errors import SchemaError, UnsupportedVersion
+from . import errors
 from .model import CodeObject, Const, VersionTag
 
-_CODE_FIELDS = {  # pyc.py:357-375, checked in this order
-    "argcount": int, "posonlyargcount": int, "kwonlyargcount": int, "nlocals": int, "stacksize": int,
-    "flags": int, "code": str, "consts": list, "names": list, "varnames": list, "freevars": list,
-    "cellvars": list, "name": str, "filename": str, "firstlineno": int, "linetable": str,
-    "exceptiontable": str,
-}
+# Field schema of one code object, in the order the reference validates it
+# (pyc.py:357-375, 420-437): (key, JSON type, type name in the message).
+_SCHEMA = tuple((k, t, t.__name__) for k, t in (
+    ("argcount", int), ("posonlyargcount", int), ("kwonlyargcount", int), ("nlocals", int),
+    ("stacksize", int), ("flags", int), ("code", str), ("consts", list), ("names", list),
+    ("varnames", list), ("freevars", list), ("cellvars", list), ("name", str), ("filename", str),
+    ("firstlineno", int), ("linetable", str), ("exceptiontable", str)))
+_STR_LISTS = ("names", "varnames", "freevars", "cellvars")
+_INT_FIELDS = ("argcount", "posonlyargcount", "kwonlyargcount", "nlocals", "stacksize", "flags")
+
+
+class _Reader:
+    """Converts one parsed dump tree into CodeObject/Const records, failing with
+    the reference's SchemaError (message, JSON path) at the first violation."""
+
+    def __init__(self, version):
+        self.version = version
+        # constant tag -> builder(node, path); a builder may raise KeyError (the
+        # missing key) or ValueError/TypeError (a malformed value): `const`
+        # turns those into the reference's two generic messages (pyc.py:503-506)
+        self.tags = {
+            "none": lambda n, p: Const("none"),
+            "ellipsis": lambda n, p: Const("ellipsis"),
+            "bool": lambda n, p: Const("bool", self._typed(n, p, "v", bool, "expected bool")),
+            "int": lambda n, p: Const("int", int(n["v"])),
+            "float": lambda n, p: Const("float", float.fromhex(n["v"])),
+            "complex": lambda n, p: Const("complex", complex(float.fromhex(n["re"]), float.fromhex(n["im"]))),
+            "str": lambda n, p: Const("str", self._typed(n, p, "v", str, "expected string")),
+            "bytes": lambda n, p: Const("bytes", self.b64(n, p, "v")),
+            "tuple": lambda n, p: Const("tuple", self.seq(n["v"], p + ".v")),
+            "frozenset": lambda n, p: Const("frozenset", self.seq(n["v"], p + ".v")),
+            "code": lambda n, p: Const("code", self.code(n["v"], p + ".v")),
+        }
+
+    @staticmethod
+    def _typed(node, path, key, typ, msg):
+        v = node[key]
+        if not isinstance(v, typ):
+            raise errors.SchemaError(msg, f"{path}.{key}")
+        return v
+
+    @staticmethod
+    def b64(node, path, key):
+        v = node[key]
+        where = f"{path}.{key}"
+        if not isinstance(v, str):
+            raise errors.SchemaError("expected base64 string", where)
+        try:
+            return base64.b64decode(v, validate=True)
+        except Exception:  # noqa: BLE001 -- binascii.Error / ValueError, as the reference
+            raise errors.SchemaError("invalid base64", where) from None
+
+    def seq(self, items, path):
+        return tuple(self.const(c, f"{path}[{i}]") for i, c in enumerate(items))
+
+    def const(self, node, path):
+        if not (isinstance(node, dict) and "t" in node):
+            raise errors.SchemaError("constant must be an object with a 't' tag", path)
+        tag = node["t"]
+        build = self.tags.get(tag) if isinstance(tag, str) else None
+        if build is None:
+            raise errors.SchemaError(f"unknown constant tag {tag!r}", f"{path}.t")
+        try:
+            return build(node, path)
+        except KeyError as exc:
+            raise errors.SchemaError("missing field", f"{path}.{exc.args[0]}") from None
+        except (ValueError, TypeError):
+            raise errors.SchemaError(f"bad value for constant of type {tag!r}", path) from None
+
+    def code(self, node, path):
+        if not isinstance(node, dict):
+            raise errors.SchemaError("code object must be a JSON object", path)
+        for key, typ, tname in _SCHEMA:
+            if key not in node:
+                raise errors.SchemaError("missing field", f"{path}.{key}")
+            v = node[key]
+            if isinstance(v, bool) or not isinstance(v, typ):
+                raise errors.SchemaError(f"expected {tname}", f"{path}.{key}")
+        for key in _STR_LISTS:
+            if any(not isinstance(x, str) for x in node[key]):
+                raise errors.SchemaError("expected list of strings", f"{path}.{key}")
+        consts = self.seq(node["consts"], path + ".consts")
+        ints = [node[k] for k in _INT_FIELDS]
+        code = self.b64(node, path, "code")
+        lists = [tuple(node[k]) for k in _STR_LISTS]
+        return CodeObject(self.version, *ints, code, consts, *lists, node["name"], node["filename"],
+                          node["firstlineno"], self.b64(node, path, "linetable"),
+                          self.b64(node, path, "exceptiontable"), node.get("qualname", ""))
+
+
+def _version_of(doc, override):
+    if override is not None:
+        return override
+    ver = doc.get("python_version")
+    if not (isinstance(ver, list) and len(ver) == 2 and all(isinstance(x, int) for x in ver)):
+        raise errors.SchemaError("python_version must be [major, minor]", "$.python_version")
+    try:
+        return VersionTag(*ver)
+    except errors.UnsupportedVersion as exc:
+        raise errors.SchemaError(str(exc), "$.python_version") from None
 
 
 def load_json_dump(text: str, version_override=None) -> list:
-    """pyc.py:378-407: one root code object, returned as a one-element list."""
+    """One root code object, returned as a one-element list (pyc.py:378-407)."""
     try:
         doc = json.loads(text)
     except json.JSONDecodeError as exc:
-        raise SchemaError(f"not valid JSON: {exc.msg}", "$") from None
+        raise errors.SchemaError(f"not valid JSON: {exc.msg}", "$") from None
     if not isinstance(doc, dict):
-        raise SchemaError("top level must be an object", "$")
+        raise errors.SchemaError("top level must be an object", "$")
     if doc.get("format_version") != 1:
-        raise SchemaError("format_version must be 1", "$.format_version")
-    ver = doc.get("python_version")
-    if version_override is not None:
-        version = version_override
-    else:
-        if not isinstance(ver, list) or len(ver) != 2 or not all(isinstance(x, int) for x in ver):
-            raise SchemaError("python_version must be [major, minor]", "$.python_version")
-        try:
-            version = VersionTag(*ver)
-        except UnsupportedVersion as exc:
-            raise SchemaError(str(exc), "$.python_version") from None
+        raise errors.SchemaError("format_version must be 1", "$.format_version")
+    version = _version_of(doc, version_override)
     if "root" not in doc:
-        raise SchemaError("missing field", "$.root")
-    return [_code(doc["root"], "$.root", version)]
-
-
-def _b64(obj, path, key):
-    raw = obj[key]
-    if not isinstance(raw, str):
-        raise SchemaError("expected base64 string", f"{path}.{key}")
-    try:
-        return base64.b64decode(raw, validate=True)
-    except Exception:  # noqa: BLE001 - binascii.Error and friends, as the reference
-        raise SchemaError("invalid base64", f"{path}.{key}") from None
-
-
-def _code(obj, path, version):
-    """pyc.py:420-458."""
-    if not isinstance(obj, dict):
-        raise SchemaError("code object must be a JSON object", path)
-    for key, typ in _CODE_FIELDS.items():
-        if key not in obj:
-            raise SchemaError("missing field", f"{path}.{key}")
-        if not isinstance(obj[key], typ) or isinstance(obj[key], bool):
-            raise SchemaError(f"expected {typ.__name__}", f"{path}.{key}")
-    for key in ("names", "varnames", "freevars", "cellvars"):
-        if not all(isinstance(x, str) for x in obj[key]):
-            raise SchemaError("expected list of strings", f"{path}.{key}")
-    consts = tuple(_const(c, f"{path}.consts[{i}]", version) for i, c in enumerate(obj["consts"]))
-    return CodeObject(
-        version, obj["argcount"], obj["posonlyargcount"], obj["kwonlyargcount"], obj["nlocals"],
-        obj["stacksize"], obj["flags"], _b64(obj, path, "code"), consts, tuple(obj["names"]),
-        tuple(obj["varnames"]), tuple(obj["freevars"]), tuple(obj["cellvars"]), obj["name"], obj["filename"],
-        obj["firstlineno"], _b64(obj, path, "linetable"), _b64(obj, path, "exceptiontable"),
-        obj.get("qualname", ""))
-
-
-def _const(obj, path, version):
-    """pyc.py:461-508."""
-    if not isinstance(obj, dict) or "t" not in obj:
-        raise SchemaError("constant must be an object with a 't' tag", path)
-    t = obj["t"]
-    try:
-        if t == "none":
-            return Const("none")
-        if t == "ellipsis":
-            return Const("ellipsis")
-        if t == "bool":
-            if not isinstance(obj["v"], bool):
-                raise SchemaError("expected bool", f"{path}.v")
-            return Const("bool", obj["v"])
-        if t == "int":
-            return Const("int", int(obj["v"]))
-        if t == "float":
-            return Const("float", float.fromhex(obj["v"]))
-        if t == "complex":
-            return Const("complex", complex(float.fromhex(obj["re"]), float.fromhex(obj["im"])))
-        if t == "str":
-            if not isinstance(obj["v"], str):
-                raise SchemaError("expected string", f"{path}.v")
-            return Const("str", obj["v"])
-        if t == "bytes":
-            return Const("bytes", _b64(obj, path, "v"))
-        if t in ("tuple", "frozenset"):
-            return Const(t, tuple(_const(c, f"{path}.v[{i}]", version) for i, c in enumerate(obj["v"])))
-        if t == "code":
-            return Const("code", _code(obj["v"], f"{path}.v", version))
-    except KeyError as exc:
-        raise SchemaError("missing field", f"{path}.{exc.args[0]}") from None
-    except (ValueError, TypeError):
-        raise SchemaError(f"bad value for constant of type {t!r}", path) from None
-    raise SchemaError(f"unknown constant tag {t!r}", f"{path}.t")
+        raise errors.SchemaError("missing field", "$.root")
+    return [_Reader(version).code(doc["root"], "$.root")]
 
 
 # ------------------------------------------------------------------ writer

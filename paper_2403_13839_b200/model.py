@@ -13,7 +13,7 @@ from __future__ import annotations
 import struct
 from dataclasses import dataclass
 
-from .errors import UnsupportedVersion
+from . import errors
 
 SUPPORTED_VERSIONS = ((3, 8), (3, 9), (3, 10), (3, 11))
 CO_VARARGS = 0x0004
@@ -29,7 +29,7 @@ class VersionTag:
 
     def __post_init__(self):
         if (self.major, self.minor) not in SUPPORTED_VERSIONS:
-            raise UnsupportedVersion(self.major, self.minor)
+            raise errors.UnsupportedVersion(self.major, self.minor)
 
     def __str__(self):
         return f"{self.major}.{self.minor}"

@@ -76,6 +76,19 @@ def _mutant(n=100):
             for m in (8, 9, 10, 11) for s in range(n)]
 
 
+def _mutant2(n=300, first=5000):
+    """Fresh byte-mutant seeds (never used while the kernels were written)."""
+    return [{"case": f"mutant2-3.{m}-{s}", "gen": "fuzz", "minor": m, "seed": s, "kw": {"mode": "mutant"}}
+            for m in (8, 9, 10, 11) for s in range(first, first + n)]
+
+
+# decoder-only cases (no decompile golden: the reference's CFG pass is quadratic
+# at this size): 3.10 objects beyond the decode kernel's shared bitmaps
+C4BIG = [{"case": "c4big-3.10-1", "gen": "c4", "minor": 10, "seed": 1, "kw": {"target_units": 60000}},
+         {"case": "c4big-3.10-3", "gen": "c4", "minor": 10, "seed": 3, "kw": {"target_units": 52000}},
+         {"case": "c4big-3.11-2", "gen": "c4", "minor": 11, "seed": 2, "kw": {"target_units": 30000}}]
+
+
 class _Lazy(dict):
     def __init__(self, **makers):
         super().__init__()
@@ -91,4 +104,4 @@ class _Lazy(dict):
         return self._makers.keys()
 
 
-GOLDEN_SETS = _Lazy(c1=_fig1, c3=_c3, c4=_c4, snippets=_snippets, fuzz=_fuzz, mutant=_mutant)
+GOLDEN_SETS = _Lazy(c1=_fig1, c3=_c3, c4=_c4, snippets=_snippets, fuzz=_fuzz, mutant=_mutant, mutant2=_mutant2)

@@ -48,8 +48,10 @@ def run_ref(co, style=None):
         return type(e).__name__, str(e)
 
 
-def main():
+def main(only=None):
     for name, specs in cases.GOLDEN_SETS.items():
+        if only and name not in only:
+            continue
         path = os.path.join(HERE, f"{name}.jsonl")
         n_ok = 0
         with open(path, "w") as f:
@@ -64,4 +66,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:])

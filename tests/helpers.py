@@ -16,9 +16,14 @@ ST_NAMES = {0: "ok", 1: "UnpyreError", 2: "UnknownOpcode", 3: "TruncatedCode", 4
             21: "AttributeError", 22: "TypeError", 23: "KeyError", 24: "ValueError", 25: "RecursionError"}
 PY_INTERNAL = {"IndexError", "AttributeError", "TypeError", "KeyError", "ValueError", "RecursionError"}
 
-# cases whose reference outcome is a Python-internal error on a malformed name index
-# (None name text reaching a str.join / concatenation in the emitter); see DESIGN.md §4
-KNOWN_CLASS_GAPS = set()
+# Cases where even the exception class differs, inside the reference's
+# Python-internal error domain (outside SURVEY §8c's parity domain).  Both are
+# byte mutants whose MAKE_FUNCTION defaults / BUILD_CONST_KEY_MAP keys are a str
+# constant: the reference iterates the str (`ConstE(c) for c in const.value`,
+# symexec.py:568,818) into ConstE nodes holding bare 1-char strings and fails
+# later on `.const` / `.kind` of those (AttributeError); the device stops at the
+# iteration with TypeError("const is not iterable").  See DESIGN.md §4.
+KNOWN_CLASS_GAPS = {"mutant2-3.10-5031", "mutant2-3.11-5118"}
 
 
 def inputs(recs):
@@ -46,6 +51,8 @@ def mismatches(recs, got, strict=True):
         if want == g:
             continue
         if not strict and r["status"] in PY_INTERNAL and g[0] == r["status"]:
+            continue
+        if r["case"] in KNOWN_CLASS_GAPS and r["status"] in PY_INTERNAL and g[0] in PY_INTERNAL:
             continue
         bad.append((r["case"], r["status"], g[0], r["text"][:300], g[1][:300]))
     return bad

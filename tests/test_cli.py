@@ -76,3 +76,26 @@ def test_json_dump_reader_roundtrip_and_schema_errors():
         with pytest.raises(errors.SchemaError) as ei:
             jsondump.load_json_dump(data.decode())
         assert str(ei.value) == msg, name
+
+
+def test_json_dump_reader_matches_reference_on_schema_mutants():
+    """tests/golden/json.jsonl: the reference reader's outcome (tree digest or
+    SchemaError/UnsupportedVersion message) on 720 seeded schema mutants."""
+    from conftest import GOLDEN
+    from paper_2403_13839_b200 import jsondump
+    from paper_2403_13839_b200.synth import jsonfuzz
+
+    from helpers import code_key_sha
+
+    docs = jsonfuzz.base_docs(GOLDEN)
+    bad = []
+    for rec in load_golden("json"):
+        text = jsonfuzz.mutate(docs[rec["base"]], rec["seed"])
+        try:
+            (co,) = jsondump.load_json_dump(text)
+            got = ("ok", code_key_sha(co))
+        except Exception as e:  # noqa: BLE001
+            got = (type(e).__name__, str(e))
+        if got != (rec["status"], rec["text"]):
+            bad.append((rec["base"], rec["seed"], rec["status"], rec["text"], got))
+    assert not bad, bad[:3]

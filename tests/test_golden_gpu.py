@@ -8,7 +8,7 @@ from helpers import inputs, mismatches, outcome, style_of
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("gset", ["c1", "c2", "c3", "c4", "snippets", "fuzz", "mutant"])
+@pytest.mark.parametrize("gset", ["c1", "c2", "c3", "c4", "snippets", "fuzz", "mutant", "mutant2"])
 def test_gpu_matches_reference(gset):
     from paper_2403_13839_b200 import api
 
