@@ -90,7 +90,9 @@ typedef struct {
   int32_t skip_decode;       /* 1: reuse the records of a previous decode_only call on the same workspace */
   int32_t schedule;          /* reserved, must be 0 (one decompile schedule: each thread takes the next root) */
   int32_t max_depth;         /* device recursion guard (UPY_ST_DEPTH_LIMIT); 0 = default 600 */
-  int32_t pad;
+  int32_t function_tree;     /* 1: emit_module([function_tree(root)]) without validation -- the
+                                reference CLI's --function path (cli.py:75-78) -- instead of
+                                decompile_source */
 } upy_options;
 
 /* Per-root results (device pointers, caller-allocated). */

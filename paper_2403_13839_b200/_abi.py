@@ -33,7 +33,7 @@ class UpyOptions(C.Structure):
         ("skip_decode", C.c_int32),
         ("schedule", C.c_int32),
         ("max_depth", C.c_int32),
-        ("pad", C.c_int32),
+        ("function_tree", C.c_int32),
     ]
 
 

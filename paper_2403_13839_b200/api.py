@@ -59,7 +59,7 @@ class DeviceArena:
     `run()` on HBM-resident inputs and `upload()+run()+fetch()` end to end)."""
 
     def __init__(self, arena: Arena, style=None, device=None, text_cap=None, arena_bytes=0, slots=0,
-                 threads_per_block=0, pinned=None):
+                 threads_per_block=0, pinned=None, function_tree=False):
         torch = _torch()
         self.torch = torch
         self.lib = _lib.load()
@@ -73,7 +73,7 @@ class DeviceArena:
         self.dev = torch.empty(self.host.numel(), dtype=torch.uint8, device=self.device)
         self.A = _abi.arena_struct(arena, self.dev.data_ptr())
         self.opts = _abi.options(style, arena_bytes=arena_bytes, slots=slots,
-                                 threads_per_block=threads_per_block)
+                                 threads_per_block=threads_per_block, function_tree=1 if function_tree else 0)
         ws = C.c_size_t(0)
         with torch.cuda.device(self.device):  # sizing reads the device's SM count
             _lib.check(self.lib.upy_query_workspace(C.byref(self.A), C.byref(self.opts), C.byref(ws)),
@@ -172,7 +172,7 @@ def tree_sizes(arena: Arena, roots) -> tuple:
     return code, payload
 
 
-def run_arena(arena: Arena, style=None, device=None, retries=3) -> BatchResult:
+def run_arena(arena: Arena, style=None, device=None, retries=3, function_tree=False) -> BatchResult:
     """Decompile every root of a packed arena on the GPU.
 
     Roots that hit a device capacity limit (per-thread arena, output buffer) are
@@ -181,7 +181,7 @@ def run_arena(arena: Arena, style=None, device=None, retries=3) -> BatchResult:
     torch = _torch()
     dev = torch.device(device or "cuda")
     with torch.cuda.device(dev):
-        da = DeviceArena(arena, style, dev)
+        da = DeviceArena(arena, style, dev, function_tree=function_tree)
         da.upload()
         da.run()
         res = da.fetch()
@@ -201,7 +201,8 @@ def run_arena(arena: Arena, style=None, device=None, retries=3) -> BatchResult:
             if slots < 1:
                 break  # not even one slot fits: the statuses stay (DeviceCapacityError)
             sub = _subset(arena, redo)
-            db = DeviceArena(sub, style, dev, text_cap=text_cap, arena_bytes=slot_bytes, slots=slots)
+            db = DeviceArena(sub, style, dev, text_cap=text_cap, arena_bytes=slot_bytes, slots=slots,
+                             function_tree=function_tree)
             db.upload()
             db.run()
             r2 = db.fetch()
@@ -231,7 +232,7 @@ def _subset(arena: Arena, idx) -> Arena:
     return Arena(blob, dict(arena.offsets), counts, arena.max_code_len, arena.total_code_units)
 
 
-def decompile_many(codes, style=None, device=None, devices=None):
+def decompile_many(codes, style=None, device=None, devices=None, function_tree=False):
     """Batched decompile_source: one entry per input, text or the exception
     instance the reference would raise (the batch keeps going, like the CLI).
 
@@ -239,15 +240,17 @@ def decompile_many(codes, style=None, device=None, devices=None):
     ranges balanced by code bytes (shard.shard_bounds), one packed arena and
     one host thread per device, results gathered back in input order.  There
     is no cross-device traffic: every root (with its nested codes) is
-    decompiled on one device."""
+    decompiled on one device.  function_tree=True renders each input as
+    emit_module([function_tree(code)]) without validation (the reference CLI's
+    --function path, cli.py:75-78) instead of decompile_source."""
     codes = list(codes)
     if not codes:
         return []
     if devices is not None and len(devices) > 1:
-        return _decompile_sharded(codes, style, list(devices))
+        return _decompile_sharded(codes, style, list(devices), function_tree)
     if devices:
         device = devices[0]
-    res = run_arena(pack(codes), style, device)
+    res = run_arena(pack(codes), style, device, function_tree=function_tree)
     return _values(res)
 
 
@@ -281,7 +284,7 @@ def shard_plan(codes, n_devices):
     return shard_bounds([tree_code(co, set()) for co in codes], n_devices)
 
 
-def _decompile_sharded(codes, style, devices):
+def _decompile_sharded(codes, style, devices, function_tree=False):
     from concurrent.futures import ThreadPoolExecutor
 
     plan = shard_plan(codes, len(devices))
@@ -290,7 +293,7 @@ def _decompile_sharded(codes, style, devices):
         lo, hi = plan[k]
         if lo == hi:
             return []
-        return _values(run_arena(pack(codes[lo:hi]), style, devices[k]))
+        return _values(run_arena(pack(codes[lo:hi]), style, devices[k], function_tree=function_tree))
 
     with ThreadPoolExecutor(len(devices)) as ex:
         parts = list(ex.map(work, range(len(devices))))

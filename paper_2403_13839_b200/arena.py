@@ -168,9 +168,9 @@ class _Packer:
         self.codes.append(bytes(co.code))
         self.excs.append(bytes(co.exceptiontable or b""))
         self.lnts.append(bytes(co.linetable or b""))
-        for f in ("argcount", "posonlyargcount", "kwonlyargcount", "nlocals", "stacksize", "flags",
-                  "firstlineno"):
-            row[f] = int(getattr(co, f))
+        for f in ("argcount", "posonlyargcount", "kwonlyargcount", "nlocals", "stacksize", "firstlineno"):
+            row[f] = _clamp(int(getattr(co, f)))
+        row["flags"] = _flags62(int(co.flags))
         row["minor"] = int(co.version.minor)
         ids = [self.const(c) for c in co.consts]
         row["consts_off"], row["n_consts"] = len(self.refs), len(ids)
@@ -181,6 +181,24 @@ class _Packer:
         row["filename"] = self.sid(co.filename)
         row["qualname"] = self.sid(co.qualname or co.name)
         return idx
+
+
+# Python ints of any size fit the device's int64 fields this way (.pyc inputs are
+# 32-bit anyway): counts and sizes saturate at +-2**62, so sums of two and
+# stacksize + 6 cannot overflow and every comparison the reference makes
+# (validation, depth guard, parameter slicing) keeps its verdict; flags keep their
+# low 62 bits (the CO_* tests) and their sign.  Only validation messages that
+# print a count of magnitude >= 2**62 differ.
+_LIM = 1 << 62
+
+
+def _clamp(v):
+    return _LIM if v > _LIM else -_LIM if v < -_LIM else v
+
+
+def _flags62(v):
+    low = v & (_LIM - 1)
+    return low if v >= 0 else low - _LIM
 
 
 def _align(x, a):

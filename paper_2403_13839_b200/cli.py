@@ -114,7 +114,7 @@ def _decompile_loaded(loaded, style, function=None):
                 jobs.append((k, flat[function]))
             else:
                 jobs.append((k, root))
-    vals = api.decompile_many([c for _, c in jobs], style) if jobs else []
+    vals = api.decompile_many([c for _, c in jobs], style, function_tree=bool(function)) if jobs else []
     pyc_k = [k for k, ld in enumerate(loaded) if ld.pyc is not None]
     pyc_vals = loader.decompile_pyc_many([loaded[k].pyc for k in pyc_k], style) if pyc_k else []
     texts = {k: [] for k in range(len(loaded))}

@@ -7,6 +7,7 @@
 
 struct EmitOpts {
   bool header;
+  bool function_tree;  // CLI --function (cli.py:75-78): no validation, always a def
   Str indent;
   Str tool;
 };
@@ -116,9 +117,9 @@ struct Validator {
 };
 
 // function_tree / module_tree (pipeline.py:121-140) around a decompiled body
-HD NOINL NV* root_tree_of(Dc* C, u32 oi, NV* body) {
+HD NOINL NV* root_tree_of(Dc* C, u32 oi, NV* body, bool function_tree = false) {
   CKR(C, nullptr);
-  if (s_eqc(obj_name(C, oi), "<module>")) {
+  if (!function_tree && s_eqc(obj_name(C, oi), "<module>")) {
     if (body->n && is_k(body->d[0], S_ASSIGN)) {
       Node* first = body->d[0];
       if (first->l1->n == 1 && is_k(first->l1->d[0], E_NAME) && s_eqc(first->l1->d[0]->s, "__doc__") &&
@@ -203,7 +204,9 @@ HD NOINL void ds_emit(Dc* C, SourceJob* S) {
 HD inline void ds_stage(Dc* C, SourceJob* S, int stage) {
   if (C->err) return;
   switch (stage) {
-    case DS_VALIDATE: ds_validate(C, S); return;
+    case DS_VALIDATE:
+      if (!S->opt->function_tree) ds_validate(C, S);
+      return;
     case DS_ANALYZE:
       S->body.oi = S->oi;
       if (++C->depth > C->max_depth) fail_msg(C, UPY_ST_DEPTH_LIMIT, "device recursion guard");
@@ -213,7 +216,7 @@ HD inline void ds_stage(Dc* C, SourceJob* S, int stage) {
     case DS_FINISH:
       if (body_finish(C, &S->body)) {
         C->depth--;
-        S->tree = root_tree_of(C, S->oi, S->body.stmts);
+        S->tree = root_tree_of(C, S->oi, S->body.stmts, S->opt->function_tree);
       }
       return;
     case DS_EMIT: ds_emit(C, S); return;

@@ -493,16 +493,18 @@ struct Parser {
 
   const u8* bytes_ptr(i32 v) { return (vals[v].in_code ? T->code.data() : T->rest.data()) + vals[v].off; }
   // co_code payloads live in the code region (16-B aligned segments at the front
-  // of the bytes section).  The payload was just appended to rest, so it moves
-  // instead of being copied (a back-reference to an earlier bytes object is
-  // copied; one to an earlier co_code is shared).
-  i32 to_code_region(i32 v) {
+  // of the bytes section).  A payload this read just appended to rest moves
+  // instead of being copied; a back-reference to an earlier bytes object (a
+  // constant, a line table, ... whose rest offset is already recorded) is
+  // copied, and one to an earlier co_code is shared.  `fresh` = the first value
+  // index created by the read that produced v.
+  i32 to_code_region(i32 v, i32 fresh) {
     Val& x = vals[v];
     if (x.in_code) return v;
     u64 off = T->code.size();
     T->code.insert(T->code.end(), T->rest.begin() + x.off, T->rest.begin() + x.off + x.n);
     T->code.resize((T->code.size() + 15) & ~(size_t)15, 0);
-    if (x.off + x.n == T->rest.size()) {
+    if (v >= fresh && x.off + x.n == T->rest.size()) {
       T->rest.resize(x.off);
       x.in_code = 1;
       x.off = off;
@@ -533,7 +535,8 @@ struct Parser {
     if (minor <= 10) o.nlocals = i32_();
     o.stacksize = i32_();
     o.flags = i32_();
-    i32 code = to_code_region(expect(read_object(), UPY_C_BYTES));
+    const i32 fresh = (i32)vals.size();
+    i32 code = to_code_region(expect(read_object(), UPY_C_BYTES), fresh);
     i32 consts = expect(read_object(), UPY_C_TUPLE);
     std::vector<i32> names, varnames, freevars, cellvars, lp;
     expect_str_tuple(read_object(), &names);

@@ -42,6 +42,7 @@ struct KParams {
   char indent[64];
   char tool[64];
   int lane_stride;  // 1: every thread takes roots; 32: one root-taking thread per warp
+  int function_tree;
 };
 
 #ifndef UPY_MINB
@@ -112,6 +113,7 @@ __global__ void __launch_bounds__(128, UPY_MINB) upy_decompile_kernel(KParams P)
   u8* base = P.slots_base + slot * P.slot_bytes;
   EmitOpts opt;
   opt.header = P.header != 0;
+  opt.function_tree = P.function_tree != 0;
   opt.indent = Str{P.indent_len <= 64 ? P.indent : P.indent_ptr, (u32)P.indent_len};
   opt.tool = Str{P.tool_len <= 64 ? P.tool : P.tool_ptr, (u32)P.tool_len};
 #ifndef UPY_DC_SHARED
@@ -306,6 +308,7 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
   P.indent_len = opt && opt->indent ? opt->indent_len : 4;
   P.tool_len = opt && opt->tool ? opt->tool_len : 6;
   P.header = opt ? opt->header : 0;
+  P.function_tree = opt ? opt->function_tree : 0;
   u8* style_ws = ws + L.style_off;
   if (P.indent_len <= 64) {
     memcpy(P.indent, ind, P.indent_len);

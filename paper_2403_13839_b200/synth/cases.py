@@ -24,6 +24,8 @@ def build(spec):
         from . import fuzz
 
         return fuzz.program(spec["seed"], m, **kw)
+    if g == "shared_bytes":
+        return corpus.shared_bytes(m)
     if g == "c2":
         # compiled from the reference's corpus sources in the build container
         # (tests/golden/make_c2_golden.py); the fixture carries the tree

@@ -298,3 +298,37 @@ def _try311(g, depth, block):
     depth_stack = 0
     a.exc.append((s, e, h, depth_stack, False))
     a.exc.append((h, cl, cl, depth_stack + 1, True))
+
+
+def shared_bytes(minor=10):
+    """A module whose second function's co_code equals a bytes constant and the
+    line table of the first (`def f(): return <bytes>` / `def g(): return None`),
+    so a marshal writer that shares equal bytes objects emits g's co_code as an
+    'r' back-reference to f's objects (the loader must not move that payload)."""
+    def fn(name, value):
+        a = Asm(minor)
+        a.const(None)
+        if minor >= 11:
+            a("RESUME", 0)
+        a("LOAD_CONST", a.const(value, "bytes") if value is not None else 0)
+        a("RETURN_VALUE")
+        return a.build(name)
+
+    import dataclasses
+
+    g = fn("g", None)
+    f = fn("f", bytes(g.code))
+    # f's line table (the last bytes object written for f) equals g's code too
+    f = dataclasses.replace(f, linetable=bytes(g.code))
+    m = Asm(minor)
+    if minor >= 11:
+        m("RESUME", 0)
+    for co in (f, g):
+        m("LOAD_CONST", m.const(co, "code"))
+        if minor <= 10:
+            m("LOAD_CONST", m.const(co.name))
+        m("MAKE_FUNCTION", 0)
+        m("STORE_NAME", m.name(co.name))
+    m("LOAD_CONST", m.const(None))
+    m("RETURN_VALUE")
+    return m.build("<module>", flags=0x40)

@@ -19,8 +19,10 @@ FLAG_REF = 0x80
 
 
 class _W:
-    def __init__(self, minor, refs=True, long_tuples=False, unicode_all=False):
+    def __init__(self, minor, refs=True, long_tuples=False, unicode_all=False, share_bytes=False):
         self.minor = minor
+        self.share_bytes = share_bytes  # equal bytes objects written once, then as 'r' back-references
+        self.bytes_refs = {}
         self.out = bytearray()
         self.use_refs = refs
         self.long_tuples = long_tuples
@@ -124,9 +126,18 @@ class _W:
                 self.const(x)
 
     def bytes_(self, b):
-        self.b(b"s")
+        b = bytes(b)
+        if self.share_bytes:
+            if b in self.bytes_refs:
+                self.b(b"r")
+                self.i32(self.bytes_refs[b])
+                return
+            self.bytes_refs[b] = self._new_ref()
+            self.b(bytes([ord("s") | FLAG_REF]))
+        else:
+            self.b(b"s")
         self.i32(len(b))
-        self.b(bytes(b))
+        self.b(b)
 
     def code(self, co):
         flag = FLAG_REF if self.use_refs else 0

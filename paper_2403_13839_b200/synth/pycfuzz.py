@@ -15,7 +15,10 @@ import struct
 
 from . import cases, marshal
 
-ENCODINGS = ({}, {"refs": False}, {"long_tuples": True, "unicode_all": True})
+ENCODINGS = ({}, {"refs": False}, {"long_tuples": True, "unicode_all": True},
+             # equal bytes objects shared by back-reference (co_code, line tables and
+             # bytes constants of different code objects alias one marshal object)
+             {"share_bytes": True})
 
 JUNK = (b"f\x031.5", b"f\x02xx", b"f\x041_00", b"f\x03inf", b"f\x05 -2e3", b"f\x04+nan", b"f\x021_",
         b"l\x02\x00\x00\x00\xff\xff\x00\x00", b"l\xfe\xff\xff\xff\x01\x00\x02\x00", b"l\x00\x00\x00\x00",
@@ -91,6 +94,7 @@ def corpus(n_valid_per_set=24, n_mutants=600, seed=0x9C):
     specs = []
     for name in ("c1", "snippets", "fuzz", "c3"):
         specs += cases.GOLDEN_SETS[name][:n_valid_per_set]
+    specs += [{"case": f"shared-bytes-3.{m}", "gen": "shared_bytes", "minor": m} for m in (8, 9, 10, 11)]
     out = []
     for i, spec in enumerate(specs):
         for e in range(len(ENCODINGS)):

@@ -84,6 +84,17 @@ def main():
         "badver.json": json.dumps({"format_version": 1, "python_version": [3, 12], "root": {}}).encode(),
     }
     names = [n for n, _ in trees]
+    # a module whose nested `f` fails validation (stacksize < 0): plain decompile
+    # reports it, --function decompiles f without validating (cli.py:75-78)
+    import dataclasses
+
+    from paper_2403_13839_b200.model import Const
+    from paper_2403_13839_b200.synth import corpus as synth_corpus
+
+    mod = synth_corpus.shared_bytes(10)
+    f_code = dataclasses.replace(mod.consts[0].value, stacksize=-1)
+    invalid = {"invalid.pyc": marshal.dump_pyc(dataclasses.replace(
+        mod, consts=(Const("code", f_code),) + tuple(mod.consts[1:])))}
     cases = [
         ("pyc-all", pyc, ["decompile", *pyc]),
         ("json-all-noheader", js, ["decompile", "--no-header", *js]),
@@ -93,6 +104,9 @@ def main():
         ("out-dir", pyc, ["decompile", "--out", "outdir", *list(pyc)[:4]]),
         ("function", pyc, ["decompile", "--function", "<module>.outer.middle", f"{names[4]}.pyc"]),
         ("function-missing", pyc, ["decompile", "--function", "nope", f"{names[0]}.pyc", f"{names[1]}.pyc"]),
+        ("function-module", pyc, ["decompile", "--function", "<module>", f"{names[6]}.pyc", f"{names[8]}.pyc"]),
+        ("invalid-nested", invalid, ["decompile", "invalid.pyc"]),
+        ("function-invalid-nested", invalid, ["decompile", "--function", "<module>.f", "invalid.pyc"]),
         ("version-override", js, ["decompile", "--version-override", "3.10", *list(js)[:2]]),
         ("version-override-bad", js, ["decompile", "--version-override", "3.x", *list(js)[:2]]),
         ("usage", {}, ["decompile"]),

@@ -99,3 +99,28 @@ def test_json_dump_reader_matches_reference_on_schema_mutants():
         if got != (rec["status"], rec["text"]):
             bad.append((rec["base"], rec["seed"], rec["status"], rec["text"], got))
     assert not bad, bad[:3]
+
+
+@pytest.mark.parametrize("case", ["function", "function-module", "invalid-nested", "function-invalid-nested"])
+def test_cli_function_path_host_build(tmp_path, case, monkeypatch):
+    """--function renders emit_module([function_tree(target)]) with no
+    validation (cli.py:75-78), also for '<module>' and for nested code that fails
+    validation: CPU tier with the host build of the device sources standing in
+    for the device batch."""
+    from paper_2403_13839_b200 import api, hostcheck
+
+    rec = next(r for r in load_golden("cli") if r["case"] == case)
+    if not any(a.endswith(".pyc") for a in rec["argv"]):
+        pytest.skip("no inputs")
+    monkeypatch.setattr(api, "decompile_many", lambda codes, style=None, function_tree=False, **kw:
+                        hostcheck.decompile_many(codes, style, function_tree=function_tree))
+    from paper_2403_13839_b200 import arena, loader
+
+    def pyc_many(blobs, style=None, **kw):
+        ar, per = loader.load_pyc_batch(blobs)
+        objs = arena.unpack(ar)
+        return [v if isinstance(v, BaseException) else hostcheck.decompile_many([objs[v]], style)[0] for v in per]
+
+    monkeypatch.setattr(loader, "decompile_pyc_many", pyc_many)
+    rc, out, err, produced = _run(tmp_path, rec)
+    assert (rc, out, err) == (rec["rc"], rec["stdout"], rec["stderr"])

@@ -13,7 +13,7 @@
 extern "C" int upyh_decompile(const upy_arena* A, int header, const char* indent, int indent_len, const char* tool,
                               int tool_len, uint64_t arena_bytes, uint8_t* text, uint64_t text_cap,
                               uint64_t* text_off, uint32_t* text_len, int32_t* status, int64_t* aux,
-                              upy_decoded* dec_out) {
+                              upy_decoded* dec_out, int function_tree) {
   std::vector<upy_ins> ins(A->total_code_units + 1);
   std::vector<upy_decoded> dec(A->n_objs);
   for (int64_t o = 0; o < A->n_objs; o++) {
@@ -26,6 +26,7 @@ extern "C" int upyh_decompile(const upy_arena* A, int header, const char* indent
   std::vector<uint8_t> sink(SINK_BYTES);
   EmitOpts opt;
   opt.header = header != 0;
+  opt.function_tree = function_tree != 0;
   opt.indent = Str{indent, (u32)indent_len};
   opt.tool = Str{tool, (u32)tool_len};
   uint64_t used = 0;
