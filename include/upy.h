@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define UPY_ABI_VERSION 2
+#define UPY_ABI_VERSION 3
 
 /* Const kinds (code_model.py:56-59). */
 enum {
@@ -93,6 +93,9 @@ typedef struct {
   int32_t function_tree;     /* 1: emit_module([function_tree(root)]) without validation -- the
                                 reference CLI's --function path (cli.py:75-78) -- instead of
                                 decompile_source */
+  int32_t output;            /* 0: source text (above); 1: the CFG export of `unpyre disasm --cfg --dot`
+                                (cli.py:103-105): to_dot(analyze(root)[2]) (cfg.py:331-344,
+                                pipeline.py:17-54) per root, no validation */
 } upy_options;
 
 /* Per-root results (device pointers, caller-allocated). */

@@ -34,6 +34,7 @@ class UpyOptions(C.Structure):
         ("schedule", C.c_int32),
         ("max_depth", C.c_int32),
         ("function_tree", C.c_int32),
+        ("output", C.c_int32),
     ]
 
 

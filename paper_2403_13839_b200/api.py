@@ -59,7 +59,7 @@ class DeviceArena:
     `run()` on HBM-resident inputs and `upload()+run()+fetch()` end to end)."""
 
     def __init__(self, arena: Arena, style=None, device=None, text_cap=None, arena_bytes=0, slots=0,
-                 threads_per_block=0, pinned=None, function_tree=False):
+                 threads_per_block=0, pinned=None, function_tree=False, output=0):
         torch = _torch()
         self.torch = torch
         self.lib = _lib.load()
@@ -73,7 +73,8 @@ class DeviceArena:
         self.dev = torch.empty(self.host.numel(), dtype=torch.uint8, device=self.device)
         self.A = _abi.arena_struct(arena, self.dev.data_ptr())
         self.opts = _abi.options(style, arena_bytes=arena_bytes, slots=slots,
-                                 threads_per_block=threads_per_block, function_tree=1 if function_tree else 0)
+                                 threads_per_block=threads_per_block, function_tree=1 if function_tree else 0,
+                                 output=output)
         ws = C.c_size_t(0)
         with torch.cuda.device(self.device):  # sizing reads the device's SM count
             _lib.check(self.lib.upy_query_workspace(C.byref(self.A), C.byref(self.opts), C.byref(ws)),
@@ -81,7 +82,9 @@ class DeviceArena:
         self.ws_bytes = ws.value
         self.ws = torch.empty(max(self.ws_bytes, 256), dtype=torch.uint8, device=self.device)
         n = max(arena.n_roots, 1)
-        cap = text_cap or max(1 << 16, 8 * arena.code_bytes + 512 * arena.n_roots)
+        # source text is ~1.5-4.5x co_code; the CFG export lists every instruction (~12x)
+        per_byte, per_root = (8, 512) if output == 0 else (32, 1024)
+        cap = text_cap or max(1 << 16, per_byte * arena.code_bytes + per_root * arena.n_roots)
         self.text = torch.empty(cap, dtype=torch.uint8, device=self.device)
         # meta layout: [used u64 | pad][off u64 n][aux i64 2n][len u32 n][status i32 n]
         self.out = _abi.UpyOut()
@@ -172,16 +175,17 @@ def tree_sizes(arena: Arena, roots) -> tuple:
     return code, payload
 
 
-def run_arena(arena: Arena, style=None, device=None, retries=3, function_tree=False) -> BatchResult:
+def run_arena(arena: Arena, style=None, device=None, retries=3, function_tree=False, output=0) -> BatchResult:
     """Decompile every root of a packed arena on the GPU.
 
     Roots that hit a device capacity limit (per-thread arena, output buffer) are
     re-run on the device with 4x larger limits per attempt, sized from the
-    retried roots' own trees and capped by the device's free memory."""
+    retried roots' own trees and capped by the device's free memory.  output=1
+    writes each root's CFG export (to_dot, csrc/dot.h) instead of its source."""
     torch = _torch()
     dev = torch.device(device or "cuda")
     with torch.cuda.device(dev):
-        da = DeviceArena(arena, style, dev, function_tree=function_tree)
+        da = DeviceArena(arena, style, dev, function_tree=function_tree, output=output)
         da.upload()
         da.run()
         res = da.fetch()
@@ -202,7 +206,7 @@ def run_arena(arena: Arena, style=None, device=None, retries=3, function_tree=Fa
                 break  # not even one slot fits: the statuses stay (DeviceCapacityError)
             sub = _subset(arena, redo)
             db = DeviceArena(sub, style, dev, text_cap=text_cap, arena_bytes=slot_bytes, slots=slots,
-                             function_tree=function_tree)
+                             function_tree=function_tree, output=output)
             db.upload()
             db.run()
             r2 = db.fetch()
@@ -220,16 +224,9 @@ def run_arena(arena: Arena, style=None, device=None, retries=3, function_tree=Fa
 
 def _subset(arena: Arena, idx) -> Arena:
     """Same objects, roots restricted to positions `idx` (a new roots section)."""
-    roots = arena.section("roots")[idx].copy()
-    blob = arena.blob.copy()
-    off = arena.offsets["roots"]
-    need = off + roots.nbytes
-    if need > len(blob):
-        blob = np.concatenate([blob, np.zeros(need - len(blob), np.uint8)])
-    blob[off:off + roots.nbytes] = roots.view(np.uint8)
-    counts = dict(arena.counts)
-    counts["roots"] = len(roots)
-    return Arena(blob, dict(arena.offsets), counts, arena.max_code_len, arena.total_code_units)
+    from .arena import with_roots
+
+    return with_roots(arena, arena.section("roots")[idx])
 
 
 def decompile_many(codes, style=None, device=None, devices=None, function_tree=False):

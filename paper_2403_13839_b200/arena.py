@@ -406,6 +406,21 @@ def tile(arena: Arena, reps: int) -> Arena:
     return out
 
 
+def with_roots(arena: Arena, objects) -> Arena:
+    """Same objects and pools, roots = the given object indices (a new roots
+    section; roots is the last section, so the blob only grows at its end)."""
+    roots = np.asarray(objects, dtype="<i4")
+    blob = arena.blob.copy()
+    off = arena.offsets["roots"]
+    need = off + roots.nbytes
+    if need > len(blob):
+        blob = np.concatenate([blob, np.zeros(need - len(blob), np.uint8)])
+    blob[off:off + roots.nbytes] = roots.view(np.uint8)
+    counts = dict(arena.counts)
+    counts["roots"] = len(roots)
+    return Arena(blob, dict(arena.offsets), counts, arena.max_code_len, arena.total_code_units)
+
+
 def from_blob(blob, header):
     """Arena from a raw blob + the header dict written by the synthetic generator."""
     offsets = {s: int(header["off_" + s]) for s in SECTIONS}

@@ -3,6 +3,7 @@
     python -m paper_2403_13839_b200 decompile FILE... [--out DIR] [--function QUALNAME]
                                               [--version-override 3.X] [--no-header]
     python -m paper_2403_13839_b200 verify CORPUS_DIR [--json-report]
+    python -m paper_2403_13839_b200 disasm FILE [--cfg] [--dot] [--version-override 3.X]
 
 Restates the reference CLI's `decompile` and `verify` commands
 (/root/reference/pkg/src/unpyre/cli.py:54-174, parser :177-217) with the same
@@ -14,8 +15,9 @@ jsondump.py) and all roots go to the device in ONE decompile_many batch.
 Diagnostics are then emitted in input order, so the output matches the
 serial reference byte for byte (verify's elapsed-time line aside).
 
-`disasm` (a text listing / Graphviz CFG) is not part of this
-build: it exits 2 with a message.
+`disasm` (cli.py:95-116) prints the instruction listing of every
+code object from the decode kernel's records, or with --cfg --dot the Graphviz
+CFG written by the device (csrc/dot.h).
 """
 from __future__ import annotations
 
@@ -239,8 +241,35 @@ def cmd_verify(args) -> int:
 
 
 def cmd_disasm(args) -> int:
-    _diag("disasm: instruction listings / CFG export are not part of the GPU build (SURVEY.md §8 f4)")
-    return 2
+    """cli.py:95-116: an instruction listing per code object (flatten order), or
+    with --cfg --dot the CFG export.  All code objects of the input go to the
+    device in one batch (decode kernel for listings, the CFG kernel for dot);
+    output and the first error are then reported in reference order."""
+    from . import disasm
+
+    path = Path(args.input)
+    if not path.exists():
+        _diag(f"{args.input}: no such file")
+        return 2
+    try:
+        override = _parse_version(args.version_override) if args.version_override else None
+        ld = _load_all([(args.input, path, path.read_bytes())], override, want_objects=True)[0]
+        if ld.error is not None:
+            raise ld.error
+        flat = [qc for root in ld.roots for qc in flatten_nested_codes(root)]
+        dot = args.cfg and args.dot
+        codes = [c for _, c in flat]
+        results = disasm.to_dot_many(codes) if dot else disasm.decode_many(codes)
+        for (qualname, _code), v in zip(flat, results):
+            if not dot:
+                print(f"-- {qualname}")
+            if isinstance(v, BaseException):
+                raise v
+            sys.stdout.write(v if dot else disasm.format_listing(v))
+    except errors.UnpyreError as exc:
+        _diag(f"{args.input}: {type(exc).__name__}: {exc}")
+        return 1
+    return 0
 
 
 def build_parser():

@@ -223,10 +223,23 @@ HD inline void ds_stage(Dc* C, SourceJob* S, int stage) {
   }
 }
 
+#if defined(UPY_PHASE_PROF) && defined(__CUDACC__)
+// Profiling variant (tools/build_variant.sh prof -DUPY_PHASE_PROF): thread-cycles
+// per stage summed over all roots, read back with upy_prof_read.
+__device__ unsigned long long g_stage_cycles[DS_STAGES];
+#endif
 HD inline void decompile_source(Dc* C, u32 oi, const EmitOpts* opt, Text* out) {
   SourceJob S;
   S.oi = oi;
   S.opt = opt;
   S.out = out;
-  for (int st = 0; st < DS_STAGES; st++) ds_stage(C, &S, st);
+  for (int st = 0; st < DS_STAGES; st++) {
+#if defined(UPY_PHASE_PROF) && defined(__CUDA_ARCH__)
+    long long t0 = clock64();
+    ds_stage(C, &S, st);
+    atomicAdd(&g_stage_cycles[st], (unsigned long long)(clock64() - t0));
+#else
+    ds_stage(C, &S, st);
+#endif
+  }
 }

@@ -11,6 +11,7 @@
 #include <stdio.h>
 #include <mutex>
 #include "pipeline.h"
+#include "dot.h"
 
 // decode_kernel.cu
 cudaError_t upy_decode_launch(const upy_arena* arena, upy_ins* ins, upy_decoded* dec, cudaStream_t s, int sms);
@@ -43,6 +44,7 @@ struct KParams {
   char tool[64];
   int lane_stride;  // 1: every thread takes roots; 32: one root-taking thread per warp
   int function_tree;
+  int output;       // upy_options.output: 0 source text, 1 CFG dot export
 };
 
 #ifndef UPY_MINB
@@ -134,6 +136,24 @@ __global__ void __launch_bounds__(128, UPY_MINB) upy_decompile_kernel(KParams P)
     dc_reset(C, P, base);
     Text out = {nullptr, 0, 0};
     decompile_source(&C, (u32)P.A.roots[r], &opt, &out);
+    emit_result(P, C, r, out);
+  }
+}
+
+// `unpyre disasm --cfg --dot` (cli.py:103-105): to_dot(analyze(root)) per root
+// (dot.h), same schedule and per-thread arena as the decompile kernel.
+__global__ void __launch_bounds__(128, UPY_MINB) upy_cfgdot_kernel(KParams P) {
+  if (P.lane_stride > 1 && (threadIdx.x & 31)) return;
+  const u64 slot = ((u64)blockIdx.x * blockDim.x + threadIdx.x) / (u64)P.lane_stride;
+  u8* base = P.slots_base + slot * P.slot_bytes;
+  Dc C;
+  const u64 n_roots = (u64)P.A.n_roots;
+  while (true) {
+    u32 r = atomicAdd(P.next_root, 1u);
+    if (r >= n_roots) break;
+    dc_reset(C, P, base);
+    Text out = {nullptr, 0, 0};
+    cfg_dot(&C, (u32)P.A.roots[r], &out);
     emit_result(P, C, r, out);
   }
 }
@@ -254,6 +274,10 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
     set_err("upy_decompile_batch: null argument");
     return 1;
   }
+  if (opt && (opt->output < 0 || opt->output > 1)) {
+    set_err("upy_decompile_batch: options.output must be 0 (source) or 1 (CFG dot)");
+    return 1;
+  }
   WsLayout L = layout(arena, opt);
   if (ws_bytes < L.total) {
     set_err("upy_decompile_batch: workspace too small");
@@ -283,6 +307,7 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
     if (!g_dev_cfg_done[dev]) {
       // no shared memory: give the whole L1/shared pool to L1 (arena + stack hit rate)
       cudaFuncSetAttribute(upy_decompile_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+      cudaFuncSetAttribute(upy_cfgdot_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
       cudaError_t e = cudaDeviceSetLimit(cudaLimitStackSize, 48 * 1024);
       if (e != cudaSuccess) {
         set_err("cudaDeviceSetLimit(stack): %s", cudaGetErrorString(e));
@@ -309,6 +334,7 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
   P.tool_len = opt && opt->tool ? opt->tool_len : 6;
   P.header = opt ? opt->header : 0;
   P.function_tree = opt ? opt->function_tree : 0;
+  P.output = opt ? opt->output : 0;
   u8* style_ws = ws + L.style_off;
   if (P.indent_len <= 64) {
     memcpy(P.indent, ind, P.indent_len);
@@ -326,7 +352,8 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
   P.lane_stride = L.lane_stride;
   int tpb = eff_tpb(opt);
   unsigned blocks = (unsigned)(L.slots * L.lane_stride / tpb);
-  upy_decompile_kernel<<<blocks, tpb, 0, s>>>(P);
+  if (P.output == 1) upy_cfgdot_kernel<<<blocks, tpb, 0, s>>>(P);
+  else upy_decompile_kernel<<<blocks, tpb, 0, s>>>(P);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_err("decompile launch: %s", cudaGetErrorString(e));
@@ -335,4 +362,15 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
   return 0;
 }
 
+#ifdef UPY_PHASE_PROF
+int upy_prof_read(unsigned long long* host, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(host, g_stage_cycles, sizeof(g_stage_cycles));
+  if (reset) {
+    unsigned long long z[DS_STAGES] = {};
+    cudaMemcpyToSymbol(g_stage_cycles, z, sizeof z);
+  }
+  return DS_STAGES;
+}
+#endif
 }  // extern "C"

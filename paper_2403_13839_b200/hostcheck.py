@@ -42,7 +42,7 @@ def lib():
     return _lib
 
 
-def run(arena, style=None, arena_bytes=256 << 20, text_cap=None, function_tree=False):
+def run(arena, style=None, arena_bytes=256 << 20, text_cap=None, function_tree=False, output=0):
     """Decompile every root of `arena` on the host; returns list of (status, text, aux)."""
     L = lib()
     blob = arena.blob
@@ -62,7 +62,7 @@ def run(arena, style=None, arena_bytes=256 << 20, text_cap=None, function_tree=F
     L.upyh_decompile(C.byref(A), header, indent, len(indent), tool, len(tool), C.c_uint64(arena_bytes),
                      text.ctypes.data_as(C.c_void_p), C.c_uint64(cap), off.ctypes.data_as(C.c_void_p),
                      ln.ctypes.data_as(C.c_void_p), st.ctypes.data_as(C.c_void_p),
-                     aux.ctypes.data_as(C.c_void_p), dec.ctypes.data_as(C.c_void_p), 1 if function_tree else 0)
+                     aux.ctypes.data_as(C.c_void_p), dec.ctypes.data_as(C.c_void_p), 1 if function_tree else 0, output)
     out = []
     tb = text.tobytes()
     for i in range(n):

@@ -37,11 +37,11 @@ MODS = ["classes/class_inherit_kw", "comprehensions/nested_listcomp", "control/f
         "functions/lambda_uses"]
 
 
-def _trees():
+def _trees(minor=10):
     with open(os.path.join(HERE, "c2.jsonl")) as f:
         recs = [json.loads(line) for line in f]
-    by = {r["case"][len("c2-3.10-"):]: codejson.from_json(r["tree"]) for r in recs
-          if not r.get("style") and r["minor"] == 10}
+    by = {r["case"][len(f"c2-3.{minor}-"):]: codejson.from_json(r["tree"]) for r in recs
+          if not r.get("style") and r["minor"] == minor}
     return [(m.split("/")[1], by[m]) for m in MODS]
 
 
@@ -110,6 +110,31 @@ def main():
         ("version-override", js, ["decompile", "--version-override", "3.10", *list(js)[:2]]),
         ("version-override-bad", js, ["decompile", "--version-override", "3.x", *list(js)[:2]]),
         ("usage", {}, ["decompile"]),
+    ]
+    # disasm (cli.py:95-116): listings and the --cfg --dot export, incl. 3.11
+    # (exception tables), a code error inside a nested code object, bad inputs
+    by311 = _trees(11)
+    pyc311 = {f"{n}_311.pyc": marshal.dump_pyc(co) for n, co in by311}
+    broken = {"brokennested.pyc": marshal.dump_pyc(dataclasses.replace(
+        mod, consts=(Const("code", dataclasses.replace(mod.consts[0].value, code=b"\x00\x00")),)
+        + tuple(mod.consts[1:])))}
+    cases += [
+        ("disasm-pyc", pyc, ["disasm", f"{names[4]}.pyc"]),
+        ("disasm-json", js, ["disasm", f"{names[0]}.json"]),
+        ("disasm-cfg-dot", pyc, ["disasm", "--cfg", "--dot", f"{names[3]}.pyc"]),
+        ("disasm-cfg-dot-loops", pyc, ["disasm", "--cfg", "--dot", f"{names[2]}.pyc"]),
+        ("disasm-cfg-only", pyc, ["disasm", "--cfg", f"{names[1]}.pyc"]),
+        ("disasm-dot-only", pyc, ["disasm", "--dot", f"{names[7]}.pyc"]),
+        ("disasm-311", pyc311, ["disasm", f"{by311[3][0]}_311.pyc"]),
+        ("disasm-311-dot", pyc311, ["disasm", "--cfg", "--dot", f"{by311[3][0]}_311.pyc"]),
+        ("disasm-311-dot-gen", pyc311, ["disasm", "--cfg", "--dot", f"{by311[5][0]}_311.pyc"]),
+        ("disasm-nested-error", broken, ["disasm", "brokennested.pyc"]),
+        ("disasm-nested-error-dot", broken, ["disasm", "--cfg", "--dot", "brokennested.pyc"]),
+        ("disasm-bad-pyc", bad, ["disasm", "trunc.pyc"]),
+        ("disasm-schema", bad, ["disasm", "schema.json"]),
+        ("disasm-missing", {}, ["disasm", "nothere.pyc"]),
+        ("disasm-version-override", js, ["disasm", "--version-override", "3.10", f"{names[5]}.json"]),
+        ("disasm-version-override-bad", js, ["disasm", "--version-override", "x", f"{names[5]}.json"]),
     ]
     # verify corpus: py310/<case>.json + <case>.expected.py
     corpus = {}

@@ -124,3 +124,39 @@ def test_cli_function_path_host_build(tmp_path, case, monkeypatch):
     monkeypatch.setattr(loader, "decompile_pyc_many", pyc_many)
     rc, out, err, produced = _run(tmp_path, rec)
     assert (rc, out, err) == (rec["rc"], rec["stdout"], rec["stderr"])
+
+
+def _host_backends(monkeypatch):
+    """disasm's two device calls served by the test-only host build of the same
+    sources (so the CLI's host logic runs on CPU)."""
+    from paper_2403_13839_b200 import arena, disasm, hostcheck
+    from paper_2403_13839_b200.errors import make_exception
+
+    def decode_many(codes, device=None):
+        ar = arena.pack(codes)
+        ins, dec = hostcheck.decode(ar)
+        objs, roots = ar.section("objs"), ar.section("roots")
+        out = []
+        for co, o in zip(codes, roots):
+            d = dec[int(o)]
+            if int(d["status"]):
+                out.append(disasm.decode_exception(co, int(d["status"]), int(d["aux0"]), int(d["aux1"])))
+            else:
+                base = int(objs[int(o)]["code_off"]) >> 1
+                out.append(disasm.instructions(co, ins[base:base + int(d["n_instrs"])]))
+        return out
+
+    def to_dot_many(codes, device=None):
+        ar = arena.pack(codes)
+        res = hostcheck.run(ar, output=1, text_cap=64 * ar.code_bytes + (1 << 20))
+        return [s if st == 0 else make_exception(st, s, aux) for st, s, aux in res]
+
+    monkeypatch.setattr(disasm, "decode_many", decode_many)
+    monkeypatch.setattr(disasm, "to_dot_many", to_dot_many)
+
+
+@pytest.mark.parametrize("rec", [r for r in load_golden("cli") if r["argv"][0] == "disasm"], ids=lambda r: r["case"])
+def test_disasm_cli_host_matches_reference_cli(tmp_path, monkeypatch, rec):
+    _host_backends(monkeypatch)
+    rc, out, err, produced = _run(tmp_path, rec)
+    assert (rc, out, err) == (rec["rc"], rec["stdout"], rec["stderr"])

@@ -74,7 +74,7 @@ def test_cuda_library_exports_every_declared_symbol():
         assert hasattr(lib, sym), sym
     _abi.check_layout(lib)
     lib.upy_abi_version.restype = ctypes.c_int
-    assert lib.upy_abi_version() == 2
+    assert lib.upy_abi_version() == 3
 
 
 def test_shard_bounds_partition_and_balance():

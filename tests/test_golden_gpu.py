@@ -42,3 +42,58 @@ def test_gpu_c2_from_pyc_images_matches_reference():
     recs = [r for r in golden_cases(["c2"]) if not r.get("style")]
     got = [outcome(v) for v in loader.decompile_pyc_many([marshal.dump_pyc(co) for co in inputs(recs)])]
     assert not mismatches(recs, got)
+
+
+THROUGHPUT_ROOTS = 148 * 32 + 1  # more roots than resident warps: every thread takes roots (upy.cu layout())
+
+
+@pytest.mark.parametrize("gset", ["c1", "c2", "c3", "c4", "snippets", "fuzz", "mutant", "mutant2"])
+def test_gpu_tiled_throughput_schedule_matches_reference(gset):
+    """The golden sets tiled past the small-batch threshold, so the kernel runs its
+    throughput schedule (32 root-taking threads per warp, divergent lanes) rather
+    than the one-thread-per-warp latency mode every untiled set above gets.  Every
+    tile's output is compared with the reference's text."""
+    import math
+
+    from paper_2403_13839_b200 import api, arena
+
+    recs = golden_cases([gset])
+    by_style = {}
+    for r in recs:
+        by_style.setdefault(repr(r.get("style")), []).append(r)
+    bad = []
+    for _, group in by_style.items():
+        base = arena.pack(inputs(group))
+        reps = math.ceil(THROUGHPUT_ROOTS / len(group))
+        res = api.run_arena(arena.tile(base, reps), style_of(group[0]))
+        assert len(res.status) == reps * len(group) >= THROUGHPUT_ROOTS
+        vals = res.values()
+        for t in range(reps):
+            got = [outcome(v) for v in vals[t * len(group):(t + 1) * len(group)]]
+            bad += [(t,) + b for b in mismatches(group, got)]
+    assert not bad, bad[:3]
+
+
+@pytest.mark.parametrize("pool,n", [("c4_310", 16), ("c4_311", 16)])
+def test_gpu_c4_10k_unit_pool_matches_reference_digests(pool, n):
+    """16 objects each of the 10K-unit C4 bench pools (3.10 and 3.11: nested
+    if/for/while/try, EXTENDED_ARG jumps, exception tables) against the SHA-256
+    of the reference's text (tests/golden/pools.json)."""
+    import hashlib
+    import json
+    import os
+
+    from conftest import GOLDEN
+    from paper_2403_13839_b200 import api
+    from paper_2403_13839_b200.bench_pools import pool_objects
+
+    with open(os.path.join(GOLDEN, "pools.json")) as f:
+        want = json.load(f)[pool]
+    codes = pool_objects(pool, 0, n)
+    assert sum(len(c.code) for c in codes) / n > 18000
+    got = api.decompile_many(codes)
+    for i, g in enumerate(got):
+        ok = isinstance(g, str)
+        assert ok == (want["status"][i] == "ok"), (i, g)
+        text = g if ok else str(g)
+        assert hashlib.sha256(text.encode("utf-8", "surrogatepass")).hexdigest()[:24] == want["sha"][i], i

@@ -9,11 +9,12 @@
 #include <vector>
 #include "../paper_2403_13839_b200/csrc/pipeline.h"
 #include "../paper_2403_13839_b200/csrc/decode.h"
+#include "../paper_2403_13839_b200/csrc/dot.h"
 
 extern "C" int upyh_decompile(const upy_arena* A, int header, const char* indent, int indent_len, const char* tool,
                               int tool_len, uint64_t arena_bytes, uint8_t* text, uint64_t text_cap,
                               uint64_t* text_off, uint32_t* text_len, int32_t* status, int64_t* aux,
-                              upy_decoded* dec_out, int function_tree) {
+                              upy_decoded* dec_out, int function_tree, int output) {
   std::vector<upy_ins> ins(A->total_code_units + 1);
   std::vector<upy_decoded> dec(A->n_objs);
   for (int64_t o = 0; o < A->n_objs; o++) {
@@ -51,7 +52,8 @@ extern "C" int upyh_decompile(const upy_arena* A, int header, const char* indent
     C.dec_all = dec.data();
     C.max_depth = 600;
     Text out = {nullptr, 0, 0};
-    decompile_source(&C, (u32)A->roots[r], &opt, &out);
+    if (output == 1) cfg_dot(&C, (u32)A->roots[r], &out);
+    else decompile_source(&C, (u32)A->roots[r], &opt, &out);
     const char* src = C.err ? C.msg : out.d;
     uint32_t len = C.err ? C.msg_len : out.n;
     int st = C.err;
@@ -78,6 +80,47 @@ extern "C" int upyh_decode(const upy_arena* A, upy_ins* ins_out, upy_decoded* de
   for (int64_t o = 0; o < A->n_objs; o++) {
     const upy_obj* ob = &A->objs[o];
     decode_scalar(A->bytes + ob->code_off, ob->code_len, (int)ob->minor, ins_out + (ob->code_off >> 1), &dec_out[o]);
+  }
+  return 0;
+}
+
+// Arena high-water mark per root (bump region + deepest scratch), for slot sizing.
+extern "C" int upyh_arena_peaks(const upy_arena* A, uint64_t arena_bytes, uint64_t* peak) {
+  std::vector<upy_ins> ins(A->total_code_units + 1);
+  std::vector<upy_decoded> dec(A->n_objs);
+  for (int64_t o = 0; o < A->n_objs; o++) {
+    const upy_obj* ob = &A->objs[o];
+    decode_scalar(A->bytes + ob->code_off, ob->code_len, (int)ob->minor, ins.data() + (ob->code_off >> 1), &dec[o]);
+  }
+  std::vector<uint8_t> slot(arena_bytes);
+  std::vector<char> msg(4096);
+  std::vector<uint8_t> sink(SINK_BYTES);
+  EmitOpts opt;
+  opt.header = false;
+  opt.function_tree = false;
+  opt.indent = Str{"    ", 4};
+  opt.tool = Str{"unpyre", 6};
+  for (int64_t r = 0; r < A->n_roots; r++) {
+    Dc C;
+    memset(&C, 0, sizeof C);
+    C.base = slot.data();
+    C.cap = C.top = C.low_top = arena_bytes;
+    C.sink = sink.data();
+    C.msg = msg.data();
+    C.msg_cap = 4096;
+    C.A = A;
+    C.objs = A->objs;
+    C.consts = A->consts;
+    C.strs = A->strs;
+    C.refs = A->refs;
+    C.limbs = A->limbs;
+    C.bytes = A->bytes;
+    C.ins_all = ins.data();
+    C.dec_all = dec.data();
+    C.max_depth = 600;
+    Text out = {nullptr, 0, 0};
+    decompile_source(&C, (u32)A->roots[r], &opt, &out);
+    peak[r] = C.used + (arena_bytes - C.low_top);
   }
   return 0;
 }
