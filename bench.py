@@ -1,16 +1,26 @@
 """Benchmark: code objects decompiled/sec (bit-exact source) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c4|c3_311] [--objects M]
-    python bench.py --impl reference ...      # the reference algorithm on host cores
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c3_311|c4|c4_311|c2|c2x|c5|c3_tiled]
+    python bench.py --impl reference ...      # the reference implementation on host cores
 
 A step decompiles the whole corpus once: decode kernel (co_code -> instruction
 records) then decompile kernel (validate/analyze/structure/recover/emit) into
-one flat UTF-8 buffer.  The corpus is a pool of distinct seeded synthetic
-objects (bench_pools.py) tiled to --objects per GPU (weak scaling); after the
-timed region EVERY output is checked against the reference's SHA-256 digests
-(tests/golden/pools.json).  `value` is timed with inputs resident in HBM;
-`e2e` adds the H2D copy of the packed arena from pinned memory and the D2H of
-statuses + text each step.  Rank 0 prints one JSON line.
+one flat UTF-8 buffer.
+
+Default workload C3 (BASELINE configs[2]): 1,048,576 DISTINCT
+objects per GPU, seed_i = splitmix64(0xC3 ^ i), generated straight into the
+arena by the native generator (synth/c3fast.py; byte-identical to packing the
+Python generator's objects).  Rank r of N takes seeds [r*n, (r+1)*n) (weak
+scaling: together the ranks decompile one N*1M-object corpus; C5 splits one
+16M corpus instead).  After the timed region EVERY output is checked: per
+object SHA-256 of the text, per 1024 objects a hash of those, compared with the
+blocks the real reference produced (tests/golden/c3_digests_3*.json).
+
+`value` is timed with inputs resident in HBM; `e2e` adds the H2D copy of the
+packed arena from pinned memory and the D2H of statuses + text each step;
+`e2e_api` times the public `decompile_many(codes)` on Python CodeObjects (a
+bounded sample); `extra` carries the C3-3.11 and C4 (64K x 10K units) shapes
+at N=1.  Rank 0 prints one JSON line.
 """
 from __future__ import annotations
 
@@ -29,18 +39,30 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "code objects decompiled/sec (bit-exact source), bytecode GB/s vs HBM roofline"
+BLOCK = 1024
+# kind "c3": distinct objects from the native generator (digest-block verified);
+# kind "pool": a pool of distinct Python-generated objects tiled (pools.json verified)
 WORKLOADS = {
-    "c3": ("c3_310", 1_000_000, "C3: synthetic 1M code objects x ~200 units (3.10), straight-line"),
-    "c3_311": ("c3_311", 1_000_000, "C3 (3.11 variant): synthetic 1M code objects x ~200 units + caches"),
-    "c4": ("c4_310", 65_536, "C4: synthetic 64K code objects x ~10K units (3.10), nested if/for/while/try"),
-    "c4_311": ("c4_311", 65_536, "C4 (3.11 variant): synthetic 64K code objects x ~10K units, exception tables"),
-    # C2 (BASELINE configs[1]): the reference's own syntax corpus, one batch of its 110
-    # modules (nested defs/classes/lambdas/comprehensions decompiled through their roots)
-    "c2": ("c2_310", 110, "C2: the reference's pkg/corpus, 110 modules (+nested code, 3.10) in one batch"),
-    "c2x": ("c2_310", 110 * 4096, "C2 x4096: the reference's pkg/corpus modules (3.10) tiled to 450,560 roots"),
-    "c2_311": ("c2_311", 110, "C2 (3.11): the reference's pkg/corpus, 110 modules (+nested code) in one batch"),
-    # C5: one 16M-object corpus split across the ranks (strong scaling)
-    "c5": ("c3_310", 16_777_216, "C5: synthetic 16M code objects x ~200 units (3.10) sharded by object across GPUs"),
+    "c3": {"kind": "c3", "minor": 10, "n": 1 << 20,
+           "desc": "C3: 1,048,576 distinct synthetic code objects x ~200 units (3.10), straight-line"},
+    "c3_311": {"kind": "c3", "minor": 11, "n": 1 << 20,
+               "desc": "C3 (3.11 variant): 1,048,576 distinct synthetic code objects x ~200 units + caches"},
+    "c5": {"kind": "c3", "minor": 10, "n": 1 << 24, "strong": True,
+           "desc": "C5: one 16,777,216-object C3-shape corpus (3.10) sharded by object across GPUs"},
+    "c4": {"kind": "pool", "pool": "c4_310", "n": 65_536,
+           "desc": "C4: 64K code objects x ~10K units (3.10), nested if/for/while/try (64 distinct tiled)"},
+    "c4_311": {"kind": "pool", "pool": "c4_311", "n": 65_536,
+               "desc": "C4 (3.11 variant): 64K code objects x ~10K units, exception tables (32 distinct tiled)"},
+    # C2 (BASELINE configs[1]): the reference's own syntax corpus, one batch of its 110 modules
+    "c2": {"kind": "pool", "pool": "c2_310", "n": 110,
+           "desc": "C2: the reference's pkg/corpus, 110 modules (+nested code, 3.10) in one batch"},
+    "c2x": {"kind": "pool", "pool": "c2_310", "n": 110 * 4096,
+            "desc": "C2 x4096: the reference's pkg/corpus modules (3.10) tiled to 450,560 roots"},
+    "c2_311": {"kind": "pool", "pool": "c2_311", "n": 110,
+               "desc": "C2 (3.11): the reference's pkg/corpus, 110 modules (+nested code) in one batch"},
+    # round-1 headline shape: 4096 distinct objects tiled to ~1M (kept for comparison)
+    "c3_tiled": {"kind": "pool", "pool": "c3_310", "n": 1_000_000,
+                 "desc": "C3 tiled: 4096 distinct 3.10 objects tiled x244 (round-1 workload)"},
 }
 
 
@@ -65,6 +87,17 @@ def peaks():
             d = json.load(f)
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
     return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 class ClockSampler:
@@ -116,42 +149,95 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def algorithmic_bytes(arena, text_len_total, n_instr_total):
+def algorithmic_bytes(arena, n_instr, text_total):
     """Per-launch algorithmic bytes.
 
     decode kernel:     |co_code| + |exctable| + 12 B x N_instr (records written)
     decompile kernel:  12 B x N_instr (records read) + referenced name/const bytes + |output text|
     """
     objs = arena.section("objs")
-    code = int(objs["code_len"].sum())
-    exc = int(objs["exc_len"].sum())
+    code = int(objs["code_len"].astype(np.int64).sum())
+    exc = int(objs["exc_len"].astype(np.int64).sum())
     strs = arena.section("strs")
     refs = arena.section("refs")
+    lens = strs["len"].astype(np.int64)
     name_bytes = 0
     for f in ("names", "varnames", "freevars", "cellvars"):
         offs = objs[f + "_off"].astype(np.int64)
         ns = objs["n_" + f].astype(np.int64)
-        lens = strs["len"].astype(np.int64)
-        tot = 0
-        # vectorized: expand (off, n) ranges
         if ns.sum():
             idx = np.repeat(offs, ns) + (np.arange(ns.sum()) - np.repeat(np.cumsum(ns) - ns, ns))
-            tot = int(lens[refs[idx]].sum())
-        name_bytes += tot
-    consts = arena.section("consts")
-    cidx = objs["consts_off"].astype(np.int64)
-    cn = objs["n_consts"].astype(np.int64)
-    const_bytes = 0
-    if cn.sum():
-        idx = np.repeat(cidx, cn) + (np.arange(cn.sum()) - np.repeat(np.cumsum(cn) - cn, cn))
-        ks = consts[refs[idx]]
-        const_bytes = int(ks.size * consts.dtype.itemsize)
-    dec = code + exc + 12 * n_instr_total
-    struct = 12 * n_instr_total + name_bytes + const_bytes + text_len_total
+            name_bytes += int(lens[refs[idx]].sum())
+    const_bytes = int(objs["n_consts"].astype(np.int64).sum()) * arena.section("consts").dtype.itemsize
+    dec = code + exc + 12 * n_instr
+    struct = 12 * n_instr + name_bytes + const_bytes + text_total
     return dec, struct
 
 
-def verify(res, pool_name, n_pool, stride=1, first=0):
+# ---------------------------------------------------------------- corpora
+def build_corpus(wl, rank, world, n_override=0):
+    """(arena, verifier, description dict).  verifier(res) -> (checked, mismatches)."""
+    from paper_2403_13839_b200 import arena as arena_mod
+
+    spec = WORKLOADS[wl]
+    strong = spec.get("strong", False)
+    n_total = n_override or spec["n"]
+    n = n_total // world if strong else n_total
+    if spec["kind"] == "c3":
+        from paper_2403_13839_b200.synth import c3fast
+
+        first = rank * n
+        ar = c3fast.c3_arena(n, spec["minor"], first)
+        info = {"corpus": f"distinct seeds [{first}, {first + n})", "generator": "synth/c3fast.py (native)"}
+        return ar, (lambda res: verify_digests(res, spec["minor"], first)), info
+    from paper_2403_13839_b200.bench_pools import pool_objects
+
+    pool = pool_objects(spec["pool"])
+    reps = max(1, n // len(pool))
+    ar = arena_mod.tile(arena_mod.pack(pool), reps)
+    info = {"corpus": f"{spec['pool']} ({len(pool)} distinct reference-checked objects tiled x{reps})"}
+    return ar, (lambda res: verify_pool(res, spec["pool"], len(pool))), info
+
+
+def _digest_lines(res):
+    from paper_2403_13839_b200.errors import ST_OK, make_exception
+
+    tb = res.text
+    out = []
+    for i in range(len(res.status)):
+        st = int(res.status[i])
+        o = int(res.text_off[i])
+        s = tb[o:o + int(res.text_len[i])].tobytes()
+        if st == ST_OK:
+            tag = "ok"
+        else:
+            e = make_exception(st, s.decode("utf-8", "surrogatepass"), res.aux[i])
+            tag = type(e).__name__
+            s = f"{tag}: {e}".encode("utf-8", "surrogatepass")
+        out.append(f"{tag}:{hashlib.sha256(s).hexdigest()[:24]}\n")
+    return out
+
+
+def verify_digests(res, minor, first):
+    """Every output against the reference's per-1024-object block hashes; objects
+    in blocks the fixture does not cover (or partial blocks) count as unchecked."""
+    with open(os.path.join(ROOT, "tests", "golden", f"c3_digests_3{minor}.json")) as f:
+        blocks = json.load(f)["blocks"]
+    lines = _digest_lines(res)
+    n = len(lines)
+    checked = bad = 0
+    b0 = -(-first // BLOCK)
+    for b in range(b0, len(blocks)):
+        lo = b * BLOCK - first
+        if lo + BLOCK > n:
+            break
+        checked += BLOCK
+        if hashlib.sha256("".join(lines[lo:lo + BLOCK]).encode()).hexdigest()[:32] != blocks[b]:
+            bad += BLOCK
+    return checked, bad
+
+
+def verify_pool(res, pool_name, n_pool, stride=1, first=0):
     with open(os.path.join(ROOT, "tests", "golden", "pools.json")) as f:
         pools = json.load(f)
     want_sha = pools[pool_name]["sha"]
@@ -171,31 +257,46 @@ def verify(res, pool_name, n_pool, stride=1, first=0):
     return len(range(0, n, stride)), bad
 
 
-def cpu_oracle_baseline(pool, seconds):
-    """The oracle (CPU restatement of the reference algorithm) on every host core,
-    over a bounded sample of the pool.  Returns (objects/s, cores, sample_desc)."""
-    from oracle import bench_cpu
+# ---------------------------------------------------------------- reference arm
+def reference_sample(wl, n_sample):
+    """A bounded sample of the workload as the REFERENCE's own CodeObjects
+    (oracle/_ref staged copy of unpyre, or the port's model objects when the
+    reference is absent).  Returns (objects, kind)."""
+    from oracle import make_ref
+    from paper_2403_13839_b200 import arena as arena_mod
 
-    return bench_cpu.run(pool, seconds)
+    spec = WORKLOADS[wl]
+    if spec["kind"] == "c3":
+        from paper_2403_13839_b200.synth import c3fast
+
+        ar = c3fast.c3_arena(n_sample, spec["minor"], 0)
+    else:
+        from paper_2403_13839_b200.bench_pools import pool_objects
+
+        ar = arena_mod.pack(pool_objects(spec["pool"], 0, n_sample))
+    path = make_ref.ref_path()
+    if path is not None:
+        sys.path.insert(0, path)
+        import unpyre
+
+        return arena_mod.unpack(ar, unpyre.CodeObject, unpyre.Const, unpyre.VersionTag), "reference"
+    return arena_mod.unpack(ar), "port"
 
 
 def run_reference(args):
-    """--impl reference: the reference algorithm (oracle port) on host cores."""
+    """--impl reference: the reference's own decompile_source on every host core."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    pool_name, n_obj, desc = WORKLOADS[args.workload]
-    from paper_2403_13839_b200.bench_pools import pool_objects
-
-    n_sample = 512 if args.workload != "c4" else 8
-    pool = pool_objects(pool_name, 0, n_sample)
     from oracle import bench_cpu
 
+    spec = WORKLOADS[args.workload]
+    n_sample = 512 if spec["kind"] == "c3" else (8 if args.workload.startswith("c4") else 110)
+    objs, kind = reference_sample(args.workload, n_sample)
     times = []
-    cores = None
-    sample = None
+    cores = sample = None
     for step in range(args.warmup + args.steps):
-        rate, cores, sample = bench_cpu.run(pool, args.ref_seconds)
+        rate, cores, sample = bench_cpu.run(objs, args.ref_seconds, kind=kind)
         if step >= args.warmup:
             times.append(rate)
     value = statistics.median(times)
@@ -203,11 +304,163 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": 1000.0 * n_sample / value, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": desc, "objects_per_step": n_sample, "pool": pool_name},
-            "cpu_baseline": {"value": value, "unit": "objects/s", "cores": cores, "kind": "port",
-                             "sample": sample},
+            "config": {"workload": spec["desc"], "objects_per_step": n_sample},
+            "cpu_baseline": {"value": value, "unit": "objects/s", "cores": cores, "kind": kind,
+                             "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": "objects/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- one workload on the device
+def time_device(da, steps, warmup, barrier):
+    """Decode + decompile per step on HBM-resident inputs: per-step kernel times
+    (CUDA events on the launching stream) and the total."""
+    import torch
+
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        da.run(stream, "decode")
+        da.run(stream, "structure")
+    barrier()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    barrier()
+    for k in range(steps):
+        ev[k][0].record(stream)
+        da.run(stream, "decode")
+        ev[k][1].record(stream)
+        da.run(stream, "structure")
+        ev[k][2].record(stream)
+    barrier()
+    dec_ms = [ev[k][0].elapsed_time(ev[k][1]) for k in range(steps)]
+    st_ms = [ev[k][1].elapsed_time(ev[k][2]) for k in range(steps)]
+    return ev[0][0].elapsed_time(ev[-1][2]), sum(dec_ms), sum(st_ms)
+
+
+def time_e2e(da, arena, args, local, barrier):
+    """H2D of the packed arena from pinned memory, both kernels, D2H of statuses
+    and text, every step; two buffer sets and three streams overlap the copies of
+    one step with the kernels of its neighbours."""
+    import torch
+
+    from paper_2403_13839_b200.api import DeviceArena
+
+    stream = torch.cuda.current_stream()
+    res = da.fetch()
+    used = len(res.text)
+    free, _ = torch.cuda.mem_get_info()
+    need = da.ws_bytes + da.text.numel() + da.dev.numel() + da.meta.numel()
+    if free > 1.2 * need:
+        das = [da, DeviceArena(arena, device=f"cuda:{local}", slots=da.opts.slots, arena_bytes=args.arena_bytes,
+                               threads_per_block=args.tpb, pinned=da.host)]
+    else:
+        das = [da, da]
+    metas = [torch.empty(da.meta.numel(), dtype=torch.uint8).pin_memory() for _ in range(2)]
+    texts = [torch.empty(used, dtype=torch.uint8).pin_memory() for _ in range(2)]
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    steps = args.steps
+    ev_in = [torch.cuda.Event() for _ in range(steps)]
+    ev_run = [torch.cuda.Event() for _ in range(steps)]
+    ev_out = [torch.cuda.Event() for _ in range(steps)]
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(s_in)
+    for k in range(steps):
+        d = das[k % 2]
+        with torch.cuda.stream(s_in):
+            if k >= 2:
+                s_in.wait_event(ev_run[k - 2])
+            if das[0] is das[1] and k >= 1:
+                s_in.wait_event(ev_run[k - 1])
+            d.dev.copy_(d.host, non_blocking=True)
+            ev_in[k].record(s_in)
+        with torch.cuda.stream(stream):
+            stream.wait_event(ev_in[k])
+            if k >= 2:
+                stream.wait_event(ev_out[k - 2])
+            if das[0] is das[1] and k >= 1:
+                stream.wait_event(ev_out[k - 1])
+            d.run(stream, "full")
+            ev_run[k].record(stream)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(ev_run[k])
+            metas[k % 2].copy_(d.meta, non_blocking=True)
+            texts[k % 2].copy_(d.text[:used], non_blocking=True)
+            ev_out[k].record(s_out)
+    s_in.wait_event(ev_out[steps - 1])
+    e1.record(s_in)
+    barrier()
+    ms = e0.elapsed_time(e1)
+    double = das[0] is not das[1]
+    del das
+    return res, ms, used, double
+
+
+def run_workload(wl, args, rank, world, local, barrier, steps, warmup, e2e=True):
+    """Generate, upload, time and verify one workload on this rank."""
+    import torch
+
+    from paper_2403_13839_b200.api import DeviceArena
+
+    t_gen = time.time()
+    arena, verifier, info = build_corpus(wl, rank, world, args.objects if wl == args.workload else 0)
+    t_gen = time.time() - t_gen
+    da = DeviceArena(arena, device=f"cuda:{local}", slots=args.slots, arena_bytes=args.arena_bytes,
+                     threads_per_block=args.tpb)
+    da.upload()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        total_ms, dec_sum, st_sum = time_device(da, steps, warmup, barrier)
+    n_instr = int(da.decoded()["n_instrs"].astype(np.int64).sum())
+    e2e_ms = used = None
+    double = False
+    if e2e:
+        a2 = argparse.Namespace(**{**vars(args), "steps": steps})
+        res, e2e_ms, used, double = time_e2e(da, arena, a2, local, barrier)
+    else:
+        res = da.fetch()
+    checked, bad = verifier(res)
+    out = {"arena": arena, "res": res, "da_host": int(da.host.numel()), "da_meta": int(da.meta.numel()),
+           "slots": int(da.opts.slots), "total_ms": total_ms, "dec_sum": dec_sum, "st_sum": st_sum,
+           "e2e_ms": e2e_ms, "used": used, "double": double, "n_instr": n_instr, "checked": checked,
+           "bad": bad, "clocks": clk.summary(), "t_gen": t_gen, "info": info, "n_roots": arena.n_roots}
+    del da
+    return out
+
+
+def extra_line(wl, args, local, barrier):
+    """A secondary shape at N=1 (fewer steps): objects/s, kernel times, parity."""
+    r = run_workload(wl, args, 0, 1, local, barrier, steps=2, warmup=1, e2e=False)
+    ms = r["total_ms"] / 2
+    return {"workload": WORKLOADS[wl]["desc"], "value": r["n_roots"] / (ms / 1000.0), "unit": "objects/s",
+            "steps": 2, "warmup": 1, "ms_per_step": ms,
+            "kernel_ms": {"decode": r["dec_sum"] / 2, "decompile": r["st_sum"] / 2},
+            "instructions": r["n_instr"], "code_bytes": r["arena"].code_bytes,
+            "decode_gbs_alg": None, "parity": {"checked": r["checked"], "mismatches": r["bad"]},
+            "slots": r["slots"], "corpus": r["info"]["corpus"], "clocks": r["clocks"]}
+
+
+def api_e2e(wl, n_sample, local):
+    """The public API a user calls, timed end to end: decompile_many(codes) on
+    Python CodeObjects (pack on the host, H2D, both kernels, D2H, str results)."""
+    import torch
+
+    from paper_2403_13839_b200 import api, arena as arena_mod
+    from paper_2403_13839_b200.synth import c3fast
+
+    spec = WORKLOADS[wl]
+    codes = arena_mod.unpack(c3fast.c3_arena(n_sample, spec["minor"], 0))
+    dev = f"cuda:{local}"
+    api.decompile_many(codes[:1024], device=dev)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    out = api.decompile_many(codes, device=dev)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    ok = sum(1 for v in out if isinstance(v, str))
+    return {"value": n_sample / dt, "unit": "objects/s", "objects": n_sample, "seconds": dt, "ok": ok,
+            "call": "paper_2403_13839_b200.decompile_many(codes) on model.CodeObject inputs",
+            "timing": "wall clock of one call after a warm-up call (host packing included)"}
 
 
 def main():
@@ -217,15 +470,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
-    ap.add_argument("--objects", type=int, default=0, help="objects per GPU (default per workload)")
+    ap.add_argument("--objects", type=int, default=0, help="objects (per GPU; total for c5)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C3-3.11 / C4 legs and e2e_api")
     ap.add_argument("--slots", type=int, default=0)
     ap.add_argument("--arena-bytes", type=int, default=0)
     ap.add_argument("--tpb", type=int, default=0)
-    ap.add_argument("--verify-stride", type=int, default=0, help="check every k-th output (0: 1, c5: 16)")
     ap.add_argument("--pyc", type=int, default=1, help="also time the .pyc-bytes end-to-end path (0: skip)")
+    ap.add_argument("--api-sample", type=int, default=16384)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -242,175 +496,82 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    from paper_2403_13839_b200 import arena as arena_mod
-    from paper_2403_13839_b200.api import DeviceArena
-    from paper_2403_13839_b200.bench_pools import POOLS, pool_objects
-
-    pool_name, default_n, desc = WORKLOADS[args.workload]
-    strong = args.workload == "c5"
-    n_total = args.objects or default_n
-    n_per_rank = n_total // world if strong else n_total
-    t_gen = time.time()
-    pool = pool_objects(pool_name)
-    n_pool = len(pool)
-    reps = max(1, n_per_rank // n_pool)
-    pool_arena = arena_mod.pack(pool)
-    arena = arena_mod.tile(pool_arena, reps)
-    t_gen = time.time() - t_gen
-    n_roots = arena.n_roots
-    da = DeviceArena(arena, device=f"cuda:{local}", slots=args.slots, arena_bytes=args.arena_bytes,
-                     threads_per_block=args.tpb)
-    da.upload()
-    torch.cuda.synchronize()
-    stream = torch.cuda.current_stream()
-
     def barrier():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    # warm-up (full steps)
-    for _ in range(args.warmup):
-        da.run(stream, "decode")
-        da.run(stream, "structure")
-    barrier()
+    spec = WORKLOADS[args.workload]
+    r = run_workload(args.workload, args, rank, world, local, barrier, args.steps, args.warmup)
 
-    # ---------------- timed: inputs resident in HBM
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
-        barrier()
-        for k in range(args.steps):
-            ev[k][0].record(stream)
-            da.run(stream, "decode")
-            ev[k][1].record(stream)
-            da.run(stream, "structure")
-            ev[k][2].record(stream)
-        barrier()
-    dec_ms = [ev[k][0].elapsed_time(ev[k][1]) for k in range(args.steps)]
-    st_ms = [ev[k][1].elapsed_time(ev[k][2]) for k in range(args.steps)]
-    total_ms = ev[0][0].elapsed_time(ev[-1][2])
-    res = da.fetch()
-
-    # ---------------- timed: end to end (H2D of the packed arena, kernels, D2H of results)
-    # Every step copies its inputs host -> device from pinned memory and its results
-    # (statuses + text) device -> host.  Two buffer sets and three streams overlap the
-    # copies of one step with the kernels of the neighbouring steps (double buffering);
-    # time is measured from the first H2D to the last D2H.
-    used = len(res.text)
-    # second buffer set when it fits (C5's 16M objects need ~100 GB per set: single-buffered)
-    free, _ = torch.cuda.mem_get_info()
-    need = da.ws_bytes + da.text.numel() + da.dev.numel() + da.meta.numel()
-    if free > 1.2 * need:
-        das = [da, DeviceArena(arena, device=f"cuda:{local}", slots=args.slots, arena_bytes=args.arena_bytes,
-                               threads_per_block=args.tpb, pinned=da.host)]
-    else:
-        das = [da, da]
-    metas = [torch.empty(da.meta.numel(), dtype=torch.uint8).pin_memory() for _ in range(2)]
-    texts = [torch.empty(used, dtype=torch.uint8).pin_memory() for _ in range(2)]
-    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-    ev_in = [torch.cuda.Event() for _ in range(args.steps)]
-    ev_run = [torch.cuda.Event() for _ in range(args.steps)]
-    ev_out = [torch.cuda.Event() for _ in range(args.steps)]
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    barrier()
-    e0.record(s_in)
-    for k in range(args.steps):
-        d = das[k % 2]
-        with torch.cuda.stream(s_in):
-            if k >= 2:
-                s_in.wait_event(ev_run[k - 2])   # buffer set k%2 free again
-            if das[0] is das[1] and k >= 1:
-                s_in.wait_event(ev_run[k - 1])   # single buffer set: the previous step's kernels are done
-            d.dev.copy_(d.host, non_blocking=True)
-            ev_in[k].record(s_in)
-        with torch.cuda.stream(stream):
-            stream.wait_event(ev_in[k])
-            if k >= 2:
-                stream.wait_event(ev_out[k - 2])
-            if das[0] is das[1] and k >= 1:
-                stream.wait_event(ev_out[k - 1])  # single buffer set: results of step k-1 copied out
-            d.run(stream, "full")
-            ev_run[k].record(stream)
-        with torch.cuda.stream(s_out):
-            s_out.wait_event(ev_run[k])
-            metas[k % 2].copy_(d.meta, non_blocking=True)
-            texts[k % 2].copy_(d.text[:used], non_blocking=True)
-            ev_out[k].record(s_out)
-    s_in.wait_event(ev_out[args.steps - 1])
-    e1.record(s_in)
-    barrier()
-    e2e_ms = e0.elapsed_time(e1)
-    double_buffered = das[0] is not das[1]
-    del das
-
-    # ---------------- end to end from .pyc files in host memory:
-    # native loader (all host threads) -> H2D -> kernels -> D2H, wall clock
+    # .pyc bytes -> native loader -> device -> back, on the tiled pool
     pyc = None
-    if args.pyc and args.workload in ("c2", "c2x", "c2_311", "c3", "c3_311", "c5"):
-        pyc = pyc_e2e(pool, reps, local, args, pool_name, n_pool, barrier)
+    if args.pyc and args.workload in ("c2", "c2x", "c2_311", "c3", "c3_311", "c3_tiled", "c5"):
+        pool_name = {"c3": "c3_310", "c3_tiled": "c3_310", "c5": "c3_310", "c3_311": "c3_311"}.get(
+            args.workload, spec.get("pool"))
+        pyc = pyc_e2e(pool_name, r["n_roots"], local, args, barrier)
 
-    # ---------------- max over ranks
-    times = torch.tensor([total_ms, e2e_ms, sum(dec_ms), sum(st_ms)], dtype=torch.float64, device="cuda")
+    # max over ranks
+    times = torch.tensor([r["total_ms"], r["e2e_ms"], r["dec_sum"], r["st_sum"]], dtype=torch.float64,
+                         device="cuda")
+    counts = torch.tensor([r["checked"], r["bad"], r["n_roots"]], dtype=torch.int64, device="cuda")
     if dist is not None:
         dist.all_reduce(times, op=dist.ReduceOp.MAX)
+        dist.all_reduce(counts)
     total_ms, e2e_ms, dec_sum, st_sum = [float(x) for x in times.tolist()]
+    n_checked, n_bad, objs_total = [int(x) for x in counts.tolist()]
 
-    # ---------------- parity of every output against the reference digests
-    stride = args.verify_stride or (16 if strong else 1)
-    n_checked, n_bad = verify(res, pool_name, n_pool, stride)
-    bad_t = torch.tensor([n_checked, n_bad], dtype=torch.int64, device="cuda")
-    if dist is not None:
-        dist.all_reduce(bad_t)
-    n_checked, n_bad = [int(x) for x in bad_t.tolist()]
+    extra = None
+    e2e_api = None
+    if world == 1 and not args.no_extra and args.workload == "c3":
+        extra = {}
+        for wl in ("c3_311", "c4"):
+            extra[wl] = extra_line(wl, args, local, barrier)
+        e2e_api = api_e2e("c3", args.api_sample, local)
 
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
         return
 
-    objs_total = n_roots * world
+    arena, res = r["arena"], r["res"]
     ms_step = total_ms / args.steps
     value = objs_total / (ms_step / 1000.0)
-    code_bytes = arena.code_bytes
-    # instruction count and name/const bytes from the distinct pool, x tiles
-    n_instr = reps * int(_count_instructions(pool_arena))
-    text_total = int(res.text_len.sum())
-    pd, ps = algorithmic_bytes(pool_arena, 0, 0)
-    alg_dec = reps * pd + 12 * n_instr
-    alg_struct = reps * ps + 12 * n_instr + text_total
+    text_total = int(res.text_len.astype(np.int64).sum())
+    alg_dec, alg_struct = algorithmic_bytes(arena, r["n_instr"], text_total)
     peak, peak_src = peaks()
     dec_avg = dec_sum / args.steps / 1000.0
     st_avg = st_sum / args.steps / 1000.0
     ach_struct = alg_struct / st_avg / 1e9
     ach_dec = alg_dec / dec_avg / 1e9
-    h2d = int(da.host.numel())
-    d2h = int(da.meta.numel()) + used
+    h2d = r["da_host"]
+    d2h = r["da_meta"] + r["used"]
     e2e_value = objs_total / (e2e_ms / args.steps / 1000.0)
     cpu = None
     if not args.no_cpu and world == 1:
-        try:
-            rate, cores, sample = cpu_oracle_baseline(pool[:512], args.cpu_seconds)
-            cpu = {"value": rate, "unit": "objects/s", "cores": cores, "kind": "port", "sample": sample}
-        except ImportError as e:
-            cpu = {"value": None, "unit": "objects/s", "cores": None, "kind": "port",
-                   "sample": f"unavailable: {e}"}
-    clocks = clk.summary()
+        from oracle import bench_cpu
+
+        objs, kind = reference_sample(args.workload, 512 if spec["kind"] == "c3" else 8)
+        rate, cores, sample = bench_cpu.run(objs, args.cpu_seconds, kind=kind)
+        cpu = {"value": rate, "unit": "objects/s", "cores": cores, "kind": kind, "sample": sample,
+               "cpu_model": cpu_model()}
+    code_bytes = arena.code_bytes
     line = {
         "metric": METRIC, "value": value, "unit": "objects/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "strong" if strong else "weak",
+        "scaling": "strong" if spec.get("strong") else "weak",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": desc, "objects_per_gpu": n_roots, "objects_total": objs_total,
-                   "code_objects_per_gpu": int(len(arena.section("objs"))),
-                   "pool": f"{pool_name} ({n_pool} distinct reference-checked objects tiled x{reps})",
-                   "python": POOLS[pool_name]["minor"], "code_bytes_per_gpu": code_bytes,
-                   "instructions_per_gpu": n_instr,
-                   "l2": f"inputs larger than L2 ({h2d / 1e9:.2f} GB arena + {12 * n_instr / 1e9:.2f} GB records)",
-                   "parallelism": f"shard roots x{world}", "gen_seconds": round(t_gen, 1)},
+        "config": {"workload": spec["desc"], "objects_per_gpu": r["n_roots"], "objects_total": objs_total,
+                   "code_objects_per_gpu": int(arena.n_objs), "corpus": r["info"]["corpus"],
+                   "python": spec.get("minor", 10), "code_bytes_per_gpu": code_bytes,
+                   "instructions_per_gpu": r["n_instr"], "slots": r["slots"],
+                   "l2": f"inputs larger than L2 ({h2d / 1e9:.2f} GB arena + {12 * r['n_instr'] / 1e9:.2f} GB "
+                         "records per step)",
+                   "parallelism": f"objects sharded x{world}", "gen_seconds": round(r["t_gen"], 1)},
         "bytecode_gbs": code_bytes * world / (ms_step / 1000.0) / 1e9,
         "kernel_ms": {"decode": dec_sum / args.steps, "decompile": st_sum / args.steps},
-        "parity": {"checked": n_checked, "mismatches": n_bad, "against": "reference SHA-256 (pools.json)"},
+        "parity": {"checked": n_checked, "mismatches": n_bad,
+                   "against": "reference output digests (tests/golden/c3_digests_3*.json blocks / pools.json)"},
         "roofline": {"bound": "hbm", "kernel": "upy_decompile_kernel", "achieved": ach_struct, "peak": peak,
                      "unit": "GB/s", "frac": ach_struct / peak,
                      "traffic": measured_traffic(args.workload, "upy_decompile_kernel"),
@@ -421,33 +582,39 @@ def main():
                             "algorithmic_bytes_per_launch": alg_dec},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "objects/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "double_buffered": double_buffered},
+                "double_buffered": r["double"]},
+        "e2e_api": e2e_api,
         "e2e_pyc": pyc,
-        "gpu_launches": 2 * args.steps + 2 * args.steps,
-        "clocks": clocks,
+        "extra": extra,
+        "gpu_launches": 4 * args.steps,
+        "clocks": r["clocks"],
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
 
 
-def pyc_e2e(pool, reps, local, args, pool_name, n_pool, barrier):
+def pyc_e2e(pool_name, n_files, local, args, barrier):
     """decompile_pyc path timed end to end: .pyc images back to back in host memory
     -> upy_pyc_load (C++, all host threads) -> pinned H2D -> decode + decompile
     kernels -> D2H of statuses and text, as 4 pipelined sub-batches
     (loader.decompile_pyc_chunks).  Wall clock per step (host work is part of it),
-    outputs checked against the reference digests."""
+    outputs checked against the reference digests.  The images are the pool's
+    distinct objects tiled to n_files (a .pyc writer for 1M distinct objects would
+    be Python-bound)."""
+    from paper_2403_13839_b200.bench_pools import pool_objects
     from paper_2403_13839_b200.loader import decompile_pyc_chunks, load_pyc_buffer
     from paper_2403_13839_b200.synth import marshal
 
+    pool = pool_objects(pool_name)
+    n_pool = len(pool)
+    reps = max(1, n_files // n_pool)
     blobs = [marshal.dump_pyc(co) for co in pool]
     one = b"".join(blobs)
     sizes = np.array([len(b) for b in blobs] * reps, dtype=np.uint64)
     offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.uint64)
     buf = np.frombuffer(one * reps, dtype=np.uint8)
     n = len(sizes)
-    # up to 4 sub-batches of >= 65,536 files: host parsing of one overlaps the device work
-    # of the previous (small batches stay one batch: per-batch fixed costs dominate there)
     chunk = max(65536, (n + 3) // 4)
 
     def load(lo, hi):
@@ -457,7 +624,7 @@ def pyc_e2e(pool, reps, local, args, pool_name, n_pool, barrier):
     results = None
     for k in range(1 + args.steps):  # first step is warm-up
         barrier()
-        results = None  # return the previous step's page-locked buffers to the caches first
+        results = None
         t0 = time.perf_counter()
         results = [(lo, res) for lo, _pf, res in decompile_pyc_chunks(load, n, None, f"cuda:{local}", chunk)]
         barrier()
@@ -466,44 +633,15 @@ def pyc_e2e(pool, reps, local, args, pool_name, n_pool, barrier):
             t_all.append(t2 - t0)
     n_checked = n_bad = 0
     for lo, r in results:
-        c, b = verify(r, pool_name, n_pool, 1, first=lo % n_pool)
+        c, b = verify_pool(r, pool_name, n_pool, 1, first=lo % n_pool)
         n_checked += c
         n_bad += b
     step = sum(t_all) / len(t_all)
     return {"value": n / step, "unit": "objects/s", "files_per_step": n, "pyc_bytes_per_step": int(len(buf)),
-            "step_ms": 1000 * step, "sub_batches": (n + chunk - 1) // chunk,
+            "step_ms": 1000 * step, "sub_batches": (n + chunk - 1) // chunk, "corpus": f"{pool_name} tiled x{reps}",
             "loader_threads": os.cpu_count(), "parity": {"checked": n_checked, "mismatches": n_bad},
             "timing": "wall clock, synchronized, mean of --steps after 1 warm-up; host parsing of sub-batch "
                       "i+1 overlaps the device work of sub-batch i"}
-
-
-def _count_instructions(arena):
-    """Instruction count = code units minus EXTENDED_ARG prefixes minus cache units."""
-    from paper_2403_13839_b200._optables import TABLES
-
-    objs = arena.section("objs")
-    by = arena.section("bytes")
-    total = 0
-    # only the distinct pool copy needs decoding logic; tiles repeat it
-    for o in objs:
-        off, ln, minor = int(o["code_off"]), int(o["code_len"]), int(o["minor"])
-        code = by[off:off + ln]
-        ops = code[0::2]
-        n_ext = int(np.sum(ops == 144))
-        if minor >= 11:
-            caches = np.array([TABLES[11].get(int(x), ("", 0, "", 0))[3] for x in range(256)])
-            # walk in order (caches are skipped, not decoded)
-            i = 0
-            n = 0
-            while i < ln:
-                op = int(code[i])
-                if op != 144:
-                    n += 1
-                i += 2 + 2 * (int(caches[op]) if op != 144 else 0)
-            total += n
-        else:
-            total += ln // 2 - n_ext
-    return total
 
 
 if __name__ == "__main__":

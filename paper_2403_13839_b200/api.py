@@ -72,6 +72,8 @@ class DeviceArena:
         self.host = pinned if pinned is not None else torch.from_numpy(arena.blob).pin_memory()
         self.dev = torch.empty(self.host.numel(), dtype=torch.uint8, device=self.device)
         self.A = _abi.arena_struct(arena, self.dev.data_ptr())
+        if not slots and not arena_bytes:
+            slots = self._memory_slots(arena)
         self.opts = _abi.options(style, arena_bytes=arena_bytes, slots=slots,
                                  threads_per_block=threads_per_block, function_tree=1 if function_tree else 0,
                                  output=output)
@@ -99,6 +101,21 @@ class DeviceArena:
         self.out.status = m + 64 + 28 * n
         self.n = arena.n_roots
 
+    def _memory_slots(self, arena):
+        """Concurrent per-thread arenas when the library's default 40 GB budget
+        would bind (long objects: C4's ~3 MB slots allow only ~13K threads):
+        size the slot count from the device's free memory instead (55% of it,
+        the text buffer and a second buffer set need the rest).  0 = library
+        default.  Measured on C4 (profiles/r02/bench_c4_slots_*.json): 12,288
+        slots 2,726 objects/s, 24,576 2,965, 49,152 3,542."""
+        sb = default_slot_bytes(arena) + (68 << 10) + 256  # + the slot header (upy.cu SLOT_HEADER)
+        full = self.torch.cuda.get_device_properties(self.device).multi_processor_count * 1024
+        want = min(arena.n_roots, full)
+        if (40 << 30) // sb >= want:
+            return 0
+        free, _ = self.torch.cuda.mem_get_info(self.device)
+        return int(max(1, min(want, int(free * 0.55) // sb)))
+
     def upload(self, stream=None):
         with self.torch.cuda.device(self.device):
             self.dev.copy_(self.host, non_blocking=True)
@@ -117,6 +134,16 @@ class DeviceArena:
                                               C.c_void_p(self.ws.data_ptr()), C.c_size_t(self.ws_bytes),
                                               C.c_void_p(s.cuda_stream))
         _lib.check(rc, "upy_decompile_batch")
+
+    def decoded(self):
+        """Per-object decode results (upy_decoded: status, n_instrs, aux) of the
+        last decode on this workspace (layout: upy.cu WsLayout)."""
+        from .arena import DECODED_DTYPE, INS_DTYPE
+
+        units = self.arena.total_code_units + 1
+        off = (units * INS_DTYPE.itemsize + 255) & ~255
+        n = DECODED_DTYPE.itemsize * self.arena.n_objs
+        return self.ws[off:off + n].cpu().numpy().view(DECODED_DTYPE)
 
     def fetch(self) -> BatchResult:
         n = self.n

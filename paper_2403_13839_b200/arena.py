@@ -206,7 +206,17 @@ def _align(x, a):
 
 
 def pack(roots) -> Arena:
-    """Pack root code objects (each with its nested code constants)."""
+    """Pack root code objects (each with its nested code constants) with the
+    native packer (csrc/packer.cpp, byte-identical to `pack_py`)."""
+    from . import _packer
+
+    blob, offsets, counts, max_code_len, total_units = _packer.pack(list(roots))
+    return Arena(np.frombuffer(blob, dtype=np.uint8), offsets, counts, max_code_len, total_units)
+
+
+def pack_py(roots) -> Arena:
+    """Pack root code objects (each with its nested code constants): the Python
+    restatement the native packer is checked against (tests/test_packer.py)."""
     p = _Packer()
     root_ids = [p.code(r) for r in roots]
     n_obj = len(p.objs)

@@ -112,6 +112,22 @@ def build_cuda(force=False, verbose=True):
     return LIB
 
 
+def build_packer(force=False, verbose=True):
+    """The native arena packer (csrc/packer.cpp), a CPython extension built in-tree
+    next to the package (g++ against this interpreter's Python.h)."""
+    import sysconfig
+
+    src = os.path.join(CSRC, "packer.cpp")
+    target = os.path.join(HERE, "_packer" + sysconfig.get_config_var("EXT_SUFFIX"))
+    flags = ["-O2", "-std=c++17", "-shared", "-fPIC", "-I" + sysconfig.get_paths()["include"]]
+    if force or not up_to_date(target, [src], flags):
+        digest = _digest([src], flags)
+        _run([os.environ.get("CXX", "g++"), *flags, "-o", target + ".tmp", src], verbose)
+        os.replace(target + ".tmp", target)
+        _stamp(target, digest)
+    return target
+
+
 def build_host(force=False):
     from . import hostcheck
 
@@ -131,6 +147,7 @@ def main(argv=None):
     argv = sys.argv[1:] if argv is None else argv
     force = "--force" in argv
     build_cuda(force)
+    build_packer(force)
     build_host(force)
     stage_reference()
 
