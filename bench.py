@@ -430,6 +430,9 @@ def run_workload(wl, args, rank, world, local, barrier, steps, warmup, e2e=True)
 
 def extra_line(wl, args, local, barrier):
     """A secondary shape at N=1 (fewer steps): objects/s, kernel times, parity."""
+    import torch
+
+    torch.cuda.empty_cache()  # the previous leg's buffers
     r = run_workload(wl, args, 0, 1, local, barrier, steps=2, warmup=1, e2e=False)
     ms = r["total_ms"] / 2
     return {"workload": WORKLOADS[wl]["desc"], "value": r["n_roots"] / (ms / 1000.0), "unit": "objects/s",

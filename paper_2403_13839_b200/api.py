@@ -114,6 +114,8 @@ class DeviceArena:
         if (40 << 30) // sb >= want:
             return 0
         free, _ = self.torch.cuda.mem_get_info(self.device)
+        # blocks torch's caching allocator holds but no tensor uses are free to us too
+        free += self.torch.cuda.memory_reserved(self.device) - self.torch.cuda.memory_allocated(self.device)
         return int(max(1, min(want, int(free * 0.55) // sb)))
 
     def upload(self, stream=None):
