@@ -336,6 +336,24 @@ def time_device(da, steps, warmup, barrier):
     return ev[0][0].elapsed_time(ev[-1][2]), sum(dec_ms), sum(st_ms)
 
 
+def time_stackscan(da, steps, barrier):
+    """The stack-depth scan kernel (csrc/stackscan_kernel.cu) over the records of
+    the last decode, timed on its own (its output does not feed the decompile
+    kernel, so it is not part of a step): mean ms per launch."""
+    import torch
+
+    stream = torch.cuda.current_stream()
+    da.stackscan(stream)  # warm-up (allocates its buffers)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        da.stackscan(stream)
+    e1.record(stream)
+    barrier()
+    return e0.elapsed_time(e1) / steps
+
+
 def time_e2e(da, arena, args, local, barrier):
     """H2D of the packed arena from pinned memory, both kernels, D2H of statuses
     and text, every step; two buffer sets and three streams overlap the copies of
@@ -412,6 +430,7 @@ def run_workload(wl, args, rank, world, local, barrier, steps, warmup, e2e=True)
     with ClockSampler(local) as clk:
         total_ms, dec_sum, st_sum = time_device(da, steps, warmup, barrier)
     n_instr = int(da.decoded()["n_instrs"].astype(np.int64).sum())
+    ss_ms = time_stackscan(da, steps, barrier)
     e2e_ms = used = None
     double = False
     if e2e:
@@ -423,7 +442,8 @@ def run_workload(wl, args, rank, world, local, barrier, steps, warmup, e2e=True)
     out = {"arena": arena, "res": res, "da_host": int(da.host.numel()), "da_meta": int(da.meta.numel()),
            "slots": int(da.opts.slots), "total_ms": total_ms, "dec_sum": dec_sum, "st_sum": st_sum,
            "e2e_ms": e2e_ms, "used": used, "double": double, "n_instr": n_instr, "checked": checked,
-           "bad": bad, "clocks": clk.summary(), "t_gen": t_gen, "info": info, "n_roots": arena.n_roots}
+           "bad": bad, "clocks": clk.summary(), "t_gen": t_gen, "info": info, "n_roots": arena.n_roots,
+           "stackscan_ms": ss_ms}
     del da
     return out
 
@@ -437,7 +457,7 @@ def extra_line(wl, args, local, barrier):
     ms = r["total_ms"] / 2
     return {"workload": WORKLOADS[wl]["desc"], "value": r["n_roots"] / (ms / 1000.0), "unit": "objects/s",
             "steps": 2, "warmup": 1, "ms_per_step": ms,
-            "kernel_ms": {"decode": r["dec_sum"] / 2, "decompile": r["st_sum"] / 2},
+            "kernel_ms": {"decode": r["dec_sum"] / 2, "decompile": r["st_sum"] / 2, "stackscan": r["stackscan_ms"]},
             "instructions": r["n_instr"], "code_bytes": r["arena"].code_bytes,
             "decode_gbs_alg": None, "parity": {"checked": r["checked"], "mismatches": r["bad"]},
             "slots": r["slots"], "corpus": r["info"]["corpus"], "clocks": r["clocks"]}
@@ -583,6 +603,13 @@ def main():
                             "unit": "GB/s", "frac": ach_dec / peak,
                             "traffic": measured_traffic(args.workload, "upy_decode_kernel"),
                             "algorithmic_bytes_per_launch": alg_dec},
+        "roofline_stackscan": {"bound": "hbm", "kernel": "upy_stackscan_kernel", "ms": r["stackscan_ms"],
+                               "achieved": (16 * r["n_instr"] + 56 * arena.n_objs) / (r["stackscan_ms"] / 1e3) / 1e9,
+                               "peak": peak, "unit": "GB/s",
+                               "frac": (16 * r["n_instr"] + 56 * arena.n_objs) / (r["stackscan_ms"] / 1e3) / 1e9 / peak,
+                               "algorithmic_bytes_per_launch": 16 * r["n_instr"] + 56 * arena.n_objs,
+                               "note": "12 B record read + 4 B depth record written per instruction, 56 B per object; "
+                                       "timed separately (not part of a step)"},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "objects/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "double_buffered": r["double"]},

@@ -125,6 +125,29 @@ typedef struct {
   int64_t aux0, aux1;   /* error attributes (opcode/offset, offset/target, position) */
 } upy_decoded;
 
+/* Stack-depth scan record, one per decoded instruction (same index as upy_ins):
+ * the symbolic stack depth after the instruction along the fall-through edge,
+ * relative to the entry of its segment -- the run of instructions from one
+ * instruction-rule block leader (first instruction, jump target, instruction
+ * after a block ender; cfg.py:72-86) to the next.  Every reference basic block
+ * lies inside one segment, so a block entered at depth E has depth
+ * E + depth[i] - depth[lo-1] after instruction i (depth[lo-1] = 0 when lo starts
+ * a segment).  Effects per symexec.py's transfer functions. */
+typedef struct {
+  int16_t depth;
+  uint8_t flags;        /* bit0 segment start, bit1 depth unknown (a contents-dependent effect
+                           earlier in the segment), bit2 block ender */
+  uint8_t pad;
+} upy_stackrec;
+/* Per-object summary of the scan. */
+typedef struct {
+  int32_t status;       /* the object's decode status (UPY_ST_OK or a decode error: no records) */
+  int32_t n_segments;
+  int32_t max_depth;    /* max / min relative depth over known positions */
+  int32_t min_depth;
+  int32_t n_pushes;     /* sum of positive known effects (symbolic values created) */
+  int32_t n_unknown;    /* instructions with a contents-dependent effect */
+} upy_stackinfo;
 enum {
   UPY_ST_OK = 0, UPY_ST_UNPYRE = 1, UPY_ST_UNKNOWN_OPCODE = 2, UPY_ST_TRUNCATED_CODE = 3,
   UPY_ST_BAD_JUMP_TARGET = 4, UPY_ST_MALFORMED_EXCTABLE = 5, UPY_ST_STACK_UNDERFLOW = 6,
@@ -140,7 +163,7 @@ enum {
 
 /* sizeof() of the ABI structs, for binding-side layout checks:
  * which = 0 upy_obj, 1 upy_const, 2 upy_str, 3 upy_arena, 4 upy_options, 5 upy_out,
- *         6 upy_ins, 7 upy_decoded.  Returns 0 for unknown. */
+ *         6 upy_ins, 7 upy_decoded, 8 upy_stackrec, 9 upy_stackinfo.  Returns 0 for unknown. */
 size_t upy_abi_sizeof(int which);
 int upy_abi_version(void);
 
@@ -159,6 +182,12 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
  * ins[objs[o].code_off/2 + j].  Returns 0 on launch success. */
 int upy_decode_batch(const upy_arena* arena, upy_ins* ins, upy_decoded* dec, void* stream);
 
+/* Stack-depth scan (north-star subsystem 3) over the records of a
+ * previous upy_decode_batch on the same ins / dec: one upy_stackrec per record
+ * (stack[objs[o].code_off/2 + i]) and one upy_stackinfo per object.  Warp per
+ * object, segmented warp scan.  Returns 0 on launch success. */
+int upy_stackscan_batch(const upy_arena* arena, const upy_ins* ins, const upy_decoded* dec, upy_stackrec* stack,
+                        upy_stackinfo* info, void* stream);
 /* Last API-level error message of this thread ("" when none). */
 const char* upy_last_error(void);
 

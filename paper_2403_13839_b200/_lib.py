@@ -42,6 +42,9 @@ def load():
                                         C.POINTER(_abi.UpyOut), C.c_void_p, C.c_size_t, C.c_void_p]
     lib.upy_decode_batch.restype = C.c_int
     lib.upy_decode_batch.argtypes = [C.POINTER(_abi.UpyArena), C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.upy_stackscan_batch.restype = C.c_int
+    lib.upy_stackscan_batch.argtypes = [C.POINTER(_abi.UpyArena), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_void_p]
     lib.upy_pyc_load.restype = C.c_int
     lib.upy_pyc_load.argtypes = [C.POINTER(C.c_void_p), C.POINTER(C.c_uint64), C.c_int64, C.c_int, C.c_int,
                                  C.POINTER(C.POINTER(_abi.UpyPycBatch))]

@@ -104,8 +104,8 @@ class DeviceArena:
     def _memory_slots(self, arena):
         """Concurrent per-thread arenas when the library's default 40 GB budget
         would bind (long objects: C4's ~3 MB slots allow only ~13K threads):
-        size the slot count from the device's free memory instead (55% of it,
-        the text buffer and a second buffer set need the rest).  0 = library
+        size the slot count from the device's free memory instead (70% of it;
+        the text buffer needs the rest).  0 = library
         default.  Measured on C4 (profiles/r02/bench_c4_slots_*.json): 12,288
         slots 2,726 objects/s, 24,576 2,965, 49,152 3,542."""
         sb = default_slot_bytes(arena) + (68 << 10) + 256  # + the slot header (upy.cu SLOT_HEADER)
@@ -116,7 +116,7 @@ class DeviceArena:
         free, _ = self.torch.cuda.mem_get_info(self.device)
         # blocks torch's caching allocator holds but no tensor uses are free to us too
         free += self.torch.cuda.memory_reserved(self.device) - self.torch.cuda.memory_allocated(self.device)
-        return int(max(1, min(want, int(free * 0.55) // sb)))
+        return int(max(1, min(want, int(free * 0.7) // sb)))
 
     def upload(self, stream=None):
         with self.torch.cuda.device(self.device):
@@ -136,6 +136,29 @@ class DeviceArena:
                                               C.c_void_p(self.ws.data_ptr()), C.c_size_t(self.ws_bytes),
                                               C.c_void_p(s.cuda_stream))
         _lib.check(rc, "upy_decompile_batch")
+
+    def stackscan(self, stream=None):
+        """Stack-depth scan (csrc/stackscan_kernel.cu) over the
+        records of the last decode on this workspace.  Returns device tensors
+        (records: int32 view of upy_stackrec per code unit slot, info: upy_stackinfo
+        bytes per object); stream-ordered."""
+        from .arena import DECODED_DTYPE, INS_DTYPE
+
+        torch = self.torch
+        s = stream or torch.cuda.current_stream(self.device)
+        units = self.arena.total_code_units + 1
+        if getattr(self, "_stack", None) is None:
+            self._stack = torch.empty(4 * units, dtype=torch.uint8, device=self.device)
+            self._stack_info = torch.empty(24 * max(self.arena.n_objs, 1), dtype=torch.uint8, device=self.device)
+        ws = self.ws.data_ptr()
+        dec_off = (units * INS_DTYPE.itemsize + 255) & ~255
+        assert DECODED_DTYPE.itemsize == 24
+        with torch.cuda.device(self.device):
+            rc = self.lib.upy_stackscan_batch(C.byref(self.A), C.c_void_p(ws), C.c_void_p(ws + dec_off),
+                                              C.c_void_p(self._stack.data_ptr()),
+                                              C.c_void_p(self._stack_info.data_ptr()), C.c_void_p(s.cuda_stream))
+        _lib.check(rc, "upy_stackscan_batch")
+        return self._stack, self._stack_info
 
     def decoded(self):
         """Per-object decode results (upy_decoded: status, n_instrs, aux) of the

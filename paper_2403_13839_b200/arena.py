@@ -36,6 +36,10 @@ INS_DTYPE = np.dtype([("offset", "<u4"), ("arg", "<u4"), ("opcode", "u1"), ("n_p
                       ("cache_units", "u1"), ("flags", "u1")], align=True)
 DECODED_DTYPE = np.dtype([("status", "<i4"), ("n_instrs", "<i4"), ("aux0", "<i8"), ("aux1", "<i8")],
                          align=True)
+STACKREC_DTYPE = np.dtype([("depth", "<i2"), ("flags", "u1"), ("pad", "u1")])
+STACKINFO_DTYPE = np.dtype([("status", "<i4"), ("n_segments", "<i4"), ("max_depth", "<i4"), ("min_depth", "<i4"),
+                            ("n_pushes", "<i4"), ("n_unknown", "<i4")])
+assert STACKREC_DTYPE.itemsize == 4 and STACKINFO_DTYPE.itemsize == 24
 assert OBJ_DTYPE.itemsize == 152 and CONST_DTYPE.itemsize == 40 and STR_DTYPE.itemsize == 16
 assert INS_DTYPE.itemsize == 12 and DECODED_DTYPE.itemsize == 24
 

@@ -35,8 +35,10 @@ BASE_DEPS = ["../../include/upy.h", "common.h", "optables.h", "unicode_tables.h"
 OBJECTS = {
     "decode_kernel": {"src": "decode_kernel.cu", "deps": BASE_DEPS + ["decode.h"],
                       "flags": COMMON + ["-Xptxas", "-O3"]},
+    "stackscan_kernel": {"src": "stackscan_kernel.cu", "deps": BASE_DEPS + ["stackscan.h"],
+                         "flags": COMMON + ["-Xptxas", "-O3"]},
     "pyc_loader": {"src": "pyc_loader.cpp", "deps": None, "flags": COMMON},
-    "upy": {"src": "upy.cu", "deps": None,  # every header but decode.h (decode_kernel.cu only)
+    "upy": {"src": "upy.cu", "deps": None,  # every header but decode.h / stackscan.h (their own kernels)
             "flags": COMMON + ["-Xcicc", CICC_OPT, "-Xptxas", "-O1"]},
 }
 LINK_FLAGS = [*ARCH, "-shared", "-Xcompiler", "-fPIC"]
@@ -46,7 +48,7 @@ NVCC_FLAGS = OBJECTS["upy"]["flags"]  # kept for tools that print the main flags
 def _obj_deps(spec):
     if spec["deps"] is None:
         deps = [os.path.join(ROOT, "include", "upy.h")]
-        deps += [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith(".h") and f != "decode.h"]
+        deps += [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith(".h") and f not in ("decode.h", "stackscan.h")]
     else:
         deps = [os.path.normpath(os.path.join(CSRC, d)) for d in spec["deps"]]
     return deps + [os.path.join(CSRC, spec["src"])]

@@ -15,8 +15,10 @@
 //     buffered) and leave as ONE bulk shared -> global copy (cp.async.bulk
 //     .global.shared::cta.bulk_group) when the destination is 16-B aligned,
 //     else as coalesced 16-B / 4-B stores.
-// 3.11 objects (inline caches make instruction starts a serial chain) are
-// decoded by lane 0 straight from global memory (decode_scalar).
+// 3.11 objects (inline caches make instruction starts a serial chain) of up to
+// 2 KB come through the same ring whole and are decoded by decode311_body from
+// the gathered copy; larger ones are copied synchronously (decode311_warp), and
+// anything the warp passes reject goes to the scalar decoder (decode_scalar).
 #include <cuda_runtime.h>
 #include "decode.h"
 
@@ -64,9 +66,15 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
-// chunks a <=3.10 object streams through the ring (0: handled from global memory)
+// chunks an object streams through the ring (0: handled from global memory).
+// 3.8-3.10: any size, decoded chunk by chunk.  3.11: objects of at most
+// DSTAGES chunks, which the consumer gathers whole (the inline-cache passes need
+// every unit) -- their code is prefetched by TMA while earlier objects decode.
+#define X11_RING_BYTES (DSTAGES * 512u)
 __device__ __forceinline__ u32 n_chunks(u32 len, u32 minor) {
-  if (minor < 8 || minor > 10 || len == 0 || (len & 1)) return 0;
+  if (len == 0 || (len & 1)) return 0;
+  if (minor == 11) return len <= X11_RING_BYTES ? (len + 511u) >> 9 : 0;
+  if (minor < 8 || minor > 10) return 0;
   return ((len >> 1) + 255) >> 8;
 }
 
@@ -82,15 +90,13 @@ __device__ __forceinline__ u32 n_chunks(u32 len, u32 minor) {
 // decode error or failed speculation sends the object to the scalar
 // reference-order decoder (same shared-memory copy), so error semantics are
 // decode_scalar's.
-__device__ __noinline__ void decode311_warp(const u8* __restrict__ gcode, u32 len, upy_ins* __restrict__ rec,
-                                            upy_decoded* res, const u32* __restrict__ tab, DecWarpSmem& S) {
+// The object's code is in S.out (decode311_warp copies it there from global
+// memory; ring objects are gathered from the TMA stages by the kernel).
+__device__ __noinline__ void decode311_body(u32 len, upy_ins* __restrict__ rec, upy_decoded* res,
+                                            const u32* __restrict__ tab, DecWarpSmem& S) {
   const int lane = threadIdx.x & 31;
   const u32 units = len >> 1;
-  if (lane == 0) bulk_wait_all();  // the staging buffers are about to hold the code
-  __syncwarp();
   uint4* buf = reinterpret_cast<uint4*>(&S.out[0][0]);
-  const uint4* src = reinterpret_cast<const uint4*>(gcode);
-  for (u32 k = lane; k < (len + 15) / 16; k += 32) buf[k] = src[k];
   const u32 nwords = (units + 31) / 32;
   for (u32 k = lane; k < nwords; k += 32) S.cov[k] = S.xs[k] = 0;
   __syncwarp();
@@ -207,6 +213,20 @@ __device__ __noinline__ void decode311_warp(const u8* __restrict__ gcode, u32 le
   __syncwarp();
 }
 
+// 3.11 objects too large for the ring (up to X11_UNITS units): a coalesced
+// synchronous copy into S.out, then the same passes.
+__device__ __noinline__ void decode311_warp(const u8* __restrict__ gcode, u32 len, upy_ins* __restrict__ rec,
+                                            upy_decoded* res, const u32* __restrict__ tab, DecWarpSmem& S) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) bulk_wait_all();  // the staging buffers are about to hold the code
+  __syncwarp();
+  uint4* buf = reinterpret_cast<uint4*>(&S.out[0][0]);
+  const uint4* src = reinterpret_cast<const uint4*>(gcode);
+  for (u32 k = lane; k < (len + 15) / 16; k += 32) buf[k] = src[k];
+  __syncwarp();
+  decode311_body(len, rec, res, tab, S);
+}
+
 __global__ void __launch_bounds__(DWARPS * 32, DEC_MINB) upy_decode_kernel(upy_arena A, upy_ins* __restrict__ ins,
                                                                     upy_decoded* __restrict__ dec) {
   __shared__ u32 tab[4][256];  // 3.8-3.11 opcode tables
@@ -316,6 +336,24 @@ __global__ void __launch_bounds__(DWARPS * 32, DEC_MINB) upy_decode_kernel(upy_a
             dec[o].aux0 = dec[o].aux1 = 0;
           }
         }
+        continue;
+      }
+      if (minor == 11) {
+        // all of the object's chunks are (or will be) in the ring: wait for them,
+        // gather them into S.out, release the stages and refill the ring before
+        // decoding, so the next objects' code is in flight meanwhile
+        for (u32 c = 0; c < nch; c++) {
+          pump();
+          mbar_wait(&S.bar[(cons + c) % DSTAGES], ((cons + c) / DSTAGES) & 1);
+        }
+        if (lane == 0) bulk_wait_all();  // S.out may still be read by a bulk store
+        __syncwarp();
+        uint4* buf = reinterpret_cast<uint4*>(&S.out[0][0]);
+        for (u32 k = lane; k < nch * 32u; k += 32) buf[k] = S.in[(cons + (k >> 5)) % DSTAGES][k & 31];
+        __syncwarp();
+        cons += nch;
+        pump();
+        decode311_body(len, rec, &dec[o], tab[3], S);
         continue;
       }
       ChunkState st;

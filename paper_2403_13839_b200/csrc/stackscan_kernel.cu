@@ -1,0 +1,204 @@
+// stackscan_kernel.cu -- the stack-depth scan (stackscan.h; SURVEY Appendix A;
+// north-star subsystem 3) on sm_100a.
+//
+// HBM-bound streaming kernel over the decode kernel's records: one warp per
+// object at a time (grid-stride over objects), 256 instructions per warp step,
+// 8 consecutive instructions per lane.  A lane loads its 8 records (96 B) as six
+// 16-B streaming loads (record runs start 96-B aligned: code_off is 16-B aligned
+// and the records of unit u live at code_off/2 + u), evaluates each effect from a
+// per-(version, opcode) descriptor table in shared memory (branch-free; the
+// descriptors are derived from the reference-order switch, stackscan.h), scans
+// its 8 values in registers with segment resets, and the warp combines the 32
+// lane aggregates with a segmented shuffle scan carried across steps.  Each lane
+// writes its 8 upy_stackrec (32 B) as two 16-B streaming stores.  Segment starts
+// need "the previous instruction ends a block": from lane - 1 by shuffle, or from
+// the previous step.
+//
+// Algorithmic bytes per object: 12 B x N_instr read + 4 B x N_instr written
+// + the object's decode result (24 B) and summary (24 B) + its code_off (8 B).
+#include <cuda_runtime.h>
+#include "stackscan.h"
+
+#define SS_WARPS 8
+#ifndef SS_MINB
+#define SS_MINB 4  // 4 x 8 warps per SM at <= 64 registers
+#endif
+
+__global__ void __launch_bounds__(SS_WARPS * 32, SS_MINB)
+    upy_stackscan_kernel(upy_arena A, const upy_ins* __restrict__ ins, const upy_decoded* __restrict__ dec,
+                         upy_stackrec* __restrict__ out, upy_stackinfo* __restrict__ info) {
+  __shared__ u32 tab[4][256];
+  for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x)
+    tab[i >> 8][i & 255] = stack_desc(8 + (i >> 8), UPY_OPTABLE_DEV[i >> 8][i & 255]);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const i64 nw = (i64)gridDim.x * SS_WARPS;
+  for (i64 o = (i64)blockIdx.x * SS_WARPS + (threadIdx.x >> 5); o < A.n_objs; o += nw) {
+    const upy_decoded d = dec[o];
+    if (d.status != UPY_ST_OK) {
+      if (lane == 0) {
+        upy_stackinfo si;
+        si.status = d.status;
+        si.n_segments = si.max_depth = si.min_depth = si.n_pushes = si.n_unknown = 0;
+        info[o] = si;
+      }
+      continue;
+    }
+    const u64 base = A.objs[o].code_off >> 1;
+    const u32* tb = tab[(A.objs[o].minor - 8) & 3];
+    const upy_ins* rec = ins + base;
+    upy_stackrec* dst = out + base;
+    const u32 n = (u32)d.n_instrs;
+    // carry from the previous step: inclusive (sum, unknown) at its last
+    // instruction, and whether that instruction ends a block
+    int c_sum = 0, c_unk = 0, c_end = 0;
+    int segs = 0, unks = 0, pushes = 0, mx = 0, mn = 0;
+    for (u32 t0 = 0; t0 < n; t0 += 256) {
+      const u32 i0 = t0 + 8 * (u32)lane;
+      const u32 cnt = i0 < n ? (n - i0 < 8 ? n - i0 : 8) : 0;
+      u32 w[24];  // 8 records x (offset, arg, opcode | prefixes | caches | flags)
+      if (cnt == 8) {
+        const uint4* p = reinterpret_cast<const uint4*>(rec + i0);
+#pragma unroll
+        for (int k = 0; k < 6; k++) {
+          const uint4 v = __ldcs(p + k);
+          w[4 * k] = v.x, w[4 * k + 1] = v.y, w[4 * k + 2] = v.z, w[4 * k + 3] = v.w;
+        }
+      } else {
+        const u32* p = reinterpret_cast<const u32*>(rec + i0);
+#pragma unroll
+        for (int k = 0; k < 24; k++) w[k] = (u32)(k / 3) < cnt ? p[k] : 0u;
+      }
+      int sums[8];
+      u32 segm = 0, unkm = 0, endm = 0;
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        const u32 arg = w[3 * q + 1], meta = w[3 * q + 2];
+        const u32 desc = tb[meta & 0xFF];
+        const bool valid = (u32)q < cnt;
+        const int eff = valid ? stack_desc_effect(desc, arg) : 0;
+        const u32 unk = valid ? (desc >> 15) & 1u : 0u;
+        sums[q] = eff;
+        pushes += (!unk && eff > 0) ? eff : 0;
+        unkm |= unk << q;
+        endm |= (valid ? (desc >> 16) & 1u : 0u) << q;
+        segm |= (valid ? (meta >> 26) & 1u : 0u) << q;  // is_jump_target (flags bit2)
+      }
+      // "the previous instruction ends a block" (or this is the object's first)
+      const u32 up = __shfl_up_sync(0xffffffffu, endm, 1);
+      const u32 prev_end = lane ? (up >> 7) & 1u : (u32)(c_end | (t0 == 0));
+      segm |= ((endm << 1) | prev_end) & (cnt >= 8 ? 0xFFu : ((1u << cnt) - 1u));
+      // in-lane inclusive scan with resets; unknown propagates to the segment's end
+      u32 unk_inc = 0, ru = 0;
+      int run = 0;
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        if ((segm >> q) & 1u) run = 0, ru = 0;
+        run += sums[q];
+        ru |= (unkm >> q) & 1u;
+        sums[q] = run;
+        unk_inc |= ru << q;
+      }
+      // warp segmented scan of the lane aggregates (segment seen, unknown, sum)
+      int a_seg = segm != 0, a_unk = (int)((unk_inc >> 7) & 1u), a_sum = sums[7];
+#pragma unroll
+      for (int dd = 1; dd < 32; dd <<= 1) {
+        const int s2 = __shfl_up_sync(0xffffffffu, a_seg, dd);
+        const int u2 = __shfl_up_sync(0xffffffffu, a_unk, dd);
+        const int v2 = __shfl_up_sync(0xffffffffu, a_sum, dd);
+        if (lane >= dd && !a_seg) {
+          a_sum += v2;
+          a_unk |= u2;
+          a_seg = s2;
+        }
+      }
+      // this lane's incoming prefix (exclusive), seeded with the carry
+      int e_seg = __shfl_up_sync(0xffffffffu, a_seg, 1);
+      int e_unk = __shfl_up_sync(0xffffffffu, a_unk, 1);
+      int e_sum = __shfl_up_sync(0xffffffffu, a_sum, 1);
+      if (lane == 0) e_seg = 0, e_unk = 0, e_sum = 0;
+      if (!e_seg) e_sum += c_sum, e_unk |= c_unk;
+      // positions before the lane's first segment start continue the incoming prefix
+      const u32 first_seg = segm ? (u32)(__ffs((int)segm) - 1) : 8u;
+      u32 words[8];
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        int v = sums[q];
+        u32 unk = (unk_inc >> q) & 1u;
+        if ((u32)q < first_seg) {
+          v += e_sum;
+          unk |= (u32)e_unk;
+        }
+        if ((u32)q < cnt && !unk) {
+          mx = v > mx ? v : mx;
+          mn = v < mn ? v : mn;
+        }
+        const int cl = v > 32767 ? 32767 : v < -32768 ? -32768 : v;
+        words[q] = ((u32)cl & 0xFFFFu) |
+                   ((((segm >> q) & 1u) * SS_SEG_START | unk * SS_UNKNOWN | ((endm >> q) & 1u) * SS_ENDER) << 16);
+        sums[q] = v;
+      }
+      segs += __popc(segm);
+      unks += __popc(unkm);
+      if (cnt == 8) {
+        uint4* p = reinterpret_cast<uint4*>(dst + i0);
+        __stcs(p, make_uint4(words[0], words[1], words[2], words[3]));
+        __stcs(p + 1, make_uint4(words[4], words[5], words[6], words[7]));
+      } else {
+        u32* p = reinterpret_cast<u32*>(dst + i0);
+#pragma unroll
+        for (int q = 0; q < 8; q++)
+          if ((u32)q < cnt) p[q] = words[q];
+      }
+      // carry: the step's last real instruction
+      const u32 last_i = t0 + 256 <= n ? t0 + 255 : n - 1;
+      const int owner = (int)((last_i - t0) >> 3);
+      const int q_last = (int)((last_i - t0) & 7);
+      int l_sum = 0, l_unk = 0, l_end = 0;
+#pragma unroll
+      for (int q = 0; q < 8; q++)
+        if (q == q_last) {
+          l_sum = sums[q];
+          l_unk = (int)((words[q] >> 17) & 1u);
+          l_end = (int)((endm >> q) & 1u);
+        }
+      c_sum = __shfl_sync(0xffffffffu, l_sum, owner);
+      c_unk = __shfl_sync(0xffffffffu, l_unk, owner);
+      c_end = __shfl_sync(0xffffffffu, l_end, owner);
+    }
+#pragma unroll
+    for (int dd = 16; dd; dd >>= 1) {
+      segs += __shfl_xor_sync(0xffffffffu, segs, dd);
+      unks += __shfl_xor_sync(0xffffffffu, unks, dd);
+      pushes += __shfl_xor_sync(0xffffffffu, pushes, dd);
+      const int a = __shfl_xor_sync(0xffffffffu, mx, dd);
+      const int b = __shfl_xor_sync(0xffffffffu, mn, dd);
+      mx = a > mx ? a : mx;
+      mn = b < mn ? b : mn;
+    }
+    if (lane == 0) {
+      upy_stackinfo si;
+      si.status = d.status;
+      si.n_segments = segs;
+      si.n_unknown = unks;
+      si.n_pushes = pushes;
+      si.max_depth = mx;
+      si.min_depth = mn;
+      info[o] = si;
+    }
+  }
+}
+
+extern "C" int upy_stackscan_batch(const upy_arena* arena, const upy_ins* ins, const upy_decoded* dec,
+                                   upy_stackrec* stack, upy_stackinfo* info, void* stream) {
+  if (!arena || !ins || !dec || !stack || !info) return 1;
+  if (arena->n_objs == 0) return 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  i64 blocks = (arena->n_objs + SS_WARPS - 1) / SS_WARPS;
+  const i64 cap = (i64)sms * SS_MINB;
+  if (blocks > cap) blocks = cap;
+  upy_stackscan_kernel<<<(unsigned)blocks, SS_WARPS * 32, 0, (cudaStream_t)stream>>>(*arena, ins, dec, stack, info);
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}

@@ -239,6 +239,8 @@ size_t upy_abi_sizeof(int which) {
     case 5: return sizeof(upy_out);
     case 6: return sizeof(upy_ins);
     case 7: return sizeof(upy_decoded);
+    case 8: return sizeof(upy_stackrec);
+    case 9: return sizeof(upy_stackinfo);
   }
   return 0;
 }

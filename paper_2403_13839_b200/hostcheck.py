@@ -88,3 +88,16 @@ def decompile_many(codes, style=None, function_tree=False):
     from .arena import pack
     res = run(pack(codes), style, function_tree=function_tree)
     return [s if st == 0 else make_exception(st, s, aux) for st, s, aux in res]
+
+
+def stackscan(arena):
+    """Stack-depth scan on the host (csrc/stackscan.h, after decode_scalar):
+    (records laid out like the device's, per-object summaries)."""
+    from .arena import STACKINFO_DTYPE, STACKREC_DTYPE
+
+    L = lib()
+    A = _abi.arena_struct(arena, arena.blob.ctypes.data)
+    out = np.zeros(arena.total_code_units + 1, dtype=STACKREC_DTYPE)
+    info = np.zeros(arena.n_objs, dtype=STACKINFO_DTYPE)
+    L.upyh_stackscan(C.byref(A), out.ctypes.data_as(C.c_void_p), info.ctypes.data_as(C.c_void_p))
+    return out, info

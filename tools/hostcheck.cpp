@@ -10,6 +10,7 @@
 #include "../paper_2403_13839_b200/csrc/pipeline.h"
 #include "../paper_2403_13839_b200/csrc/decode.h"
 #include "../paper_2403_13839_b200/csrc/dot.h"
+#include "../paper_2403_13839_b200/csrc/stackscan.h"
 
 extern "C" int upyh_decompile(const upy_arena* A, int header, const char* indent, int indent_len, const char* tool,
                               int tool_len, uint64_t arena_bytes, uint8_t* text, uint64_t text_cap,
@@ -124,3 +125,21 @@ extern "C" int upyh_arena_peaks(const upy_arena* A, uint64_t arena_bytes, uint64
   }
   return 0;
 }
+
+// Stack-depth scan (csrc/stackscan.h) of every object after the scalar decoder:
+// the reference-order oracle of the device's segmented warp scan.
+extern "C" int upyh_stackscan(const upy_arena* A, upy_stackrec* out, upy_stackinfo* info) {
+  std::vector<upy_ins> ins(A->total_code_units + 1);
+  for (int64_t o = 0; o < A->n_objs; o++) {
+    const upy_obj* ob = &A->objs[o];
+    upy_decoded d;
+    upy_ins* rec = ins.data() + (ob->code_off >> 1);
+    decode_scalar(A->bytes + ob->code_off, ob->code_len, (int)ob->minor, rec, &d);
+    memset(&info[o], 0, sizeof info[o]);
+    info[o].status = d.status;
+    if (d.status == UPY_ST_OK) stackscan_scalar(rec, d.n_instrs, (int)ob->minor, out + (ob->code_off >> 1), &info[o]);
+  }
+  return 0;
+}
+
+extern "C" uint64_t upyh_stack_desc_selfcheck(uint32_t n_args) { return stack_desc_selfcheck(n_args); }
