@@ -44,6 +44,20 @@ class BatchResult:
         return int(self.status[i]), bytes(s).decode("utf-8", "surrogatepass")
 
     def values(self):
+        """One str (or exception instance) per root.  When the whole text buffer is
+        ASCII (the usual case) it is decoded once and sliced by the byte offsets,
+        instead of one decode per root."""
+        tb = self.text.tobytes() if len(self.text) else b""
+        if tb.isascii():
+            whole = tb.decode("ascii")
+            offs = self.text_off.tolist()
+            lens = self.text_len.tolist()
+            sts = self.status.tolist()
+            out = [whole[o:o + n] for o, n in zip(offs, lens)]
+            for i, st in enumerate(sts):
+                if st != ST_OK:
+                    out[i] = make_exception(st, out[i], self.aux[i])
+            return out
         out = []
         for i in range(len(self.status)):
             st, s = self.item(i)

@@ -2,7 +2,8 @@
 // north-star subsystem 3) on sm_100a.
 //
 // HBM-bound streaming kernel over the decode kernel's records: one warp per
-// object at a time (grid-stride over objects), 256 instructions per warp step,
+// group of 32 consecutive objects (headers loaded one per lane, summaries stored
+// one per lane), one object at a time, 256 instructions per warp step,
 // 8 consecutive instructions per lane.  A lane loads its 8 records (96 B) as six
 // 16-B streaming loads (record runs start 96-B aligned: code_off is 16-B aligned
 // and the records of unit u live at code_off/2 + u), evaluates each effect from a
@@ -33,159 +34,161 @@ __global__ void __launch_bounds__(SS_WARPS * 32, SS_MINB)
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const i64 nw = (i64)gridDim.x * SS_WARPS;
-  for (i64 o = (i64)blockIdx.x * SS_WARPS + (threadIdx.x >> 5); o < A.n_objs; o += nw) {
-    const upy_decoded d = dec[o];
-    if (d.status != UPY_ST_OK) {
-      if (lane == 0) {
-        upy_stackinfo si;
-        si.status = d.status;
-        si.n_segments = si.max_depth = si.min_depth = si.n_pushes = si.n_unknown = 0;
-        info[o] = si;
-      }
-      continue;
+  const i64 n_groups = (A.n_objs + 31) >> 5;
+  // groups of 32 consecutive objects per warp: lane j loads object j's decode
+  // result and code offset (one round of loads per 32 objects), the warp scans the
+  // objects one after another, and lane j keeps object j's summary for one
+  // coalesced store at the end of the group
+  for (i64 g = (i64)blockIdx.x * SS_WARPS + (threadIdx.x >> 5); g < n_groups; g += nw) {
+    const i64 my_o = g * 32 + lane;
+    int h_status = UPY_ST_INTERNAL, h_n = 0;
+    u64 h_base = 0;
+    u32 h_minor = 8;
+    if (my_o < A.n_objs) {
+      const upy_decoded d = dec[my_o];
+      h_status = d.status;
+      h_n = d.n_instrs;
+      h_base = A.objs[my_o].code_off >> 1;
+      h_minor = A.objs[my_o].minor;
     }
-    const u64 base = A.objs[o].code_off >> 1;
-    const u32* tb = tab[(A.objs[o].minor - 8) & 3];
-    const upy_ins* rec = ins + base;
-    upy_stackrec* dst = out + base;
-    const u32 n = (u32)d.n_instrs;
-    // carry from the previous step: inclusive (sum, unknown) at its last
-    // instruction, and whether that instruction ends a block
-    int c_sum = 0, c_unk = 0, c_end = 0;
-    int segs = 0, unks = 0, pushes = 0, mx = 0, mn = 0;
-    for (u32 t0 = 0; t0 < n; t0 += 256) {
-      const u32 i0 = t0 + 8 * (u32)lane;
-      const u32 cnt = i0 < n ? (n - i0 < 8 ? n - i0 : 8) : 0;
-      u32 w[24];  // 8 records x (offset, arg, opcode | prefixes | caches | flags)
-      if (cnt == 8) {
-        const uint4* p = reinterpret_cast<const uint4*>(rec + i0);
+    upy_stackinfo mine;
+    mine.status = h_status;
+    mine.n_segments = mine.max_depth = mine.min_depth = mine.n_pushes = mine.n_unknown = 0;
+    const int cnt_objs = (int)(A.n_objs - g * 32 < 32 ? A.n_objs - g * 32 : 32);
+    for (int j = 0; j < cnt_objs; j++) {
+      const int status = __shfl_sync(0xffffffffu, h_status, j);
+      if (status != UPY_ST_OK) continue;
+      const u32 n = (u32)__shfl_sync(0xffffffffu, h_n, j);
+      const u64 base = __shfl_sync(0xffffffffu, h_base, j);
+      const u32* tb = tab[(__shfl_sync(0xffffffffu, h_minor, j) - 8) & 3];
+      const upy_ins* rec = ins + base;
+      upy_stackrec* dst = out + base;
+      // carry from the previous step: inclusive (sum, unknown) at its last
+      // instruction, and whether that instruction ends a block
+      int c_sum = 0, c_unk = 0, c_end = 0;
+      int segs = 0, unks = 0, pushes = 0, mx = 0, mn = 0;
+      for (u32 t0 = 0; t0 < n; t0 += 256) {
+        const u32 i0 = t0 + 8 * (u32)lane;
+        const u32 cnt = i0 < n ? (n - i0 < 8 ? n - i0 : 8) : 0;
+        u32 w[24];  // 8 records x (offset, arg, opcode | prefixes | caches | flags)
+        if (cnt == 8) {
+          const uint4* p = reinterpret_cast<const uint4*>(rec + i0);
 #pragma unroll
-        for (int k = 0; k < 6; k++) {
-          const uint4 v = __ldcs(p + k);
-          w[4 * k] = v.x, w[4 * k + 1] = v.y, w[4 * k + 2] = v.z, w[4 * k + 3] = v.w;
+          for (int k = 0; k < 6; k++) {
+            const uint4 v = __ldcs(p + k);
+            w[4 * k] = v.x, w[4 * k + 1] = v.y, w[4 * k + 2] = v.z, w[4 * k + 3] = v.w;
+          }
+        } else {
+          const u32* p = reinterpret_cast<const u32*>(rec + i0);
+#pragma unroll
+          for (int k = 0; k < 24; k++) w[k] = (u32)(k / 3) < cnt ? p[k] : 0u;
         }
-      } else {
-        const u32* p = reinterpret_cast<const u32*>(rec + i0);
+        int sums[8];
+        u32 segm = 0, unkm = 0, endm = 0;
 #pragma unroll
-        for (int k = 0; k < 24; k++) w[k] = (u32)(k / 3) < cnt ? p[k] : 0u;
-      }
-      int sums[8];
-      u32 segm = 0, unkm = 0, endm = 0;
+        for (int q = 0; q < 8; q++) {
+          const u32 arg = w[3 * q + 1], meta = w[3 * q + 2];
+          const u32 desc = tb[meta & 0xFF];
+          const bool valid = (u32)q < cnt;
+          const int eff = valid ? stack_desc_effect(desc, arg) : 0;
+          const u32 unk = valid ? (desc >> 15) & 1u : 0u;
+          sums[q] = eff;
+          pushes += (!unk && eff > 0) ? eff : 0;
+          unkm |= unk << q;
+          endm |= (valid ? (desc >> 16) & 1u : 0u) << q;
+          segm |= (valid ? (meta >> 26) & 1u : 0u) << q;  // is_jump_target (flags bit2)
+        }
+        // "the previous instruction ends a block" (or this is the object's first)
+        const u32 up = __shfl_up_sync(0xffffffffu, endm, 1);
+        const u32 prev_end = lane ? (up >> 7) & 1u : (u32)(c_end | (t0 == 0));
+        segm |= ((endm << 1) | prev_end) & (cnt >= 8 ? 0xFFu : ((1u << cnt) - 1u));
+        // in-lane inclusive scan with resets; unknown propagates to the segment's end
+        u32 unk_inc = 0, ru = 0;
+        int run = 0;
 #pragma unroll
-      for (int q = 0; q < 8; q++) {
-        const u32 arg = w[3 * q + 1], meta = w[3 * q + 2];
-        const u32 desc = tb[meta & 0xFF];
-        const bool valid = (u32)q < cnt;
-        const int eff = valid ? stack_desc_effect(desc, arg) : 0;
-        const u32 unk = valid ? (desc >> 15) & 1u : 0u;
-        sums[q] = eff;
-        pushes += (!unk && eff > 0) ? eff : 0;
-        unkm |= unk << q;
-        endm |= (valid ? (desc >> 16) & 1u : 0u) << q;
-        segm |= (valid ? (meta >> 26) & 1u : 0u) << q;  // is_jump_target (flags bit2)
-      }
-      // "the previous instruction ends a block" (or this is the object's first)
-      const u32 up = __shfl_up_sync(0xffffffffu, endm, 1);
-      const u32 prev_end = lane ? (up >> 7) & 1u : (u32)(c_end | (t0 == 0));
-      segm |= ((endm << 1) | prev_end) & (cnt >= 8 ? 0xFFu : ((1u << cnt) - 1u));
-      // in-lane inclusive scan with resets; unknown propagates to the segment's end
-      u32 unk_inc = 0, ru = 0;
-      int run = 0;
+        for (int q = 0; q < 8; q++) {
+          if ((segm >> q) & 1u) run = 0, ru = 0;
+          run += sums[q];
+          ru |= (unkm >> q) & 1u;
+          sums[q] = run;
+          unk_inc |= ru << q;
+        }
+        // warp segmented scan of the lane aggregates (segment seen, unknown, sum)
+        int a_seg = segm != 0, a_unk = (int)((unk_inc >> 7) & 1u), a_sum = sums[7];
 #pragma unroll
-      for (int q = 0; q < 8; q++) {
-        if ((segm >> q) & 1u) run = 0, ru = 0;
-        run += sums[q];
-        ru |= (unkm >> q) & 1u;
-        sums[q] = run;
-        unk_inc |= ru << q;
-      }
-      // warp segmented scan of the lane aggregates (segment seen, unknown, sum)
-      int a_seg = segm != 0, a_unk = (int)((unk_inc >> 7) & 1u), a_sum = sums[7];
+        for (int dd = 1; dd < 32; dd <<= 1) {
+          const int s2 = __shfl_up_sync(0xffffffffu, a_seg, dd);
+          const int u2 = __shfl_up_sync(0xffffffffu, a_unk, dd);
+          const int v2 = __shfl_up_sync(0xffffffffu, a_sum, dd);
+          if (lane >= dd && !a_seg) {
+            a_sum += v2;
+            a_unk |= u2;
+            a_seg = s2;
+          }
+        }
+        // this lane's incoming prefix (exclusive), seeded with the carry
+        int e_seg = __shfl_up_sync(0xffffffffu, a_seg, 1);
+        int e_unk = __shfl_up_sync(0xffffffffu, a_unk, 1);
+        int e_sum = __shfl_up_sync(0xffffffffu, a_sum, 1);
+        if (lane == 0) e_seg = 0, e_unk = 0, e_sum = 0;
+        if (!e_seg) e_sum += c_sum, e_unk |= c_unk;
+        // positions before the lane's first segment start continue the incoming prefix
+        const u32 first_seg = segm ? (u32)(__ffs((int)segm) - 1) : 8u;
+        u32 words[8];
 #pragma unroll
-      for (int dd = 1; dd < 32; dd <<= 1) {
-        const int s2 = __shfl_up_sync(0xffffffffu, a_seg, dd);
-        const int u2 = __shfl_up_sync(0xffffffffu, a_unk, dd);
-        const int v2 = __shfl_up_sync(0xffffffffu, a_sum, dd);
-        if (lane >= dd && !a_seg) {
-          a_sum += v2;
-          a_unk |= u2;
-          a_seg = s2;
+        for (int q = 0; q < 8; q++) {
+          int v = sums[q];
+          u32 unk = (unk_inc >> q) & 1u;
+          if ((u32)q < first_seg) {
+            v += e_sum;
+            unk |= (u32)e_unk;
+          }
+          if ((u32)q < cnt && !unk) {
+            mx = v > mx ? v : mx;
+            mn = v < mn ? v : mn;
+          }
+          const int cl = v > 32767 ? 32767 : v < -32768 ? -32768 : v;
+          words[q] = ((u32)cl & 0xFFFFu) |
+                     ((((segm >> q) & 1u) * SS_SEG_START | unk * SS_UNKNOWN | ((endm >> q) & 1u) * SS_ENDER) << 16);
+          sums[q] = v;
+        }
+        segs += __popc(segm);
+        unks += __popc(unkm);
+        if (cnt == 8) {
+          uint4* p = reinterpret_cast<uint4*>(dst + i0);
+          __stcs(p, make_uint4(words[0], words[1], words[2], words[3]));
+          __stcs(p + 1, make_uint4(words[4], words[5], words[6], words[7]));
+        } else {
+          u32* p = reinterpret_cast<u32*>(dst + i0);
+#pragma unroll
+          for (int q = 0; q < 8; q++)
+            if ((u32)q < cnt) p[q] = words[q];
+        }
+        if (t0 + 256 < n) {  // carry: the step's last instruction (lane 31, q = 7)
+          c_sum = __shfl_sync(0xffffffffu, sums[7], 31);
+          c_unk = __shfl_sync(0xffffffffu, (int)((words[7] >> 17) & 1u), 31);
+          c_end = __shfl_sync(0xffffffffu, (int)((endm >> 7) & 1u), 31);
         }
       }
-      // this lane's incoming prefix (exclusive), seeded with the carry
-      int e_seg = __shfl_up_sync(0xffffffffu, a_seg, 1);
-      int e_unk = __shfl_up_sync(0xffffffffu, a_unk, 1);
-      int e_sum = __shfl_up_sync(0xffffffffu, a_sum, 1);
-      if (lane == 0) e_seg = 0, e_unk = 0, e_sum = 0;
-      if (!e_seg) e_sum += c_sum, e_unk |= c_unk;
-      // positions before the lane's first segment start continue the incoming prefix
-      const u32 first_seg = segm ? (u32)(__ffs((int)segm) - 1) : 8u;
-      u32 words[8];
 #pragma unroll
-      for (int q = 0; q < 8; q++) {
-        int v = sums[q];
-        u32 unk = (unk_inc >> q) & 1u;
-        if ((u32)q < first_seg) {
-          v += e_sum;
-          unk |= (u32)e_unk;
-        }
-        if ((u32)q < cnt && !unk) {
-          mx = v > mx ? v : mx;
-          mn = v < mn ? v : mn;
-        }
-        const int cl = v > 32767 ? 32767 : v < -32768 ? -32768 : v;
-        words[q] = ((u32)cl & 0xFFFFu) |
-                   ((((segm >> q) & 1u) * SS_SEG_START | unk * SS_UNKNOWN | ((endm >> q) & 1u) * SS_ENDER) << 16);
-        sums[q] = v;
+      for (int dd = 16; dd; dd >>= 1) {
+        segs += __shfl_xor_sync(0xffffffffu, segs, dd);
+        unks += __shfl_xor_sync(0xffffffffu, unks, dd);
+        pushes += __shfl_xor_sync(0xffffffffu, pushes, dd);
+        const int a = __shfl_xor_sync(0xffffffffu, mx, dd);
+        const int b = __shfl_xor_sync(0xffffffffu, mn, dd);
+        mx = a > mx ? a : mx;
+        mn = b < mn ? b : mn;
       }
-      segs += __popc(segm);
-      unks += __popc(unkm);
-      if (cnt == 8) {
-        uint4* p = reinterpret_cast<uint4*>(dst + i0);
-        __stcs(p, make_uint4(words[0], words[1], words[2], words[3]));
-        __stcs(p + 1, make_uint4(words[4], words[5], words[6], words[7]));
-      } else {
-        u32* p = reinterpret_cast<u32*>(dst + i0);
-#pragma unroll
-        for (int q = 0; q < 8; q++)
-          if ((u32)q < cnt) p[q] = words[q];
+      if (lane == j) {
+        mine.n_segments = segs;
+        mine.n_unknown = unks;
+        mine.n_pushes = pushes;
+        mine.max_depth = mx;
+        mine.min_depth = mn;
       }
-      // carry: the step's last real instruction
-      const u32 last_i = t0 + 256 <= n ? t0 + 255 : n - 1;
-      const int owner = (int)((last_i - t0) >> 3);
-      const int q_last = (int)((last_i - t0) & 7);
-      int l_sum = 0, l_unk = 0, l_end = 0;
-#pragma unroll
-      for (int q = 0; q < 8; q++)
-        if (q == q_last) {
-          l_sum = sums[q];
-          l_unk = (int)((words[q] >> 17) & 1u);
-          l_end = (int)((endm >> q) & 1u);
-        }
-      c_sum = __shfl_sync(0xffffffffu, l_sum, owner);
-      c_unk = __shfl_sync(0xffffffffu, l_unk, owner);
-      c_end = __shfl_sync(0xffffffffu, l_end, owner);
     }
-#pragma unroll
-    for (int dd = 16; dd; dd >>= 1) {
-      segs += __shfl_xor_sync(0xffffffffu, segs, dd);
-      unks += __shfl_xor_sync(0xffffffffu, unks, dd);
-      pushes += __shfl_xor_sync(0xffffffffu, pushes, dd);
-      const int a = __shfl_xor_sync(0xffffffffu, mx, dd);
-      const int b = __shfl_xor_sync(0xffffffffu, mn, dd);
-      mx = a > mx ? a : mx;
-      mn = b < mn ? b : mn;
-    }
-    if (lane == 0) {
-      upy_stackinfo si;
-      si.status = d.status;
-      si.n_segments = segs;
-      si.n_unknown = unks;
-      si.n_pushes = pushes;
-      si.max_depth = mx;
-      si.min_depth = mn;
-      info[o] = si;
-    }
+    if (my_o < A.n_objs) info[my_o] = mine;
   }
 }
 
@@ -196,7 +199,8 @@ extern "C" int upy_stackscan_batch(const upy_arena* arena, const upy_ins* ins, c
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  i64 blocks = (arena->n_objs + SS_WARPS - 1) / SS_WARPS;
+  const i64 groups = (arena->n_objs + 31) / 32;  // one warp per 32 consecutive objects
+  i64 blocks = (groups + SS_WARPS - 1) / SS_WARPS;
   const i64 cap = (i64)sms * SS_MINB;
   if (blocks > cap) blocks = cap;
   upy_stackscan_kernel<<<(unsigned)blocks, SS_WARPS * 32, 0, (cudaStream_t)stream>>>(*arena, ins, dec, stack, info);

@@ -97,3 +97,15 @@ def test_gpu_c4_10k_unit_pool_matches_reference_digests(pool, n):
         assert ok == (want["status"][i] == "ok"), (i, g)
         text = g if ok else str(g)
         assert hashlib.sha256(text.encode("utf-8", "surrogatepass")).hexdigest()[:24] == want["sha"][i], i
+
+
+def test_gpu_sharded_decompile_many_matches_reference():
+    """decompile_many(devices=[...]) partitions the roots (shard_plan, balanced by
+    code bytes), runs one host thread per device and gathers in input order.  The
+    box has one GPU, so both shards run on cuda:0 from two threads at once (the
+    C ABI's per-device setup and stream-ordered launches must be thread-safe)."""
+    from paper_2403_13839_b200 import api
+
+    recs = [r for r in golden_cases(["c2", "c4", "fuzz"]) if not r.get("style")]
+    got = [outcome(v) for v in api.decompile_many(inputs(recs), devices=["cuda:0", "cuda:0", "cuda:0"])]
+    assert not mismatches(recs, got)

@@ -11,6 +11,6 @@ mkdir -p $P/_variants
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -diag-suppress 550 \
   -Xcicc ${CICC_OPT:--O3} -Xptxas ${PTXAS_OPT:--O1} "$@" -c -o $P/_variants/$name.o $P/csrc/upy.cu
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -Xcompiler -fPIC -o $P/_variants/$name.so \
-  $P/_build/decode_kernel.o $P/_build/pyc_loader.o $P/_variants/$name.o
+  $(ls $P/_build/*.o | grep -v '/upy.o$') $P/_variants/$name.o
 rm -f $P/_variants/$name.o
 echo built $P/_variants/$name.so
