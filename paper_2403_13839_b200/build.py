@@ -33,9 +33,9 @@ CICC_OPT = "-O1" if os.environ.get("UPY_FAST_BUILD") else "-O3"
 COMMON = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-diag-suppress", "550"]
 BASE_DEPS = ["../../include/upy.h", "common.h", "optables.h", "unicode_tables.h"]
 OBJECTS = {
-    "decode_kernel": {"src": "decode_kernel.cu", "deps": BASE_DEPS + ["decode.h"],
+    "decode_kernel": {"src": "decode_kernel.cu", "deps": BASE_DEPS + ["decode.h", "tma.h"],
                       "flags": COMMON + ["-Xptxas", "-O3"]},
-    "stackscan_kernel": {"src": "stackscan_kernel.cu", "deps": BASE_DEPS + ["stackscan.h"],
+    "stackscan_kernel": {"src": "stackscan_kernel.cu", "deps": BASE_DEPS + ["stackscan.h", "tma.h"],
                          "flags": COMMON + ["-Xptxas", "-O3"]},
     "pyc_loader": {"src": "pyc_loader.cpp", "deps": None, "flags": COMMON},
     "upy": {"src": "upy.cu", "deps": None,  # every header but decode.h / stackscan.h (their own kernels)
@@ -48,7 +48,7 @@ NVCC_FLAGS = OBJECTS["upy"]["flags"]  # kept for tools that print the main flags
 def _obj_deps(spec):
     if spec["deps"] is None:
         deps = [os.path.join(ROOT, "include", "upy.h")]
-        deps += [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith(".h") and f not in ("decode.h", "stackscan.h")]
+        deps += [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith(".h") and f not in ("decode.h", "stackscan.h", "tma.h")]
     else:
         deps = [os.path.normpath(os.path.join(CSRC, d)) for d in spec["deps"]]
     return deps + [os.path.join(CSRC, spec["src"])]

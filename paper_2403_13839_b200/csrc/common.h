@@ -331,15 +331,8 @@ HD inline Vec<T>* vcopy(Dc* C, const Vec<T>* src, u32 lo = 0, u32 hi = 0xFFFFFFF
   if (lo == 0 && hi) {
     copy16(v->d, src->d, (u64)hi * sizeof(T));
   } else {
-#ifdef UPY_HOIST
-    T* dd = v->d;
-    const T* sd = src->d;
-#pragma unroll 1
-    for (u32 i = lo; i < hi; i++) dd[i - lo] = sd[i];
-#else
 #pragma unroll 1
     for (u32 i = lo; i < hi; i++) v->d[i - lo] = src->d[i];
-#endif
   }
   v->n = hi - lo;
   return v;
@@ -350,18 +343,8 @@ HD inline void vextend(Dc* C, Vec<T>* dst, const Vec<T>* src, u32 lo = 0, u32 hi
   if (hi > src->n) hi = src->n;
   if (lo >= hi) return;
   if (dst->n + (hi - lo) > dst->cap && !vgrow(C, dst, dst->n + (hi - lo))) return;
-#ifdef UPY_HOIST
-  // element pointers in registers: the stores cannot be seen to leave dst->d /
-  // dst->n / src->d alone, so the plain loop reloads all three per element
-  T* dd = dst->d + dst->n;
-  const T* sd = src->d;
-#pragma unroll 1
-  for (u32 i = lo; i < hi; i++) dd[i - lo] = sd[i];
-  dst->n += hi - lo;
-#else
 #pragma unroll 1
   for (u32 i = lo; i < hi; i++) dst->d[dst->n++] = src->d[i];
-#endif
 }
 template <class T>
 HD inline T vlast(const Vec<T>* v) { return v->d[v->n - 1]; }

@@ -11,7 +11,10 @@
 // descriptors are derived from the reference-order switch, stackscan.h), scans
 // its 8 values in registers with segment resets, and the warp combines the 32
 // lane aggregates with a segmented shuffle scan carried across steps.  Each lane
-// writes its 8 upy_stackrec (32 B) as two 16-B streaming stores.  Segment starts
+// writes its 8 upy_stackrec (32 B) as two 16-B streaming stores.  An object's
+// first 256 records arrive in a per-warp shared-memory stage by one TMA bulk copy
+// (cp.async.bulk + mbarrier) issued while the previous object is scanned, so the
+// load latency of short objects (C3: ~200 records) is hidden.  Segment starts
 // need "the previous instruction ends a block": from lane - 1 by shuffle, or from
 // the previous step.
 //
@@ -19,32 +22,52 @@
 // + the object's decode result (24 B) and summary (24 B) + its code_off (8 B).
 #include <cuda_runtime.h>
 #include "stackscan.h"
+#include "tma.h"
 
-#define SS_WARPS 8
+#define SS_WARPS 8  // 8 x 3 KB record stages + 4 KB descriptor table per block
 #ifndef SS_MINB
 #define SS_MINB 4  // 4 x 8 warps per SM at <= 64 registers
 #endif
 
 __global__ void __launch_bounds__(SS_WARPS * 32, SS_MINB)
     upy_stackscan_kernel(upy_arena A, const upy_ins* __restrict__ ins, const upy_decoded* __restrict__ dec,
-                         upy_stackrec* __restrict__ out, upy_stackinfo* __restrict__ info) {
+                         upy_stackrec* __restrict__ out, upy_stackinfo* __restrict__ info, int gshift) {
   __shared__ u32 tab[4][256];
+  // per warp: one 256-record stage the next object's first step lands in by TMA
+  // while the current object is scanned from registers
+  __shared__ __align__(128) upy_ins stage[SS_WARPS][256];
+  __shared__ unsigned long long bar[SS_WARPS];
   for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x)
     tab[i >> 8][i & 255] = stack_desc(8 + (i >> 8), UPY_OPTABLE_DEV[i >> 8][i & 255]);
-  __syncthreads();
   const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    mbar_init(&bar[wid], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  u32 phase = 0;
+  auto prefetch = [&](u64 rbase, u32 n) {  // lane 0: the object's first <= 256 records
+    if (lane == 0) {
+      const u32 bytes = ((n < 256 ? n : 256) * 12u + 15u) & ~15u;
+      fence_async_smem();
+      mbar_expect_tx(&bar[wid], bytes);
+      bulk_g2s(&stage[wid][0], ins + rbase, bytes, &bar[wid]);
+    }
+  };
   const i64 nw = (i64)gridDim.x * SS_WARPS;
-  const i64 n_groups = (A.n_objs + 31) >> 5;
+  const int gsize = 1 << gshift;  // objects per group (32 for short objects, fewer for long)
+  const i64 n_groups = (A.n_objs + gsize - 1) >> gshift;
   // groups of 32 consecutive objects per warp: lane j loads object j's decode
   // result and code offset (one round of loads per 32 objects), the warp scans the
   // objects one after another, and lane j keeps object j's summary for one
   // coalesced store at the end of the group
   for (i64 g = (i64)blockIdx.x * SS_WARPS + (threadIdx.x >> 5); g < n_groups; g += nw) {
-    const i64 my_o = g * 32 + lane;
+    const i64 my_o = g * gsize + lane;
     int h_status = UPY_ST_INTERNAL, h_n = 0;
     u64 h_base = 0;
     u32 h_minor = 8;
-    if (my_o < A.n_objs) {
+    if (lane < gsize && my_o < A.n_objs) {
       const upy_decoded d = dec[my_o];
       h_status = d.status;
       h_n = d.n_instrs;
@@ -54,10 +77,15 @@ __global__ void __launch_bounds__(SS_WARPS * 32, SS_MINB)
     upy_stackinfo mine;
     mine.status = h_status;
     mine.n_segments = mine.max_depth = mine.min_depth = mine.n_pushes = mine.n_unknown = 0;
-    const int cnt_objs = (int)(A.n_objs - g * 32 < 32 ? A.n_objs - g * 32 : 32);
-    for (int j = 0; j < cnt_objs; j++) {
-      const int status = __shfl_sync(0xffffffffu, h_status, j);
-      if (status != UPY_ST_OK) continue;
+    // objects of the group with records, and the first one's prefetch
+    u32 todo = __ballot_sync(0xffffffffu, h_status == UPY_ST_OK && h_n > 0);
+    if (todo) {
+      const int f = __ffs((int)todo) - 1;
+      prefetch(__shfl_sync(0xffffffffu, h_base, f), (u32)__shfl_sync(0xffffffffu, h_n, f));
+    }
+    while (todo) {
+      const int j = __ffs((int)todo) - 1;
+      todo &= todo - 1;
       const u32 n = (u32)__shfl_sync(0xffffffffu, h_n, j);
       const u64 base = __shfl_sync(0xffffffffu, h_base, j);
       const u32* tb = tab[(__shfl_sync(0xffffffffu, h_minor, j) - 8) & 3];
@@ -71,7 +99,28 @@ __global__ void __launch_bounds__(SS_WARPS * 32, SS_MINB)
         const u32 i0 = t0 + 8 * (u32)lane;
         const u32 cnt = i0 < n ? (n - i0 < 8 ? n - i0 : 8) : 0;
         u32 w[24];  // 8 records x (offset, arg, opcode | prefixes | caches | flags)
-        if (cnt == 8) {
+        if (t0 == 0) {
+          // first step: from the TMA stage; then the stage takes the next object's
+          mbar_wait(&bar[wid], phase);
+          phase ^= 1;
+          const u32* sp = reinterpret_cast<const u32*>(&stage[wid][8 * lane]);
+          if (cnt == 8) {
+            const uint4* p4 = reinterpret_cast<const uint4*>(sp);
+#pragma unroll
+            for (int k = 0; k < 6; k++) {
+              const uint4 v = p4[k];
+              w[4 * k] = v.x, w[4 * k + 1] = v.y, w[4 * k + 2] = v.z, w[4 * k + 3] = v.w;
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 24; k++) w[k] = (u32)(k / 3) < cnt ? sp[k] : 0u;
+          }
+          __syncwarp();
+          if (todo) {
+            const int nx = __ffs((int)todo) - 1;
+            prefetch(__shfl_sync(0xffffffffu, h_base, nx), (u32)__shfl_sync(0xffffffffu, h_n, nx));
+          }
+        } else if (cnt == 8) {
           const uint4* p = reinterpret_cast<const uint4*>(rec + i0);
 #pragma unroll
           for (int k = 0; k < 6; k++) {
@@ -188,7 +237,7 @@ __global__ void __launch_bounds__(SS_WARPS * 32, SS_MINB)
         mine.min_depth = mn;
       }
     }
-    if (my_o < A.n_objs) info[my_o] = mine;
+    if (lane < gsize && my_o < A.n_objs) info[my_o] = mine;
   }
 }
 
@@ -199,10 +248,15 @@ extern "C" int upy_stackscan_batch(const upy_arena* arena, const upy_ins* ins, c
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const i64 groups = (arena->n_objs + 31) / 32;  // one warp per 32 consecutive objects
+  // one warp per group of consecutive objects: 32 objects for short ones (headers and
+  // summaries move one per lane), down to 1 for long ones (each warp gets work)
+  const double avg = (double)arena->total_code_units / (double)arena->n_objs;
+  int gshift = 5;
+  while (gshift > 0 && avg * (double)(1 << gshift) > 8192.0) gshift--;
+  const i64 groups = (arena->n_objs + (1 << gshift) - 1) >> gshift;
   i64 blocks = (groups + SS_WARPS - 1) / SS_WARPS;
   const i64 cap = (i64)sms * SS_MINB;
   if (blocks > cap) blocks = cap;
-  upy_stackscan_kernel<<<(unsigned)blocks, SS_WARPS * 32, 0, (cudaStream_t)stream>>>(*arena, ins, dec, stack, info);
+  upy_stackscan_kernel<<<(unsigned)blocks, SS_WARPS * 32, 0, (cudaStream_t)stream>>>(*arena, ins, dec, stack, info, gshift);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
