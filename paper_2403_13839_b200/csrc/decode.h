@@ -278,6 +278,11 @@ __device__ __forceinline__ int decode_chunk(const u8* __restrict__ code, u32 len
       }
     }
   } else {
+    // no EXTENDED_ARG anywhere in the chunk and none pending (the usual 3.11 case,
+    // where only the inline-cache skips keep it off the fast path): no run scan
+    const bool noext = __ballot_sync(0xffffffffu, ext_mask != 0) == 0 && st.carry.len == 0;
+    ExtRun excl = {0, 0, 0};
+    if (!noext) {
     // lane summary of its 8 units
     ExtRun mine;
     {
@@ -305,9 +310,12 @@ __device__ __forceinline__ int decode_chunk(const u8* __restrict__ code, u32 len
       ExtRun o = shfl_up_run(inc, d);
       if (lane >= d) inc = ext_combine(o, inc);
     }
-    ExtRun excl = shfl_up_run(inc, 1);
+    excl = shfl_up_run(inc, 1);
     if (lane == 0) excl = ExtRun{1, 0, 0};
     excl = ext_combine(st.carry, excl);
+    } else {
+      inc = ExtRun{0, 0, 0};
+    }
     // instruction slots: non-EXT units before this lane
     u32 my_ins = (u32)__popc((~(ext_mask | skip)) & (nu >= 8 ? 0xFF : ((1u << nu) - 1)));
     u32 pre = my_ins;

@@ -181,15 +181,17 @@ HD inline u32 stack_desc_make(int base, int term, int mul, bool unknown, bool en
   return (u32)(base & 0xFF) | ((u32)term << 8) | ((u32)(mul & 0xF) << 11) | (unknown ? 1u << 15 : 0u) |
          (ender ? 1u << 16 : 0u);
 }
-HD inline int stack_desc_term(u32 d, u32 arg) {
-  switch ((d >> 8) & 7) {
-    case SD_N: return (int)(arg > 0x7FFF ? 0x7FFF : arg);
-    case SD_POP4: return __builtin_popcount(arg & 0xF);
-    case SD_BIT0: return (int)(arg & 1);
-    case SD_BIT2: return (arg & 4) ? 1 : 0;
-    case SD_UNPACK_EX: return (int)(arg & 0xFF) + (int)((arg >> 8) & 0xFFFF);
-    default: return 0;
-  }
+HD inline int stack_desc_term(u32 d, u32 arg) {  // branch-free selection of the arg term
+  const u32 k = (d >> 8) & 7;
+  const int n = (int)(arg > 0x7FFF ? 0x7FFF : arg);
+  const int pop = __builtin_popcount(arg & 0xF);
+  const int ux = (int)(arg & 0xFF) + (int)((arg >> 8) & 0xFFFF);
+  int t = k == SD_N ? n : 0;
+  t = k == SD_POP4 ? pop : t;
+  t = k == SD_BIT0 ? (int)(arg & 1) : t;
+  t = k == SD_BIT2 ? (int)((arg >> 2) & 1) : t;
+  t = k == SD_UNPACK_EX ? ux : t;
+  return t;
 }
 HD inline int stack_desc_effect(u32 d, u32 arg) {
   const int base = (int)(int8_t)(d & 0xFF);

@@ -162,25 +162,21 @@ __global__ void __launch_bounds__(SS_WARPS * 32, SS_MINB)
           sums[q] = run;
           unk_inc |= ru << q;
         }
-        // warp segmented scan of the lane aggregates (segment seen, unknown, sum)
-        int a_seg = segm != 0, a_unk = (int)((unk_inc >> 7) & 1u), a_sum = sums[7];
+        // warp segmented scan of the lane aggregates, packed in one word per lane:
+        // bit31 segment seen, bit30 unknown, bits 0-29 the sum (30-bit two's
+        // complement; a step's sums stay far inside that range)
+        u32 agg = (segm ? 0x80000000u : 0u) | (((unk_inc >> 7) & 1u) << 30) | ((u32)sums[7] & 0x3FFFFFFFu);
 #pragma unroll
         for (int dd = 1; dd < 32; dd <<= 1) {
-          const int s2 = __shfl_up_sync(0xffffffffu, a_seg, dd);
-          const int u2 = __shfl_up_sync(0xffffffffu, a_unk, dd);
-          const int v2 = __shfl_up_sync(0xffffffffu, a_sum, dd);
-          if (lane >= dd && !a_seg) {
-            a_sum += v2;
-            a_unk |= u2;
-            a_seg = s2;
-          }
+          const u32 o = __shfl_up_sync(0xffffffffu, agg, dd);
+          if (lane >= dd && !(agg >> 31))
+            agg = (o & 0x80000000u) | ((o | agg) & 0x40000000u) | ((o + agg) & 0x3FFFFFFFu);
         }
         // this lane's incoming prefix (exclusive), seeded with the carry
-        int e_seg = __shfl_up_sync(0xffffffffu, a_seg, 1);
-        int e_unk = __shfl_up_sync(0xffffffffu, a_unk, 1);
-        int e_sum = __shfl_up_sync(0xffffffffu, a_sum, 1);
-        if (lane == 0) e_seg = 0, e_unk = 0, e_sum = 0;
-        if (!e_seg) e_sum += c_sum, e_unk |= c_unk;
+        u32 ex = __shfl_up_sync(0xffffffffu, agg, 1);
+        if (lane == 0) ex = 0;
+        int e_sum = (int)(ex << 2) >> 2, e_unk = (int)((ex >> 30) & 1u);
+        if (!(ex >> 31)) e_sum += c_sum, e_unk |= c_unk;
         // positions before the lane's first segment start continue the incoming prefix
         const u32 first_seg = segm ? (u32)(__ffs((int)segm) - 1) : 8u;
         u32 words[8];
@@ -219,16 +215,11 @@ __global__ void __launch_bounds__(SS_WARPS * 32, SS_MINB)
           c_end = __shfl_sync(0xffffffffu, (int)((endm >> 7) & 1u), 31);
         }
       }
-#pragma unroll
-      for (int dd = 16; dd; dd >>= 1) {
-        segs += __shfl_xor_sync(0xffffffffu, segs, dd);
-        unks += __shfl_xor_sync(0xffffffffu, unks, dd);
-        pushes += __shfl_xor_sync(0xffffffffu, pushes, dd);
-        const int a = __shfl_xor_sync(0xffffffffu, mx, dd);
-        const int b = __shfl_xor_sync(0xffffffffu, mn, dd);
-        mx = a > mx ? a : mx;
-        mn = b < mn ? b : mn;
-      }
+      segs = (int)__reduce_add_sync(0xffffffffu, (u32)segs);
+      unks = (int)__reduce_add_sync(0xffffffffu, (u32)unks);
+      pushes = (int)__reduce_add_sync(0xffffffffu, (u32)pushes);
+      mx = __reduce_max_sync(0xffffffffu, mx);
+      mn = __reduce_min_sync(0xffffffffu, mn);
       if (lane == j) {
         mine.n_segments = segs;
         mine.n_unknown = unks;
