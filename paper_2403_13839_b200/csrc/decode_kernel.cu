@@ -82,6 +82,12 @@ __device__ __noinline__ void decode311_body(u32 len, upy_ins* __restrict__ rec, 
   int ok = 1;
   int cmax = -1;          // max span end of earlier chunks
   u32 prev_ext = 0;       // last unit of the previous chunk is an uncovered EXTENDED_ARG
+  // Lean path: while no chunk so far has an EXTENDED_ARG or a jump, every uncovered
+  // unit is one instruction with a 1-byte arg, so the records are written right here
+  // (slots by a warp scan of per-lane counts, staged in S.out[1], copied out as
+  // coalesced words) and pass 2 is skipped.  Code up to 3 KB sits in S.out[0].
+  bool lean = len <= 3072u;
+  u32 n_lean = 0;
   for (u32 base = 0; base < units; base += 256) {
     const u32 u0 = base + 8 * lane;
     u32 nu = 0;
@@ -142,8 +148,52 @@ __device__ __noinline__ void decode311_body(u32 len, upy_ins* __restrict__ rec, 
       ok = 0;
       break;
     }
+    if (lean) {
+      const u32 inst = ~cov_bits & (nu >= 8 ? 0xFFu : ((1u << nu) - 1));
+      u32 jmp = 0;
+#pragma unroll
+      for (int q = 0; q < 8; q++) jmp |= ((inst >> q) & (ent[q] >> ENT_JUMP_BIT) & 1u) << q;
+      if (__ballot_sync(0xffffffffu, ext_bits | jmp) != 0) {
+        lean = false;  // pass 2 redoes the object from its first record
+      } else {
+        const u32 cnt = (u32)__popc(inst);
+        u32 incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const u32 o = __shfl_up_sync(0xffffffffu, incl, d);
+          if (lane >= d) incl += o;
+        }
+        const u32 total = __shfl_sync(0xffffffffu, incl, 31);
+        u32* sw = reinterpret_cast<u32*>(&S.out[1][0]) + 3 * (incl - cnt);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          if (!((inst >> q) & 1u)) continue;
+          const u32 unit = (words[q >> 1] >> (16 * (q & 1))) & 0xFFFFu;
+          const u32 has_arg = UPY_ENT_HASARG(ent[q]);
+          sw[0] = 2 * (u0 + q);
+          sw[1] = has_arg ? (unit >> 8) : 0u;
+          sw[2] = (unit & 0xFFu) | (UPY_ENT_CACHE(ent[q]) << 16) | (has_arg << 24);
+          sw += 3;
+        }
+        __syncwarp();
+        const u32* src = reinterpret_cast<const u32*>(&S.out[1][0]);
+        u32* dst = reinterpret_cast<u32*>(rec + n_lean);
+        for (u32 k = lane; k < 3 * total; k += 32) dst[k] = src[k];
+        __syncwarp();
+        n_lean += total;
+      }
+    }
     cmax = __shfl_sync(0xffffffffu, inc, 31);
     prev_ext = __shfl_sync(0xffffffffu, (ext_bits >> 7) & 1u, 31);
+  }
+  if (ok && lean) {  // no EXTENDED_ARG, so no run can reach the end; no jumps to mark
+    if (lane == 0) {
+      res->status = UPY_ST_OK;
+      res->n_instrs = (i32)n_lean;
+      res->aux0 = res->aux1 = 0;
+    }
+    __syncwarp();
+    return;
   }
   // an EXTENDED_ARG run reaching the end of the code: the scalar decoder's error
   __syncwarp();
