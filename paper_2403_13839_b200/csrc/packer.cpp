@@ -6,7 +6,7 @@
 // It restates arena.py's `_Packer` + `pack` exactly (same object / const / ref /
 // string order, the same 16-B code alignment and 256-B sections, the same int
 // clamping), so its output is byte-identical to the Python packer
-// (tests/test_packer.py) -- at ~1M objects/s instead of ~25K/s, which is what
+// (tests/test_packer.py) -- at ~0.3M C3 objects/s instead of ~24K/s, which is what
 // keeps `decompile_many(codes)` from being host-bound (the
 // flattening of nested code trees into the arena happens here, in one pass).
 //
@@ -87,11 +87,44 @@ struct Packer {
   std::vector<std::string> strs;
   std::vector<uint32_t> refs;
   std::vector<uint32_t> limbs;
-  std::vector<std::string> codes, excs, lnts;
+  // code / exception / line tables: a pointer into the caller's bytes object (kept
+  // alive by a reference) or, for other buffer types, an owned copy
+  struct Bytes {
+    PyObject* ref;
+    const char* p;
+    size_t n;
+    std::string own;
+    size_t size() const { return n; }
+    const char* data() const { return p; }
+  };
+  std::vector<Bytes> codes, excs, lnts;
   std::string payload;
   bool err = false;
 
-  ~Packer() { Py_XDECREF(str_index); }
+  ~Packer() {
+    Py_XDECREF(str_index);
+    for (auto* v : {&codes, &excs, &lnts})
+      for (auto& b : *v) Py_XDECREF(b.ref);
+  }
+  static bool take_bytes(PyObject* v, std::vector<Bytes>* out) {  // bytes(v or b"")
+    out->emplace_back();
+    Bytes& b = out->back();
+    b.ref = nullptr;
+    b.p = "";
+    b.n = 0;
+    if (v == Py_None) return true;
+    if (PyBytes_CheckExact(v)) {
+      Py_INCREF(v);
+      b.ref = v;
+      b.p = PyBytes_AS_STRING(v);
+      b.n = (size_t)PyBytes_GET_SIZE(v);
+      return true;
+    }
+    if (!as_bytes(v, &b.own)) return false;
+    b.p = b.own.data();
+    b.n = b.own.size();
+    return true;
+  }
 
   static bool utf8(PyObject* s, std::string* out) {
     Ref b(PyUnicode_AsEncodedString(s, "utf-8", "surrogatepass"));
@@ -154,6 +187,16 @@ struct Packer {
   bool flags_attr(PyObject* co, int64_t* out) {
     Ref v(PyObject_GetAttr(co, N.flags));
     if (!v) return false;
+    if (PyLong_Check(v)) {  // fits int64: two's complement & equals Python's & here
+      int ovf = 0;
+      const long long x = PyLong_AsLongLongAndOverflow(v, &ovf);
+      if (!ovf && !(x == -1 && PyErr_Occurred())) {
+        const long long lo = x & (kLim - 1);
+        *out = x < 0 ? lo - kLim : lo;
+        return true;
+      }
+      PyErr_Clear();
+    }
     Ref iv(PyNumber_Long(v));
     if (!iv) return false;
     Ref mask(PyLong_FromLongLong(kLim - 1));
@@ -199,6 +242,33 @@ struct Packer {
     return -1;
   }
 
+  // int(v) of any size: sign and 32-bit limbs of the magnitude (arena.py _Packer.const)
+  bool int_slow(PyObject* v, ConstRow* row) {
+    Ref iv(PyNumber_Long(v));
+    if (!iv) return false;
+    row->ival = _PyLong_Sign(iv.p);
+    Ref mag(PyNumber_Absolute(iv));
+    if (!mag) return false;
+    int64_t bits = (int64_t)_PyLong_NumBits(mag.p);
+    if (bits < 0) return false;
+    uint32_t nb = bits ? (uint32_t)((bits + 31) / 32) : 1u;
+    std::vector<uint8_t> buf((size_t)nb * 4);
+    if (_PyLong_AsByteArray((PyLongObject*)mag.p, buf.data(), buf.size(), 1, 0) < 0) return false;
+    row->n = nb;
+    row->off = limbs.size();
+    for (uint32_t i = 0; i < nb; i++) {
+      uint32_t w;
+      memcpy(&w, buf.data() + 4 * i, 4);
+      limbs.push_back(w);
+    }
+    return true;
+  }
+  int64_t push_row(const ConstRow& row, uint8_t is_payload) {
+    consts.push_back(row);
+    payload_of.push_back(is_payload);
+    return (int64_t)consts.size() - 1;
+  }
+
   int64_t cnst(PyObject* c) {  // _Packer.const
     Ref kobj(PyObject_GetAttr(c, N.kind));
     if (!kobj) return -1;
@@ -214,25 +284,19 @@ struct Packer {
       int t = PyObject_IsTrue(v);
       if (t < 0) return -1;
       row.ival = t ? 1 : 0;
-    } else if (k == K_INT) {
-      Ref iv(PyNumber_Long(v));
-      if (!iv) return -1;
-      int sign = _PyLong_Sign(iv.p);
-      row.ival = sign;
-      Ref mag(PyNumber_Absolute(iv));
-      if (!mag) return -1;
-      int64_t bits = (int64_t)_PyLong_NumBits(mag.p);
-      if (bits < 0) return -1;
-      uint32_t nb = bits ? (uint32_t)((bits + 31) / 32) : 1u;
-      std::vector<uint8_t> buf((size_t)nb * 4);
-      if (_PyLong_AsByteArray((PyLongObject*)mag.p, buf.data(), buf.size(), 1, 0) < 0) return -1;
-      row.n = nb;
+    } else if (k == K_INT && PyLong_Check(v) && !PyBool_Check(v)) {
+      int ovf = 0;
+      const long long x = PyLong_AsLongLongAndOverflow(v, &ovf);
+      if (x == -1 && PyErr_Occurred()) return -1;
+      if (ovf) return int_slow(v, &row) ? push_row(row, 0) : -1;
+      row.ival = (x > 0) - (x < 0);
+      const unsigned long long mag = x < 0 ? 0ull - (unsigned long long)x : (unsigned long long)x;
+      row.n = (mag >> 32) ? 2u : 1u;
       row.off = limbs.size();
-      for (uint32_t i = 0; i < nb; i++) {
-        uint32_t w;
-        memcpy(&w, buf.data() + 4 * i, 4);
-        limbs.push_back(w);
-      }
+      limbs.push_back((uint32_t)mag);
+      if (row.n == 2) limbs.push_back((uint32_t)(mag >> 32));
+    } else if (k == K_INT) {
+      if (!int_slow(v, &row)) return -1;
     } else if (k == K_FLOAT) {
       row.re = PyFloat_AsDouble(v);
       if (row.re == -1.0 && PyErr_Occurred()) return -1;
@@ -287,21 +351,17 @@ struct Packer {
     obj_index.emplace(co, idx);
     objs.emplace_back();
     memset(&objs.back(), 0, sizeof(Obj));
-    std::string b;
     {
       Ref v(PyObject_GetAttr(co, N.code));
-      if (!v || !as_bytes(v, &b)) return -1;
-      codes.push_back(b);
+      if (!v || !take_bytes(v, &codes)) return -1;
     }
     {
       Ref v(PyObject_GetAttr(co, N.exceptiontable));
-      if (!v || !as_bytes(v, &b)) return -1;
-      excs.push_back(b);
+      if (!v || !take_bytes(v, &excs)) return -1;
     }
     {
       Ref v(PyObject_GetAttr(co, N.linetable));
-      if (!v || !as_bytes(v, &b)) return -1;
-      lnts.push_back(b);
+      if (!v || !take_bytes(v, &lnts)) return -1;
     }
     Obj o;
     memset(&o, 0, sizeof o);
