@@ -1,4 +1,4 @@
-# Round-2 check: smoke, GPU tests, the new default bench line (distinct C3 corpus
+# Evidence run: smoke, GPU tests, the new default bench line (distinct C3 corpus
 # + extras), the reference arm, an ncu DRAM-traffic launch list and a full-set
 # capture of the decompile kernel.  Outputs in gpurun_out/.
 mkdir -p gpurun_out /tmp/ncu

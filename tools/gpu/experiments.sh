@@ -1,0 +1,50 @@
+# Round-2 GPU experiments, one function each (outputs in gpurun_out/):
+#   bash tools/gpu/experiments.sh <name> [...]
+# c4_slots   C4 throughput vs concurrent arena slots (profiles/r02/bench_c4_slots_*.json)
+# stages     thread-cycles per pipeline stage (needs tools/build_variant.sh prof -DUPY_PHASE_PROF)
+# noemit     decompile kernel without the emit stage vs full, + icache metrics (variant noemit -DUPY_SKIP_EMIT)
+# variant    same-session A/B of a variant library: VARIANT=<name> (built by tools/build_variant.sh)
+# stackscan  stack-scan kernel: timing on C3 / C4 and a full ncu capture
+# decode311  3.11 decode timing and a full ncu capture on C3-3.11
+set -u
+mkdir -p gpurun_out /tmp/ncu
+python -m paper_2403_13839_b200.build > gpurun_out/build.log 2>&1 || { tail -20 gpurun_out/build.log; exit 1; }
+V=paper_2403_13839_b200/_variants
+c4_slots() {
+  for s in 12288 24576 49152; do
+    timeout 600 python bench.py --workload c4 --steps 1 --warmup 1 --no-cpu --pyc 0 --slots $s --arena-bytes 2621440 \
+      2>&1 | tail -1 > gpurun_out/c4_slots_$s.json
+  done
+}
+stages() {
+  UPY_LIB=$V/prof.so timeout 600 python tools/stage_prof.py c3_310 c3_311 | tee gpurun_out/stage_prof_c3.txt
+  UPY_LIB=$V/prof.so timeout 900 python tools/stage_prof.py c4_310 c4_311 --objects 16384 | tee gpurun_out/stage_prof_c4.txt
+}
+ab() {  # ab <variant> : base / variant / base / variant, kernel times
+  for v in base $1 base $1; do
+    if [ $v = base ]; then L=; else L=$V/$v.so; fi
+    UPY_LIB=$L timeout 900 python bench.py --no-cpu --pyc 0 --no-extra --steps 3 2>&1 | tail -1 > gpurun_out/ab_$v.json
+    python -c "import json; d=json.load(open('gpurun_out/ab_$v.json')); print('$v', d['kernel_ms'], d['parity'])" \
+      | tee -a gpurun_out/ab_$1.txt
+  done
+}
+icc() {  # icc <lib or empty> <tag>
+  M=sm__icc_request_hit_rate.pct,gcc__cache_requests_type_instruction.sum,gcc__cache_requests_type_instruction.sum.pct_of_peak_sustained_elapsed,smsp__average_warp_latency_per_inst_issued.ratio,gpu__time_duration.sum
+  UPY_LIB=$1 ncu --metrics $M -k regex:upy_decompile -s 1 -c 1 --csv \
+    python bench.py --no-cpu --pyc 0 --no-extra --steps 1 --warmup 1 --objects 262144 > gpurun_out/icc_$2.csv 2>&1
+}
+noemit() { ab noemit; icc "" base; icc $V/noemit.so noemit; }
+variant() { ab "$VARIANT"; }
+stackscan() {
+  timeout 900 python bench.py --no-cpu --pyc 0 --no-extra 2>&1 | tail -1 > gpurun_out/bench_stackscan_c3.json
+  timeout 900 python bench.py --workload c4 --no-cpu --pyc 0 --steps 1 --warmup 1 2>&1 | tail -1 > gpurun_out/bench_stackscan_c4.json
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:upy_stackscan -s 1 -c 1 -o /tmp/ncu/stackscan -f \
+    python bench.py --no-cpu --pyc 0 --no-extra --steps 1 --warmup 1 > gpurun_out/ncu_stackscan.log 2>&1
+  ncu -i /tmp/ncu/stackscan.ncu-rep --page raw --csv > gpurun_out/ncu_stackscan_raw.csv 2>&1
+}
+decode311() {
+  timeout 900 python bench.py --workload c3_311 --no-cpu --pyc 0 --no-extra --steps 3 2>&1 | tail -1 > gpurun_out/bench_decode311.json
+  timeout 600 ncu --set full --clock-control none -k regex:upy_decode -s 3 -c 1 --csv --page raw \
+    python bench.py --workload c3_311 --no-cpu --pyc 0 --no-extra --steps 1 --warmup 2 > gpurun_out/ncu_decode311_raw.csv 2>&1
+}
+for f in "$@"; do $f; done
