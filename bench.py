@@ -369,6 +369,7 @@ def time_e2e(da, arena, args, local, barrier):
     need = da.ws_bytes + da.text.numel() + da.dev.numel() + da.meta.numel()
     if free > 1.2 * need:
         das = [da, DeviceArena(arena, device=f"cuda:{local}", slots=da.opts.slots, arena_bytes=args.arena_bytes,
+                               schedule=args.schedule,
                                threads_per_block=args.tpb, pinned=da.host)]
     else:
         das = [da, da]
@@ -423,8 +424,12 @@ def run_workload(wl, args, rank, world, local, barrier, steps, warmup, e2e=True)
     t_gen = time.time()
     arena, verifier, info = build_corpus(wl, rank, world, args.objects if wl == args.workload else 0)
     t_gen = time.time() - t_gen
+    schedule = args.schedule
+    if schedule == "auto":
+        schedule = "cost" if WORKLOADS[wl]["kind"] == "c3" else "input"
+    info["schedule"] = schedule
     da = DeviceArena(arena, device=f"cuda:{local}", slots=args.slots, arena_bytes=args.arena_bytes,
-                     threads_per_block=args.tpb)
+                     threads_per_block=args.tpb, schedule=schedule)
     da.upload()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
@@ -434,7 +439,7 @@ def run_workload(wl, args, rank, world, local, barrier, steps, warmup, e2e=True)
     e2e_ms = used = None
     double = False
     if e2e:
-        a2 = argparse.Namespace(**{**vars(args), "steps": steps})
+        a2 = argparse.Namespace(**{**vars(args), "steps": steps, "schedule": schedule})
         res, e2e_ms, used, double = time_e2e(da, arena, a2, local, barrier)
     else:
         res = da.fetch()
@@ -460,7 +465,8 @@ def extra_line(wl, args, local, barrier):
             "kernel_ms": {"decode": r["dec_sum"] / 2, "decompile": r["st_sum"] / 2, "stackscan": r["stackscan_ms"]},
             "instructions": r["n_instr"], "code_bytes": r["arena"].code_bytes,
             "decode_gbs_alg": None, "parity": {"checked": r["checked"], "mismatches": r["bad"]},
-            "slots": r["slots"], "corpus": r["info"]["corpus"], "clocks": r["clocks"]}
+            "slots": r["slots"], "corpus": r["info"]["corpus"], "schedule": r["info"]["schedule"],
+            "clocks": r["clocks"]}
 
 
 def api_e2e(wl, n_sample, local):
@@ -503,6 +509,10 @@ def main():
     ap.add_argument("--tpb", type=int, default=0)
     ap.add_argument("--pyc", type=int, default=1, help="also time the .pyc-bytes end-to-end path (0: skip)")
     ap.add_argument("--api-sample", type=int, default=16384)
+    ap.add_argument("--schedule", default="auto", choices=["auto", "input", "cost"],
+                    help="root order of the decompile kernel: cost = largest tree first (the API default); "
+                         "auto = cost on distinct corpora, input on tiled pools (a size order would put a "
+                         "pool object's copies side by side and the warps would run them in lockstep)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -587,7 +597,7 @@ def main():
         "config": {"workload": spec["desc"], "objects_per_gpu": r["n_roots"], "objects_total": objs_total,
                    "code_objects_per_gpu": int(arena.n_objs), "corpus": r["info"]["corpus"],
                    "python": spec.get("minor", 10), "code_bytes_per_gpu": code_bytes,
-                   "instructions_per_gpu": r["n_instr"], "slots": r["slots"],
+                   "instructions_per_gpu": r["n_instr"], "slots": r["slots"], "schedule": r["info"]["schedule"],
                    "l2": f"inputs larger than L2 ({h2d / 1e9:.2f} GB arena + {12 * r['n_instr'] / 1e9:.2f} GB "
                          "records per step)",
                    "parallelism": f"objects sharded x{world}", "gen_seconds": round(r["t_gen"], 1)},

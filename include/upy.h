@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define UPY_ABI_VERSION 3
+#define UPY_ABI_VERSION 4
 
 /* Const kinds (code_model.py:56-59). */
 enum {
@@ -96,6 +96,11 @@ typedef struct {
   int32_t output;            /* 0: source text (above); 1: the CFG export of `unpyre disasm --cfg --dot`
                                 (cli.py:103-105): to_dot(analyze(root)[2]) (cfg.py:331-344,
                                 pipeline.py:17-54) per root, no validation */
+  int32_t pad0;
+  const int32_t* order;      /* device pointer or NULL: the order in which root positions are taken (a
+                                permutation of [0, n_roots)); results stay indexed by root position.
+                                The host layer passes largest-tree-first (paper_2403_13839_b200
+                                .api schedule "cost"), so big objects do not form the batch's tail */
 } upy_options;
 
 /* Per-root results (device pointers, caller-allocated). */

@@ -35,6 +35,8 @@ class UpyOptions(C.Structure):
         ("max_depth", C.c_int32),
         ("function_tree", C.c_int32),
         ("output", C.c_int32),
+        ("pad0", C.c_int32),
+        ("order", C.c_void_p),
     ]
 
 

@@ -73,7 +73,7 @@ class DeviceArena:
     `run()` on HBM-resident inputs and `upload()+run()+fetch()` end to end)."""
 
     def __init__(self, arena: Arena, style=None, device=None, text_cap=None, arena_bytes=0, slots=0,
-                 threads_per_block=0, pinned=None, function_tree=False, output=0):
+                 threads_per_block=0, pinned=None, function_tree=False, output=0, schedule="input"):
         torch = _torch()
         self.torch = torch
         self.lib = _lib.load()
@@ -86,6 +86,17 @@ class DeviceArena:
         self.host = pinned if pinned is not None else torch.from_numpy(arena.blob).pin_memory()
         self.dev = torch.empty(self.host.numel(), dtype=torch.uint8, device=self.device)
         self.A = _abi.arena_struct(arena, self.dev.data_ptr())
+        # schedule="cost": roots are taken largest code-object tree first (longest-
+        # processing-time order: big objects do not start last and form the batch's
+        # tail, and lanes of a warp get objects of similar size).  The order is
+        # computed on the device from the uploaded arena at every run (cost_order)
+        # and handed to the kernel as upy_options.order; results stay in input order.
+        if schedule not in ("input", "cost"):
+            raise ValueError(f"schedule must be 'input' or 'cost', not {schedule!r}")
+        self.schedule = schedule if arena.n_roots > 1 else "input"
+        roots = arena.section("roots")
+        self._trees_contiguous = bool(len(roots) < 2 or np.all(np.diff(roots.astype(np.int64)) > 0))
+        self._order = None
         if not slots and not arena_bytes:
             slots = self._memory_slots(arena)
         self.opts = _abi.options(style, arena_bytes=arena_bytes, slots=slots,
@@ -146,6 +157,13 @@ class DeviceArena:
         with torch.cuda.device(self.device):  # the C ABI launches on the current device
             if mode != "decode":
                 self.meta[:8].zero_()
+                if self.schedule == "cost":
+                    with torch.cuda.stream(s):
+                        self._order = cost_order(self.dev, self.arena.offsets, self.arena.counts,
+                                                 self._trees_contiguous)
+                    self.opts.order = self._order.data_ptr()
+                else:
+                    self.opts.order = None
             rc = self.lib.upy_decompile_batch(C.byref(self.A), C.byref(self.opts), C.byref(self.out),
                                               C.c_void_p(self.ws.data_ptr()), C.c_size_t(self.ws_bytes),
                                               C.c_void_p(s.cuda_stream))
@@ -204,6 +222,47 @@ class DeviceArena:
         return BatchResult(st, off, ln, aux, text)
 
 
+def cost_order(blob, offsets, counts, trees_contiguous):
+    """Largest-tree-first order of the root positions (int32 tensor on blob's
+    device), from the arena image itself: a root's cost is the code bytes of its
+    tree -- the run of objects from the root to the next root when the roots are
+    in packing order (pack / tile lay each tree out contiguously), else the root's
+    own code length.  Stable, so equal costs keep input order."""
+    import torch
+
+    from .arena import OBJ_DTYPE
+
+    n_objs, n_roots = int(counts["objs"]), int(counts["roots"])
+    o0, r0 = int(offsets["objs"]), int(offsets["roots"])
+    rec = OBJ_DTYPE.itemsize
+    cl_at = OBJ_DTYPE.fields["code_len"][1]
+    objs = blob[o0:o0 + n_objs * rec].view(n_objs, rec)
+    lens = objs[:, cl_at:cl_at + 4].contiguous().view(torch.int32).view(-1).to(torch.int64)
+    roots = blob[r0:r0 + 4 * n_roots].view(torch.int32).to(torch.int64)
+    if trees_contiguous:
+        csum = torch.zeros(n_objs + 1, dtype=torch.int64, device=blob.device)
+        csum[1:] = torch.cumsum(lens, 0)
+        ends = torch.cat([roots[1:], torch.full((1,), n_objs, dtype=torch.int64, device=blob.device)])
+        cost = csum[ends] - csum[roots]
+    else:
+        cost = lens[roots]
+    return torch.sort(cost, descending=True, stable=True).indices.to(torch.int32)
+
+
+def root_cost_order(arena: Arena):
+    """Host (numpy) restatement of cost_order, for tests."""
+    objs = arena.section("objs")
+    roots = arena.section("roots").astype(np.int64)
+    lens = objs["code_len"].astype(np.int64)
+    if len(roots) < 2 or np.all(np.diff(roots) > 0):
+        csum = np.concatenate([[0], np.cumsum(lens)])
+        ends = np.concatenate([roots[1:], [len(lens)]])
+        cost = csum[ends] - csum[roots]
+    else:
+        cost = lens[roots]
+    return np.argsort(-cost, kind="stable")
+
+
 def default_slot_bytes(arena: Arena) -> int:
     """The per-thread arena size upy_query_workspace picks (upy.cu layout())."""
     return (64 << 10) + 160 * arena.max_code_len
@@ -241,7 +300,8 @@ def tree_sizes(arena: Arena, roots) -> tuple:
     return code, payload
 
 
-def run_arena(arena: Arena, style=None, device=None, retries=3, function_tree=False, output=0) -> BatchResult:
+def run_arena(arena: Arena, style=None, device=None, retries=3, function_tree=False, output=0,
+              schedule="cost") -> BatchResult:
     """Decompile every root of a packed arena on the GPU.
 
     Roots that hit a device capacity limit (per-thread arena, output buffer) are
@@ -251,7 +311,7 @@ def run_arena(arena: Arena, style=None, device=None, retries=3, function_tree=Fa
     torch = _torch()
     dev = torch.device(device or "cuda")
     with torch.cuda.device(dev):
-        da = DeviceArena(arena, style, dev, function_tree=function_tree, output=output)
+        da = DeviceArena(arena, style, dev, function_tree=function_tree, output=output, schedule=schedule)
         da.upload()
         da.run()
         res = da.fetch()

@@ -45,6 +45,7 @@ struct KParams {
   int lane_stride;  // 1: every thread takes roots; 32: one root-taking thread per warp
   int function_tree;
   int output;       // upy_options.output: 0 source text, 1 CFG dot export
+  const int32_t* order;  // upy_options.order: processing order of root positions (or null)
 };
 
 #ifndef UPY_MINB
@@ -133,6 +134,7 @@ __global__ void __launch_bounds__(128, UPY_MINB) upy_decompile_kernel(KParams P)
   while (true) {
     u32 r = atomicAdd(P.next_root, 1u);
     if (r >= n_roots) break;
+    if (P.order) r = (u32)P.order[r];
     dc_reset(C, P, base);
     Text out = {nullptr, 0, 0};
     decompile_source(&C, (u32)P.A.roots[r], &opt, &out);
@@ -151,6 +153,7 @@ __global__ void __launch_bounds__(128, UPY_MINB) upy_cfgdot_kernel(KParams P) {
   while (true) {
     u32 r = atomicAdd(P.next_root, 1u);
     if (r >= n_roots) break;
+    if (P.order) r = (u32)P.order[r];
     dc_reset(C, P, base);
     Text out = {nullptr, 0, 0};
     cfg_dot(&C, (u32)P.A.roots[r], &out);
@@ -337,6 +340,7 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
   P.header = opt ? opt->header : 0;
   P.function_tree = opt ? opt->function_tree : 0;
   P.output = opt ? opt->output : 0;
+  P.order = opt ? opt->order : nullptr;
   u8* style_ws = ws + L.style_off;
   if (P.indent_len <= 64) {
     memcpy(P.indent, ind, P.indent_len);

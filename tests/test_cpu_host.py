@@ -74,7 +74,7 @@ def test_cuda_library_exports_every_declared_symbol():
         assert hasattr(lib, sym), sym
     _abi.check_layout(lib)
     lib.upy_abi_version.restype = ctypes.c_int
-    assert lib.upy_abi_version() == 3
+    assert lib.upy_abi_version() == 4
 
 
 def test_shard_bounds_partition_and_balance():
@@ -165,3 +165,23 @@ def test_gloo_sharded_decompile_and_gather(tmp_path):
     assert res[0]["lo"] == 0 and res[0]["hi"] == res[1]["lo"] and res[1]["hi"] == res[0]["n"]
     assert 0 < res[0]["hi"] < res[0]["n"]  # both ranks got work
     assert all(x["bad"] == 0 and x["own_bad"] == 0 for x in res), res
+
+
+def test_cost_order_matches_host_restatement():
+    """The device-side largest-tree-first order (api.cost_order, torch ops, run here
+    on a CPU tensor) equals its numpy restatement, for contiguous trees (pack /
+    tile layout) and for a roots array in arbitrary order."""
+    import numpy as np
+    import torch
+
+    from conftest import golden_cases
+    from helpers import inputs
+    from paper_2403_13839_b200 import api, arena
+
+    ar = arena.tile(arena.pack(inputs([r for r in golden_cases(["c2"]) if not r.get("style")])), 3)
+    for a in (ar, arena.with_roots(ar, ar.section("roots")[::-1].copy())):
+        roots = a.section("roots").astype(np.int64)
+        contiguous = bool(np.all(np.diff(roots) > 0))
+        got = api.cost_order(torch.from_numpy(a.blob), a.offsets, a.counts, contiguous).numpy()
+        assert np.array_equal(got, api.root_cost_order(a))
+        assert sorted(got.tolist()) == list(range(a.n_roots))

@@ -6,6 +6,7 @@
 # variant    same-session A/B of a variant library: VARIANT=<name> (built by tools/build_variant.sh)
 # stackscan  stack-scan kernel: timing on C3 / C4 and a full ncu capture
 # decode311  3.11 decode timing and a full ncu capture on C3-3.11
+# schedule   root order input vs largest-tree-first (api.root_cost_order) on C2x / C4 / C2
 set -u
 mkdir -p gpurun_out /tmp/ncu
 python -m paper_2403_13839_b200.build > gpurun_out/build.log 2>&1 || { tail -20 gpurun_out/build.log; exit 1; }
@@ -46,5 +47,15 @@ decode311() {
   timeout 900 python bench.py --workload c3_311 --no-cpu --pyc 0 --no-extra --steps 3 2>&1 | tail -1 > gpurun_out/bench_decode311.json
   timeout 600 ncu --set full --clock-control none -k regex:upy_decode -s 3 -c 1 --csv --page raw \
     python bench.py --workload c3_311 --no-cpu --pyc 0 --no-extra --steps 1 --warmup 2 > gpurun_out/ncu_decode311_raw.csv 2>&1
+}
+schedule() {  # root order: input vs largest-tree-first, on the mixed-size shapes
+  for wl in c2x c4 c2; do
+    for sc in input cost input cost; do
+      timeout 900 python bench.py --workload $wl --schedule $sc --no-cpu --pyc 0 --no-extra --steps 2 --warmup 1 \
+        2>&1 | tail -1 > gpurun_out/sched_${wl}_$sc.json
+      python -c "import json; d=json.load(open('gpurun_out/sched_${wl}_$sc.json')); print('$wl $sc', round(d['value']), d['kernel_ms'], d['parity'])" \
+        | tee -a gpurun_out/schedule.txt
+    done
+  done
 }
 for f in "$@"; do $f; done
