@@ -7,6 +7,7 @@
 # stackscan  stack-scan kernel: timing on C3 / C4 and a full ncu capture
 # decode311  3.11 decode timing and a full ncu capture on C3-3.11
 # schedule   root order input vs largest-tree-first (api.root_cost_order) on C2x / C4 / C2
+# c5         the 16M-object corpus on one GPU, and torchrun N=1 lines (ours and the reference arm)
 set -u
 mkdir -p gpurun_out /tmp/ncu
 python -m paper_2403_13839_b200.build > gpurun_out/build.log 2>&1 || { tail -20 gpurun_out/build.log; exit 1; }
@@ -57,5 +58,12 @@ schedule() {  # root order: input vs largest-tree-first, on the mixed-size shape
         | tee -a gpurun_out/schedule.txt
     done
   done
+}
+c5() {  # one 16M-object corpus on this GPU (strong-scaling shape at N=1) + torchrun N=1 lines
+  timeout 1800 python bench.py --workload c5 --no-cpu --pyc 0 --steps 3 --warmup 3 2>&1 | tail -1 > gpurun_out/bench_c5.json
+  timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29611 \
+    bench.py --gpus 1 --no-extra --no-cpu 2>&1 | tail -1 > gpurun_out/bench_torchrun1.json
+  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29612 \
+    bench.py --impl reference --gpus 1 2>&1 | tail -1 > gpurun_out/bench_ref_torchrun1.json
 }
 for f in "$@"; do $f; done
