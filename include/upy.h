@@ -88,7 +88,8 @@ typedef struct {
   int32_t decode_only;       /* 1: run only the decode kernel */
   uint64_t arena_bytes;      /* bytes per slot arena; 0 = auto from max_code_len */
   int32_t skip_decode;       /* 1: reuse the records of a previous decode_only call on the same workspace */
-  int32_t schedule;          /* reserved, must be 0 (one decompile schedule: each thread takes the next root) */
+  int32_t schedule;          /* 0: each thread takes the next root position; 1: warp-synchronous (a warp
+                                takes 32 consecutive positions of `order` and its lanes start together) */
   int32_t max_depth;         /* device recursion guard (UPY_ST_DEPTH_LIMIT); 0 = default 600 */
   int32_t function_tree;     /* 1: emit_module([function_tree(root)]) without validation -- the
                                 reference CLI's --function path (cli.py:75-78) -- instead of

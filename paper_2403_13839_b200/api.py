@@ -91,12 +91,17 @@ class DeviceArena:
         # tail, and lanes of a warp get objects of similar size).  The order is
         # computed on the device from the uploaded arena at every run (cost_order)
         # and handed to the kernel as upy_options.order; results stay in input order.
-        if schedule not in ("input", "cost"):
-            raise ValueError(f"schedule must be 'input' or 'cost', not {schedule!r}")
-        self.schedule = schedule if arena.n_roots > 1 else "input"
+        base_sched, _, sync = schedule.partition("+")
+        if base_sched not in ("input", "cost", "similar") or sync not in ("", "sync"):
+            raise ValueError(f"schedule must be input|cost|similar[+sync], not {schedule!r}")
+        self.schedule = base_sched if arena.n_roots > 1 else "input"
+        self.warp_sync = 1 if sync else 0
+        if self.schedule == "similar":  # experiment: host-computed prefix-similarity order
+            self._order = torch.from_numpy(root_similarity_order(arena).astype(np.int32)).to(self.device)
         roots = arena.section("roots")
         self._trees_contiguous = bool(len(roots) < 2 or np.all(np.diff(roots.astype(np.int64)) > 0))
-        self._order = None
+        if self.schedule != "similar":
+            self._order = None
         if not slots and not arena_bytes:
             slots = self._memory_slots(arena)
         self.opts = _abi.options(style, arena_bytes=arena_bytes, slots=slots,
@@ -161,9 +166,8 @@ class DeviceArena:
                     with torch.cuda.stream(s):
                         self._order = cost_order(self.dev, self.arena.offsets, self.arena.counts,
                                                  self._trees_contiguous)
-                    self.opts.order = self._order.data_ptr()
-                else:
-                    self.opts.order = None
+                self.opts.order = self._order.data_ptr() if self._order is not None else None
+                self.opts.schedule = self.warp_sync
             rc = self.lib.upy_decompile_batch(C.byref(self.A), C.byref(self.opts), C.byref(self.out),
                                               C.c_void_p(self.ws.data_ptr()), C.c_size_t(self.ws_bytes),
                                               C.c_void_p(s.cuda_stream))
@@ -247,6 +251,25 @@ def cost_order(blob, offsets, counts, trees_contiguous):
     else:
         cost = lens[roots]
     return torch.sort(cost, descending=True, stable=True).indices.to(torch.int32)
+
+
+def root_similarity_order(arena: Arena, prefix=32):
+    """Experiment: root positions sorted by the first `prefix` bytes of their
+    co_code (then by length), so neighbouring roots start with the same
+    instructions (profiles/r02/schedule/)."""
+    objs = arena.section("objs")
+    roots = arena.section("roots").astype(np.int64)
+    offs = objs["code_off"].astype(np.int64)[roots]
+    lens = objs["code_len"].astype(np.int64)[roots]
+    by = arena.section("bytes")
+    j = np.arange(prefix, dtype=np.int64)
+    idx = np.minimum(offs[:, None] + j[None, :], len(by) - 1)
+    pre = np.where(j[None, :] < lens[:, None], by[idx], 0).astype(np.uint8)
+    words = pre.reshape(len(roots), prefix // 8, 8)
+    keys = [lens]
+    for w in range(prefix // 8 - 1, -1, -1):  # lexsort: last key is primary
+        keys.append(words[:, w, :].copy().view(">u8").ravel())
+    return np.lexsort(keys)
 
 
 def root_cost_order(arena: Arena):

@@ -43,6 +43,7 @@ struct KParams {
   char indent[64];
   char tool[64];
   int lane_stride;  // 1: every thread takes roots; 32: one root-taking thread per warp
+  int schedule;     // upy_options.schedule: 0 each thread takes the next root, 1 warp-synchronous
   int function_tree;
   int output;       // upy_options.output: 0 source text, 1 CFG dot export
   const int32_t* order;  // upy_options.order: processing order of root positions (or null)
@@ -130,6 +131,27 @@ __global__ void __launch_bounds__(128, UPY_MINB) upy_decompile_kernel(KParams P)
   Dc& C = dcs[threadIdx.x];
 #endif
   const u64 n_roots = (u64)P.A.n_roots;
+  if (P.schedule == 1 && P.lane_stride == 1) {
+    // warp-synchronous: a warp takes 32 consecutive positions of the order and its
+    // lanes start their objects together (similar neighbours then share code paths)
+    const int lane = threadIdx.x & 31;
+    while (true) {
+      u32 k0 = 0;
+      if (lane == 0) k0 = atomicAdd(P.next_root, 32u);
+      k0 = __shfl_sync(0xffffffffu, k0, 0);
+      if (k0 >= n_roots) break;
+      const u32 k = k0 + (u32)lane;
+      if (k < n_roots) {
+        const u32 r = P.order ? (u32)P.order[k] : k;
+        dc_reset(C, P, base);
+        Text out = {nullptr, 0, 0};
+        decompile_source(&C, (u32)P.A.roots[r], &opt, &out);
+        emit_result(P, C, r, out);
+      }
+      __syncwarp();
+    }
+    return;
+  }
   // each thread takes the next root from the global queue
   while (true) {
     u32 r = atomicAdd(P.next_root, 1u);
@@ -341,6 +363,7 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
   P.function_tree = opt ? opt->function_tree : 0;
   P.output = opt ? opt->output : 0;
   P.order = opt ? opt->order : nullptr;
+  P.schedule = opt ? opt->schedule : 0;
   u8* style_ws = ws + L.style_off;
   if (P.indent_len <= 64) {
     memcpy(P.indent, ind, P.indent_len);

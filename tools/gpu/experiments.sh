@@ -7,6 +7,7 @@
 # stackscan  stack-scan kernel: timing on C3 / C4 and a full ncu capture
 # decode311  3.11 decode timing and a full ncu capture on C3-3.11
 # schedule   root order input vs largest-tree-first (api.root_cost_order) on C2x / C4 / C2
+# sync       warp-synchronous root fetch (upy_options.schedule = 1) x root order
 # c5         the 16M-object corpus on one GPU, and torchrun N=1 lines (ours and the reference arm)
 set -u
 mkdir -p gpurun_out /tmp/ncu
@@ -56,6 +57,17 @@ schedule() {  # root order: input vs largest-tree-first, on the mixed-size shape
         2>&1 | tail -1 > gpurun_out/sched_${wl}_$sc.json
       python -c "import json; d=json.load(open('gpurun_out/sched_${wl}_$sc.json')); print('$wl $sc', round(d['value']), d['kernel_ms'], d['parity'])" \
         | tee -a gpurun_out/schedule.txt
+    done
+  done
+}
+sync() {  # warp-synchronous root fetch x root order, distinct C3 and the tiled C4
+  for wl in c3 c4; do
+    for sc in cost cost+sync similar similar+sync input+sync; do
+      st=2; [ $wl = c4 ] && st=1
+      timeout 900 python bench.py --workload $wl --schedule $sc --no-cpu --pyc 0 --no-extra --steps $st --warmup 1 \
+        2>&1 | tail -1 > gpurun_out/sync_${wl}_$sc.json
+      python -c "import json; d=json.load(open('gpurun_out/sync_${wl}_$sc.json')); print('$wl $sc', round(d['value']), d['kernel_ms'], d['parity'])" \
+        | tee -a gpurun_out/sync.txt
     done
   done
 }
