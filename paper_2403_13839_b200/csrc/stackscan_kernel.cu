@@ -134,12 +134,27 @@ __global__ void __launch_bounds__(SS_WARPS * 32, SS_MINB)
         }
         int sums[8];
         u32 segm = 0, unkm = 0, endm = 0;
+        u32 descs[8];
+        u32 rare = 0;  // arg terms other than none / n (popcount, bit tests, UNPACK_EX)
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          descs[q] = tb[w[3 * q + 2] & 0xFF];
+          rare |= ((descs[q] >> 8) & 7u) > SD_N;
+        }
+        const bool common = !__any_sync(0xffffffffu, rare);  // warp-uniform
 #pragma unroll
         for (int q = 0; q < 8; q++) {
           const u32 arg = w[3 * q + 1], meta = w[3 * q + 2];
-          const u32 desc = tb[meta & 0xFF];
+          const u32 desc = descs[q];
           const bool valid = (u32)q < cnt;
-          const int eff = valid ? stack_desc_effect(desc, arg) : 0;
+          int eff;
+          if (common) {  // base + mul * min(arg, 0x7FFF) (mul is 0 for term "none")
+            const int mul = (int)((desc >> 11) & 0xF) - (((desc >> 11) & 0x8) ? 16 : 0);
+            eff = (int)(int8_t)(desc & 0xFF) + mul * (int)(arg > 0x7FFF ? 0x7FFF : arg);
+          } else {
+            eff = stack_desc_effect(desc, arg);
+          }
+          eff = valid ? eff : 0;
           const u32 unk = valid ? (desc >> 15) & 1u : 0u;
           sums[q] = eff;
           pushes += (!unk && eff > 0) ? eff : 0;

@@ -71,6 +71,11 @@ sync() {  # warp-synchronous root fetch x root order, distinct C3 and the tiled 
     done
   done
 }
+quick_ss() {  # stack-scan parity + timing on C3 / C4
+  timeout 900 python -m pytest -m gpu -x -q tests/test_stackscan.py 2>&1 | tail -3 | tee gpurun_out/pytest_ss.txt
+  stackscan
+  python -c "import json; [print(f, json.load(open('gpurun_out/'+f+'.json'))['roofline_stackscan']) for f in ('bench_stackscan_c3','bench_stackscan_c4')]" | tee gpurun_out/ss.txt
+}
 c5() {  # one 16M-object corpus on this GPU (strong-scaling shape at N=1) + torchrun N=1 lines
   timeout 1800 python bench.py --workload c5 --no-cpu --pyc 0 --steps 3 --warmup 3 2>&1 | tail -1 > gpurun_out/bench_c5.json
   timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29611 \
