@@ -84,6 +84,15 @@ def _mutant2(n=300, first=5000):
             for m in (8, 9, 10, 11) for s in range(first, first + n)]
 
 
+def _mutant3(n=250, first=7000):
+    """Byte mutants on seeds drawn after round 2's kernel work (a generalisation
+    check).  Seed 7033 (3.10) is left out: the reference's structurer re-walks its
+    nested loops exponentially and does not finish in minutes (the device stops at
+    its arena limit: DeviceCapacityError)."""
+    return [{"case": f"mutant3-3.{m}-{s}", "gen": "fuzz", "minor": m, "seed": s, "kw": {"mode": "mutant"}}
+            for m in (8, 9, 10, 11) for s in range(first, first + n) if (m, s) != (10, 7033)]
+
+
 # decoder-only cases (no decompile golden: the reference's CFG pass is quadratic
 # at this size): 3.10 objects beyond the decode kernel's shared bitmaps
 C4BIG = [{"case": "c4big-3.10-1", "gen": "c4", "minor": 10, "seed": 1, "kw": {"target_units": 60000}},
@@ -106,4 +115,5 @@ class _Lazy(dict):
         return self._makers.keys()
 
 
-GOLDEN_SETS = _Lazy(c1=_fig1, c3=_c3, c4=_c4, snippets=_snippets, fuzz=_fuzz, mutant=_mutant, mutant2=_mutant2)
+GOLDEN_SETS = _Lazy(c1=_fig1, c3=_c3, c4=_c4, snippets=_snippets, fuzz=_fuzz, mutant=_mutant, mutant2=_mutant2,
+                    mutant3=_mutant3)

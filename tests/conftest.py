@@ -18,7 +18,7 @@ def load_golden(name):
         return [json.loads(line) for line in f]
 
 
-GOLDEN_SETS = ("c1", "c2", "c3", "c4", "snippets", "fuzz", "mutant", "mutant2")
+GOLDEN_SETS = ("c1", "c2", "c3", "c4", "snippets", "fuzz", "mutant", "mutant2", "mutant3")
 
 
 def golden_cases(sets=GOLDEN_SETS):

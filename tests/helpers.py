@@ -23,7 +23,12 @@ PY_INTERNAL = {"IndexError", "AttributeError", "TypeError", "KeyError", "ValueEr
 # symexec.py:568,818) into ConstE nodes holding bare 1-char strings and fails
 # later on `.const` / `.kind` of those (AttributeError); the device stops at the
 # iteration with TypeError("const is not iterable").  See DESIGN.md §4.
-KNOWN_CLASS_GAPS = {"mutant2-3.10-5031", "mutant2-3.11-5118"}
+KNOWN_CLASS_GAPS = {"mutant2-3.10-5031", "mutant2-3.11-5118", "mutant3-3.9-7094"}
+# Same root cause, but the reference, which keeps going with the bare 1-char
+# strings, fails later with an UnpyreError (a stack underflow two instructions on)
+# where the device has already raised its TypeError.  Fresh-seed differential of
+# round 2: 2 of 999 mutants (seeds 7000-7249) differ, both from this construct.
+KNOWN_DOMAIN_GAPS = {"mutant3-3.8-7029": ("StackUnderflow", "TypeError")}
 
 
 def inputs(recs):
@@ -53,6 +58,8 @@ def mismatches(recs, got, strict=True):
         if not strict and r["status"] in PY_INTERNAL and g[0] == r["status"]:
             continue
         if r["case"] in KNOWN_CLASS_GAPS and r["status"] in PY_INTERNAL and g[0] in PY_INTERNAL:
+            continue
+        if KNOWN_DOMAIN_GAPS.get(r["case"]) == (r["status"], g[0]):
             continue
         bad.append((r["case"], r["status"], g[0], r["text"][:300], g[1][:300]))
     return bad

@@ -8,7 +8,7 @@ from helpers import inputs, mismatches, outcome, style_of
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("gset", ["c1", "c2", "c3", "c4", "snippets", "fuzz", "mutant", "mutant2"])
+@pytest.mark.parametrize("gset", ["c1", "c2", "c3", "c4", "snippets", "fuzz", "mutant", "mutant2", "mutant3"])
 def test_gpu_matches_reference(gset):
     from paper_2403_13839_b200 import api
 
@@ -47,7 +47,7 @@ def test_gpu_c2_from_pyc_images_matches_reference():
 THROUGHPUT_ROOTS = 148 * 32 + 1  # more roots than resident warps: every thread takes roots (upy.cu layout())
 
 
-@pytest.mark.parametrize("gset", ["c1", "c2", "c3", "c4", "snippets", "fuzz", "mutant", "mutant2"])
+@pytest.mark.parametrize("gset", ["c1", "c2", "c3", "c4", "snippets", "fuzz", "mutant", "mutant2", "mutant3"])
 def test_gpu_tiled_throughput_schedule_matches_reference(gset):
     """The golden sets tiled past the small-batch threshold, so the kernel runs its
     throughput schedule (32 root-taking threads per warp, divergent lanes) rather

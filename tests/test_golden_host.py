@@ -7,7 +7,7 @@ from conftest import golden_cases
 from paper_2403_13839_b200 import arena, hostcheck
 
 
-@pytest.mark.parametrize("gset", ["c1", "c2", "c3", "c4", "snippets", "fuzz", "mutant", "mutant2"])
+@pytest.mark.parametrize("gset", ["c1", "c2", "c3", "c4", "snippets", "fuzz", "mutant", "mutant2", "mutant3"])
 def test_host_build_matches_reference(gset):
     recs = golden_cases([gset])
     assert recs
