@@ -510,7 +510,8 @@ def main():
     ap.add_argument("--pyc", type=int, default=1, help="also time the .pyc-bytes end-to-end path (0: skip)")
     ap.add_argument("--api-sample", type=int, default=16384)
     ap.add_argument("--schedule", default="auto",
-                    choices=["auto", "input", "cost", "similar", "input+sync", "cost+sync", "similar+sync"],
+                    choices=["auto", "input", "cost", "similar", "shape", "input+sync", "cost+sync", "similar+sync",
+                             "shape+sync"],
                     help="root order of the decompile kernel: cost = largest tree first (the API default); "
                          "auto = cost on distinct corpora, input on tiled pools (a size order would put a "
                          "pool object's copies side by side and the warps would run them in lockstep)")

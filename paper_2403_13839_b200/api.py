@@ -92,15 +92,16 @@ class DeviceArena:
         # computed on the device from the uploaded arena at every run (cost_order)
         # and handed to the kernel as upy_options.order; results stay in input order.
         base_sched, _, sync = schedule.partition("+")
-        if base_sched not in ("input", "cost", "similar") or sync not in ("", "sync"):
-            raise ValueError(f"schedule must be input|cost|similar[+sync], not {schedule!r}")
+        if base_sched not in ("input", "cost", "similar", "shape") or sync not in ("", "sync"):
+            raise ValueError(f"schedule must be input|cost|similar|shape[+sync], not {schedule!r}")
         self.schedule = base_sched if arena.n_roots > 1 else "input"
         self.warp_sync = 1 if sync else 0
-        if self.schedule == "similar":  # experiment: host-computed prefix-similarity order
-            self._order = torch.from_numpy(root_similarity_order(arena).astype(np.int32)).to(self.device)
+        if self.schedule in ("similar", "shape"):  # experiments: host-computed orders
+            fn = root_similarity_order if self.schedule == "similar" else root_shape_order
+            self._order = torch.from_numpy(fn(arena).astype(np.int32)).to(self.device)
         roots = arena.section("roots")
         self._trees_contiguous = bool(len(roots) < 2 or np.all(np.diff(roots.astype(np.int64)) > 0))
-        if self.schedule != "similar":
+        if self.schedule not in ("similar", "shape"):
             self._order = None
         if not slots and not arena_bytes:
             slots = self._memory_slots(arena)
@@ -251,6 +252,25 @@ def cost_order(blob, offsets, counts, trees_contiguous):
     else:
         cost = lens[roots]
     return torch.sort(cost, descending=True, stable=True).indices.to(torch.int32)
+
+
+def root_shape_order(arena: Arena, prefix=64):
+    """Experiment: root positions sorted by their first `prefix` OPCODES (args
+    ignored), so neighbouring roots share the longest possible run of identical
+    control flow through the transfer functions (profiles/r02/schedule/)."""
+    objs = arena.section("objs")
+    roots = arena.section("roots").astype(np.int64)
+    offs = objs["code_off"].astype(np.int64)[roots]
+    lens = objs["code_len"].astype(np.int64)[roots]
+    by = arena.section("bytes")
+    j = np.arange(prefix, dtype=np.int64)
+    idx = np.minimum(offs[:, None] + 2 * j[None, :], len(by) - 1)
+    pre = np.where(2 * j[None, :] < lens[:, None], by[idx], 0).astype(np.uint8)
+    words = pre.reshape(len(roots), prefix // 8, 8)
+    keys = [lens]
+    for w in range(prefix // 8 - 1, -1, -1):
+        keys.append(words[:, w, :].copy().view(">u8").ravel())
+    return np.lexsort(keys)
 
 
 def root_similarity_order(arena: Arena, prefix=32):

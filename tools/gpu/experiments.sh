@@ -76,6 +76,14 @@ quick_ss() {  # stack-scan parity + timing on C3 / C4
   stackscan
   python -c "import json; [print(f, json.load(open('gpurun_out/'+f+'.json'))['roofline_stackscan']) for f in ('bench_stackscan_c3','bench_stackscan_c4')]" | tee gpurun_out/ss.txt
 }
+shape() {  # opcode-prefix order (args ignored), with and without warp-synchronous fetch, on distinct C3
+  for sc in cost shape shape+sync cost shape+sync; do
+    timeout 900 python bench.py --workload c3 --schedule $sc --no-cpu --pyc 0 --no-extra --steps 3 --warmup 2 \
+      2>&1 | tail -1 > gpurun_out/shape_c3_$sc.json
+    python -c "import json; d=json.load(open('gpurun_out/shape_c3_$sc.json')); print('c3 $sc', round(d['value']), d['kernel_ms'], d['parity'])" \
+      | tee -a gpurun_out/shape.txt
+  done
+}
 c5() {  # one 16M-object corpus on this GPU (strong-scaling shape at N=1) + torchrun N=1 lines
   timeout 1800 python bench.py --workload c5 --no-cpu --pyc 0 --steps 3 --warmup 3 2>&1 | tail -1 > gpurun_out/bench_c5.json
   timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29611 \
