@@ -89,7 +89,9 @@ typedef struct {
   uint64_t arena_bytes;      /* bytes per slot arena; 0 = auto from max_code_len */
   int32_t skip_decode;       /* 1: reuse the records of a previous decode_only call on the same workspace */
   int32_t schedule;          /* 0: each thread takes the next root position; 1: warp-synchronous (a warp
-                                takes 32 consecutive positions of `order` and its lanes start together) */
+                                takes 32 consecutive positions of `order` and its lanes start together);
+                                2: warp-synchronous with statement-parallel emission (the warp emits
+                                each of its 32 trees with the statements spread over its lanes) */
   int32_t max_depth;         /* device recursion guard (UPY_ST_DEPTH_LIMIT); 0 = default 600 */
   int32_t function_tree;     /* 1: emit_module([function_tree(root)]) without validation -- the
                                 reference CLI's --function path (cli.py:75-78) -- instead of

@@ -91,11 +91,13 @@ class DeviceArena:
         # tail, and lanes of a warp get objects of similar size).  The order is
         # computed on the device from the uploaded arena at every run (cost_order)
         # and handed to the kernel as upy_options.order; results stay in input order.
-        base_sched, _, sync = schedule.partition("+")
-        if base_sched not in ("input", "cost", "similar", "shape") or sync not in ("", "sync"):
-            raise ValueError(f"schedule must be input|cost|similar|shape[+sync], not {schedule!r}")
+        base_sched, _, mode = schedule.partition("+")
+        if base_sched not in ("input", "cost", "similar", "shape") or mode not in ("", "sync", "coemit"):
+            raise ValueError(f"schedule must be input|cost|similar|shape[+sync|+coemit], not {schedule!r}")
         self.schedule = base_sched if arena.n_roots > 1 else "input"
-        self.warp_sync = 1 if sync else 0
+        # kernel schedule: 0 each thread takes the next root, 1 warp-synchronous,
+        # 2 warp-synchronous with statement-parallel emission (upy_options.schedule)
+        self.warp_sync = {"": 0, "sync": 1, "coemit": 2}[mode]
         if self.schedule in ("similar", "shape"):  # experiments: host-computed orders
             fn = root_similarity_order if self.schedule == "similar" else root_shape_order
             self._order = torch.from_numpy(fn(arena).astype(np.int32)).to(self.device)
@@ -343,8 +345,11 @@ def tree_sizes(arena: Arena, roots) -> tuple:
     return code, payload
 
 
+DEFAULT_SCHEDULE = os.environ.get("UPY_SCHEDULE", "cost")
+
+
 def run_arena(arena: Arena, style=None, device=None, retries=3, function_tree=False, output=0,
-              schedule="cost") -> BatchResult:
+              schedule=None) -> BatchResult:
     """Decompile every root of a packed arena on the GPU.
 
     Roots that hit a device capacity limit (per-thread arena, output buffer) are
@@ -354,7 +359,8 @@ def run_arena(arena: Arena, style=None, device=None, retries=3, function_tree=Fa
     torch = _torch()
     dev = torch.device(device or "cuda")
     with torch.cuda.device(dev):
-        da = DeviceArena(arena, style, dev, function_tree=function_tree, output=output, schedule=schedule)
+        da = DeviceArena(arena, style, dev, function_tree=function_tree, output=output,
+                         schedule=schedule or DEFAULT_SCHEDULE)
         da.upload()
         da.run()
         res = da.fetch()

@@ -218,6 +218,21 @@ struct Emitter {
     depth--;
   }
   HD void stmt(Node* s);
+  HD NOINL void funcdef_head(Node* s) {  // decorators and the def line (emitter.py:285-295)
+    for (u32 q = 0; q < s->l2->n && !C->err; q++) {
+      line_start();
+      t_put(C, out, '@');
+      concat_none(sub(out, s->l2->d[q]));
+      line_end();
+    }
+    line_start();
+    t_puts(C, out, "def ");
+    t_str(C, out, s->s);
+    t_put(C, out, '(');
+    params(out, s->p);
+    t_puts(C, out, "):");
+    line_end();
+  }
   HD void emit_if(Node* s, const char* kw);
   HD void params(Text* t, Node* p);
   // Python-None text.  In the reference a Name whose id is None (an
@@ -1326,19 +1341,7 @@ HD NOINL void Emitter::stmt(Node* s) {  // emitter.py:136-283
       return;
     }
     case S_FUNCDEF:
-      for (u32 q = 0; q < s->l2->n && !C->err; q++) {
-        line_start();
-        t_put(C, out, '@');
-        concat_none(sub(out, s->l2->d[q]));
-        line_end();
-      }
-      line_start();
-      t_puts(C, out, "def ");
-      t_str(C, out, s->s);
-      t_put(C, out, '(');
-      params(out, s->p);
-      t_puts(C, out, "):");
-      line_end();
+      funcdef_head(s);
       block(s->l1);
       return;
     case S_CLASSDEF: {

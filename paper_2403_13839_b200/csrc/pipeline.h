@@ -232,6 +232,11 @@ HD inline void ds_stage(Dc* C, SourceJob* S, int stage) {
 // per stage summed over all roots, read back with upy_prof_read.
 __device__ unsigned long long g_stage_cycles[DS_STAGES];
 #endif
+// Stages validate .. finish of decompile_source: the tree to emit (S->tree), or C->err.
+HD inline void decompile_tree(Dc* C, SourceJob* S) {
+  for (int st = 0; st < DS_EMIT; st++) ds_stage(C, S, st);
+}
+
 HD inline void decompile_source(Dc* C, u32 oi, const EmitOpts* opt, Text* out) {
   SourceJob S;
   S.oi = oi;

@@ -107,6 +107,128 @@ __device__ __forceinline__ void emit_result(const KParams& P, Dc& C, u32 r, cons
   P.out.aux[2 * (u64)r + 1] = C.aux1;
 }
 
+// ---------------------------------------------------------------- statement-parallel emit
+// North-star subsystem (5): a warp emits one object at a time with its statements
+// spread over the 32 lanes.  The emitter is stateless across statements apart from
+// the indentation depth (emitter.py:112-132), so statement s rendered on its own at
+// the right depth is exactly its slice of the sequential text.  Each lane renders
+// statements s = lane, lane + 32, ... into its own scratch (its arena above its live
+// data, a fresh error state and message buffer), the lengths are summed, the owner
+// reserves the object's range of the flat output once, and a per-round exclusive
+// scan of the statement lengths places every lane's text.  The first failing
+// statement in order decides the error, as in the sequential emitter.  A root that
+// is one `def` (every function root: root_tree_of, pipeline.py:121-130) is split
+// into its header lines (decorators, the def line; the owner lane) and its body at
+// depth 1.
+__device__ __forceinline__ void copy_bytes(char* dst, const char* src, u32 n) {
+#pragma unroll 1
+  for (u32 i = 0; i < n; i++) dst[i] = src[i];
+}
+
+__device__ __noinline__ void coemit_object(const KParams& P, Dc& C, const EmitOpts& opt, int j, u32 r, u32 oi,
+                                           NV* tree) {
+  const int lane = threadIdx.x & 31;
+  Dc E = C;  // scratch context on this lane's arena, above its live data
+  E.err = 0;
+  E.aux0 = E.aux1 = 0;
+  E.depth = 0;
+  E.msg = (char*)ualloc(&E, MSG_BYTES);
+  E.msg_len = 0;
+  E.msg_cap = E.err ? 0 : MSG_BYTES;
+  if (E.err) E.msg = C.msg;  // no room: the overflow status stands, the message is empty
+  const bool split = tree->n == 1 && tree->d[0]->k == S_FUNCDEF;
+  NV* body = split ? tree->d[0]->l1 : tree;
+  const int depth = split ? 1 : 0;
+  const u32 nb = body->n;
+  Emitter EM;
+  EM.C = &E;
+  EM.indent = opt.indent;
+  // the owner's header lines: provenance comment, decorators + def line, or `pass`
+  Text head = {nullptr, 0, 0};
+  if (lane == j) {
+    EM.out = &head;
+    EM.depth = 0;
+    if (opt.header) {
+      t_puts(&E, &head, "# decompiled by ");
+      t_str(&E, &head, opt.tool);
+      t_puts(&E, &head, " from ");
+      Str qn = obj_qualname(&E, oi);
+      t_str(&E, &head, qn.n ? qn : obj_name(&E, oi));
+      t_puts(&E, &head, " (python 3.");
+      t_i64(&E, &head, obj_at(&E, oi)->minor);
+      t_puts(&E, &head, ")\n");
+    }
+    if (split) EM.funcdef_head(tree->d[0]);
+    if (!nb) {
+      EM.depth = depth;
+      EM.simple_line("pass");
+    }
+  }
+  const int head_err = __shfl_sync(0xffffffffu, E.err, j);
+  // this lane's statements, rendered back to back; ends[] marks where each stops
+  Text mine = {nullptr, 0, 0};
+  const u32 m = nb > (u32)lane ? (nb - (u32)lane + 31) / 32 : 0;
+  u32* ends = m ? (u32*)ualloc(&E, 4ull * m) : nullptr;
+  u32 fail = 0xFFFFFFFFu;  // index of this lane's first failing statement
+  if (!head_err) {
+    EM.out = &mine;
+    EM.depth = depth;
+    for (u32 q = 0; q < m && !E.err; q++) {
+      EM.stmt(body->d[(u64)lane + 32ull * q]);
+      if (E.err) fail = (u32)lane + 32u * q;
+      else ends[q] = mine.n;
+    }
+    if (E.err && fail == 0xFFFFFFFFu) fail = (u32)lane;  // the scratch itself overflowed (retryable)
+  }
+  const u32 first_fail = __reduce_min_sync(0xffffffffu, fail);
+  // result: an error (header first, then the lowest failing statement) or the text
+  int src_lane = -1;
+  if (head_err) src_lane = j;
+  else if (first_fail != 0xFFFFFFFFu) src_lane = (int)(first_fail & 31u);
+  if (src_lane >= 0) {
+    if (lane == src_lane) {  // the failing context's status and message (emit_result)
+      Text none = {nullptr, 0, 0};
+      emit_result(P, E, r, none);
+    }
+    return;
+  }
+  const u32 head_len = __shfl_sync(0xffffffffu, head.n, j);
+  const u32 total = head_len + __reduce_add_sync(0xffffffffu, mine.n);
+  u64 off = 0;
+  int status = 0;
+  if (lane == j) {
+    const u64 resv = ((u64)total + 15) & ~(u64)15;
+    off = atomicAdd((unsigned long long*)P.out.text_used, (unsigned long long)resv);
+    if (off + resv > P.out.text_cap) status = UPY_ST_OUTPUT_OVERFLOW;
+    else copy_bytes((char*)P.out.text + off, head.d, head.n);
+  }
+  off = __shfl_sync(0xffffffffu, off, j);
+  status = __shfl_sync(0xffffffffu, status, j);
+  if (!status) {
+    u64 base = off + head_len;
+    for (u32 q = 0; 32ull * q < nb; q++) {  // round q: statements 32q .. 32q+31
+      const bool has = q < m;
+      const u32 beg = has ? (q ? ends[q - 1] : 0u) : 0u;
+      const u32 len = has ? ends[q] - beg : 0u;
+      u32 incl = len;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const u32 o = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += o;
+      }
+      if (len) copy_bytes((char*)P.out.text + base + (incl - len), mine.d + beg, len);
+      base += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+  if (lane == j) {
+    P.out.text_off[r] = off;
+    P.out.text_len[r] = status ? 0 : total;
+    P.out.status[r] = status;
+    P.out.aux[2 * (u64)r] = 0;
+    P.out.aux[2 * (u64)r + 1] = 0;
+  }
+}
+
 __global__ void __launch_bounds__(128, UPY_MINB) upy_decompile_kernel(KParams P) {
   // Small batches (fewer roots than resident warps) run one root-taking thread per
   // warp: a lone thread issues without divergence serialisation, and the roots
@@ -131,6 +253,41 @@ __global__ void __launch_bounds__(128, UPY_MINB) upy_decompile_kernel(KParams P)
   Dc& C = dcs[threadIdx.x];
 #endif
   const u64 n_roots = (u64)P.A.n_roots;
+  if (P.schedule == 2 && P.lane_stride == 1) {
+    // warp-synchronous + statement-parallel emission: every lane builds its own
+    // object's tree (validate .. finish), then the warp emits the 32 trees in turn
+    const int lane = threadIdx.x & 31;
+    while (true) {
+      u32 k0 = 0;
+      if (lane == 0) k0 = atomicAdd(P.next_root, 32u);
+      k0 = __shfl_sync(0xffffffffu, k0, 0);
+      if (k0 >= n_roots) break;
+      const u32 k = k0 + (u32)lane;
+      const bool has = k < n_roots;
+      const u32 r = has ? (P.order ? (u32)P.order[k] : k) : 0u;
+      dc_reset(C, P, base);
+      SourceJob S;
+      S.oi = has ? (u32)P.A.roots[r] : 0u;
+      S.opt = &opt;
+      S.tree = nullptr;
+      Text none = {nullptr, 0, 0};
+      S.out = &none;
+      if (has) decompile_tree(&C, &S);
+      __syncwarp();
+      const u32 has_m = __ballot_sync(0xffffffffu, has);
+      const u32 err_m = __ballot_sync(0xffffffffu, has && C.err);
+      if (err_m & (1u << lane)) emit_result(P, C, r, none);  // failed before emit: its message
+      for (u32 todo = has_m & ~err_m; todo; todo &= todo - 1) {
+        const int j = __ffs((int)todo) - 1;
+        const u32 rj = __shfl_sync(0xffffffffu, r, j);
+        const u32 oj = __shfl_sync(0xffffffffu, S.oi, j);
+        NV* tj = (NV*)__shfl_sync(0xffffffffu, (unsigned long long)S.tree, j);
+        coemit_object(P, C, opt, j, rj, oj, tj);
+      }
+      __syncwarp();
+    }
+    return;
+  }
   if (P.schedule == 1 && P.lane_stride == 1) {
     // warp-synchronous: a warp takes 32 consecutive positions of the order and its
     // lanes start their objects together (similar neighbours then share code paths)

@@ -84,6 +84,24 @@ shape() {  # opcode-prefix order (args ignored), with and without warp-synchrono
       | tee -a gpurun_out/shape.txt
   done
 }
+coemit() {  # statement-parallel emission: parity on every golden set (throughput mode) + A/B on C3 / C3-3.11 / C4
+  UPY_SCHEDULE=cost+coemit timeout 1500 python -m pytest -m gpu -x -q tests/test_golden_gpu.py tests/test_cli.py \
+    2>&1 | tail -4 | tee gpurun_out/pytest_coemit.txt
+  for wl in c3 c3_311; do
+    for sc in cost cost+coemit cost cost+coemit; do
+      timeout 900 python bench.py --workload $wl --schedule $sc --no-cpu --pyc 0 --no-extra --steps 3 --warmup 2 \
+        2>&1 | tail -1 > gpurun_out/coemit_${wl}_$sc.json
+      python -c "import json; d=json.load(open('gpurun_out/coemit_${wl}_$sc.json')); print('$wl $sc', round(d['value']), d['kernel_ms'], d['parity'])" \
+        | tee -a gpurun_out/coemit.txt
+    done
+  done
+  for sc in input input+coemit; do
+    timeout 900 python bench.py --workload c4 --schedule $sc --no-cpu --pyc 0 --no-extra --steps 1 --warmup 1 \
+      2>&1 | tail -1 > gpurun_out/coemit_c4_$sc.json
+    python -c "import json; d=json.load(open('gpurun_out/coemit_c4_$sc.json')); print('c4 $sc', round(d['value']), d['kernel_ms'], d['parity'])" \
+      | tee -a gpurun_out/coemit.txt
+  done
+}
 c5() {  # one 16M-object corpus on this GPU (strong-scaling shape at N=1) + torchrun N=1 lines
   timeout 1800 python bench.py --workload c5 --no-cpu --pyc 0 --steps 3 --warmup 3 2>&1 | tail -1 > gpurun_out/bench_c5.json
   timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29611 \
