@@ -92,7 +92,7 @@ class DeviceArena:
         # computed on the device from the uploaded arena at every run (cost_order)
         # and handed to the kernel as upy_options.order; results stay in input order.
         base_sched, _, mode = schedule.partition("+")
-        if base_sched not in ("input", "cost", "similar", "shape") or \
+        if base_sched not in ("input", "cost", "similar", "shape", "dshape1", "dshape2", "dshape4") or \
                 mode not in ("", "thread", "sync", "coemit"):
             raise ValueError(f"schedule must be input|cost|similar|shape[+thread|+sync|+coemit], "
                              f"not {schedule!r}")
@@ -176,6 +176,10 @@ class DeviceArena:
                     with torch.cuda.stream(s):
                         self._order = cost_order(self.dev, self.arena.offsets, self.arena.counts,
                                                  self._trees_contiguous)
+                elif self.schedule.startswith("dshape"):  # experiment: device opcode-shape order
+                    with torch.cuda.stream(s):
+                        self._order = shape_order(self.dev, self.arena.offsets, self.arena.counts,
+                                                  int(self.schedule[6:]))
                 self.opts.order = self._order.data_ptr() if self._order is not None else None
                 self.opts.schedule = self.warp_sync
             rc = self.lib.upy_decompile_batch(C.byref(self.A), C.byref(self.opts), C.byref(self.out),
@@ -307,6 +311,41 @@ def root_similarity_order(arena: Arena, prefix=32):
     for w in range(prefix // 8 - 1, -1, -1):  # lexsort: last key is primary
         keys.append(words[:, w, :].copy().view(">u8").ravel())
     return np.lexsort(keys)
+
+
+def shape_order(blob, offsets, counts, n_words):
+    """Device form of the opcode-shape order: roots sorted by their first
+    8 * n_words opcodes (args ignored), most significant first, via n_words chained
+    stable sorts of 64-bit keys (int32 tensor on blob's device)."""
+    import torch
+
+    from .arena import OBJ_DTYPE
+
+    n_objs, n_roots = int(counts["objs"]), int(counts["roots"])
+    o0, r0, b0 = int(offsets["objs"]), int(offsets["roots"]), int(offsets["bytes"])
+    n_bytes = int(counts["bytes"])
+    rec = OBJ_DTYPE.itemsize
+    co_at = OBJ_DTYPE.fields["code_off"][1]
+    cl_at = OBJ_DTYPE.fields["code_len"][1]
+    objs = blob[o0:o0 + n_objs * rec].view(n_objs, rec)
+    roots = blob[r0:r0 + 4 * n_roots].view(torch.int32).to(torch.int64)
+    code_off = objs[:, co_at:co_at + 8].contiguous().view(torch.int64).view(-1)[roots]
+    code_len = objs[:, cl_at:cl_at + 4].contiguous().view(torch.int32).view(-1).to(torch.int64)[roots]
+    by = blob[b0:b0 + n_bytes]
+    j = torch.arange(8 * n_words, device=blob.device, dtype=torch.int64)
+    idx = (code_off[:, None] + 2 * j[None, :]).clamp_(max=max(n_bytes - 1, 0))
+    ops = torch.where(2 * j[None, :] < code_len[:, None], by[idx], torch.zeros((), dtype=torch.uint8,
+                                                                                     device=blob.device))
+    perm = torch.arange(n_roots, device=blob.device)
+    weights = (256 ** torch.arange(7, -1, -1, device=blob.device, dtype=torch.int64))
+    for w in range(n_words - 1, -1, -1):  # least significant word first (stable)
+        word = ops[:, 8 * w:8 * w + 8].to(torch.int64)
+        # big-endian 8 bytes as a signed 64-bit key, top byte offset by -128 so the
+        # signed order is the unsigned (lexicographic) one
+        key = (word[:, 0] - 128) * weights[0] + (word[:, 1:] * weights[1:]).sum(1)
+        k = key[perm]
+        perm = perm[torch.sort(k, stable=True).indices]
+    return perm.to(torch.int32)
 
 
 def root_cost_order(arena: Arena):

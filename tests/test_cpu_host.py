@@ -185,3 +185,26 @@ def test_cost_order_matches_host_restatement():
         got = api.cost_order(torch.from_numpy(a.blob), a.offsets, a.counts, contiguous).numpy()
         assert np.array_equal(got, api.root_cost_order(a))
         assert sorted(got.tolist()) == list(range(a.n_roots))
+
+
+def test_shape_order_is_lexicographic_on_opcodes():
+    """api.shape_order (torch, chained stable sorts of 64-bit keys; run here on a
+    CPU tensor) equals a numpy lexsort of the roots' first 8*n opcodes, input
+    order breaking ties."""
+    import numpy as np
+    import torch
+
+    from paper_2403_13839_b200 import api
+    from paper_2403_13839_b200.synth import c3fast
+
+    a = c3fast.c3_arena(3000, 11)
+    objs, roots = a.section("objs"), a.section("roots").astype(np.int64)
+    offs = objs["code_off"].astype(np.int64)[roots]
+    lens = objs["code_len"].astype(np.int64)[roots]
+    by = a.section("bytes")
+    for nw in (1, 2, 4):
+        j = np.arange(8 * nw)
+        ops = np.where(2 * j[None, :] < lens[:, None], by[np.minimum(offs[:, None] + 2 * j[None, :], len(by) - 1)], 0)
+        want = np.lexsort([np.arange(len(roots))] + [ops[:, c] for c in range(8 * nw - 1, -1, -1)])
+        got = api.shape_order(torch.from_numpy(a.blob), a.offsets, a.counts, nw).numpy()
+        assert np.array_equal(got, want), nw

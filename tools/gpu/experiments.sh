@@ -102,6 +102,14 @@ coemit() {  # statement-parallel emission: parity on every golden set (throughpu
       | tee -a gpurun_out/coemit.txt
   done
 }
+dshape() {  # device-side opcode-shape orders (1, 2, 4 chained 64-bit sorts) vs cost, distinct C3
+  for sc in cost dshape1 dshape2 dshape4 cost dshape2 dshape4; do
+    timeout 900 python bench.py --workload c3 --schedule $sc --no-cpu --pyc 0 --no-extra --steps 3 --warmup 2 \
+      2>&1 | tail -1 > gpurun_out/dshape_c3_$sc.json
+    python -c "import json; d=json.load(open('gpurun_out/dshape_c3_$sc.json')); print('c3 $sc', round(d['value']), round(d['e2e']['value']), d['kernel_ms'], d['parity'])" \
+      | tee -a gpurun_out/dshape.txt
+  done
+}
 c5() {  # one 16M-object corpus on this GPU (strong-scaling shape at N=1) + torchrun N=1 lines
   timeout 1800 python bench.py --workload c5 --no-cpu --pyc 0 --steps 3 --warmup 3 2>&1 | tail -1 > gpurun_out/bench_c5.json
   timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29611 \
