@@ -125,107 +125,123 @@ __device__ __forceinline__ void copy_bytes(char* dst, const char* src, u32 n) {
   for (u32 i = 0; i < n; i++) dst[i] = src[i];
 }
 
-__device__ __noinline__ void coemit_object(const KParams& P, Dc& C, const EmitOpts& opt, int j, u32 r, u32 oi,
-                                           NV* tree) {
+// One round: lane k owns object k (ok: tree built, r its root position, oi its
+// object).  Every lane first renders its OWN object's header lines in parallel (the
+// provenance comment, decorators and the def line of a single-def root, `pass` for
+// an empty body); then the warp emits the objects one after another, statements
+// spread over the lanes.  One scratch context per lane for the whole round.
+__device__ __noinline__ void coemit_round(const KParams& P, Dc& C, const EmitOpts& opt, bool ok, u32 r, u32 oi,
+                                          NV* tree) {
   const int lane = threadIdx.x & 31;
-  Dc E = C;  // scratch context on this lane's arena, above its live data
-  E.err = 0;
-  E.aux0 = E.aux1 = 0;
-  E.depth = 0;
-  E.msg = (char*)ualloc(&E, MSG_BYTES);
-  E.msg_len = 0;
-  E.msg_cap = E.err ? 0 : MSG_BYTES;
-  if (E.err) E.msg = C.msg;  // no room: the overflow status stands, the message is empty
-  const bool split = tree->n == 1 && tree->d[0]->k == S_FUNCDEF;
-  NV* body = split ? tree->d[0]->l1 : tree;
-  const int depth = split ? 1 : 0;
-  const u32 nb = body->n;
+  Dc H = C;  // scratch context on this lane's arena, above its live data
+  H.err = 0;
+  H.aux0 = H.aux1 = 0;
+  H.depth = 0;
+  H.msg = (char*)ualloc(&H, MSG_BYTES);
+  H.msg_len = 0;
+  H.msg_cap = H.err ? 0 : MSG_BYTES;
+  if (H.err) H.msg = C.msg;
   Emitter EM;
-  EM.C = &E;
+  EM.C = &H;
   EM.indent = opt.indent;
-  // the owner's header lines: provenance comment, decorators + def line, or `pass`
+  // own header
+  NV* body = nullptr;
+  int depth = 0;
   Text head = {nullptr, 0, 0};
-  if (lane == j) {
+  if (ok) {
+    const bool split = tree->n == 1 && tree->d[0]->k == S_FUNCDEF;
+    body = split ? tree->d[0]->l1 : tree;
+    depth = split ? 1 : 0;
     EM.out = &head;
     EM.depth = 0;
     if (opt.header) {
-      t_puts(&E, &head, "# decompiled by ");
-      t_str(&E, &head, opt.tool);
-      t_puts(&E, &head, " from ");
-      Str qn = obj_qualname(&E, oi);
-      t_str(&E, &head, qn.n ? qn : obj_name(&E, oi));
-      t_puts(&E, &head, " (python 3.");
-      t_i64(&E, &head, obj_at(&E, oi)->minor);
-      t_puts(&E, &head, ")\n");
+      t_puts(&H, &head, "# decompiled by ");
+      t_str(&H, &head, opt.tool);
+      t_puts(&H, &head, " from ");
+      Str qn = obj_qualname(&H, oi);
+      t_str(&H, &head, qn.n ? qn : obj_name(&H, oi));
+      t_puts(&H, &head, " (python 3.");
+      t_i64(&H, &head, obj_at(&H, oi)->minor);
+      t_puts(&H, &head, ")\n");
     }
     if (split) EM.funcdef_head(tree->d[0]);
-    if (!nb) {
+    if (!body->n) {
       EM.depth = depth;
       EM.simple_line("pass");
     }
+    if (H.err) {  // the header failed: that is the object's result
+      Text none = {nullptr, 0, 0};
+      emit_result(P, H, r, none);
+      ok = false;
+    }
   }
-  const int head_err = __shfl_sync(0xffffffffu, E.err, j);
-  // this lane's statements, rendered back to back; ends[] marks where each stops
-  Text mine = {nullptr, 0, 0};
-  const u32 m = nb > (u32)lane ? (nb - (u32)lane + 31) / 32 : 0;
-  u32* ends = m ? (u32*)ualloc(&E, 4ull * m) : nullptr;
-  u32 fail = 0xFFFFFFFFu;  // index of this lane's first failing statement
-  if (!head_err) {
+  const u64 mark = H.used;
+  for (u32 todo = __ballot_sync(0xffffffffu, ok); todo; todo &= todo - 1) {
+    const int j = __ffs((int)todo) - 1;
+    NV* bj = (NV*)__shfl_sync(0xffffffffu, (unsigned long long)body, j);
+    const int dj = __shfl_sync(0xffffffffu, depth, j);
+    const u32 rj = __shfl_sync(0xffffffffu, r, j);
+    const u32 nb = bj->n;
+    H.used = mark;
+    H.err = 0;
+    H.msg_len = 0;
+    H.aux0 = H.aux1 = 0;
+    // this lane's statements of object j, back to back; ends[] marks where each stops
+    Text mine = {nullptr, 0, 0};
+    const u32 m = nb > (u32)lane ? (nb - (u32)lane + 31) / 32 : 0;
+    u32* ends = m ? (u32*)ualloc(&H, 4ull * m) : nullptr;
+    u32 fail = H.err ? (u32)lane : 0xFFFFFFFFu;  // scratch overflow: retryable
     EM.out = &mine;
-    EM.depth = depth;
-    for (u32 q = 0; q < m && !E.err; q++) {
-      EM.stmt(body->d[(u64)lane + 32ull * q]);
-      if (E.err) fail = (u32)lane + 32u * q;
+    EM.depth = dj;
+    for (u32 q = 0; q < m && !H.err; q++) {
+      EM.stmt(bj->d[(u64)lane + 32ull * q]);
+      if (H.err) fail = (u32)lane + 32u * q;
       else ends[q] = mine.n;
     }
-    if (E.err && fail == 0xFFFFFFFFu) fail = (u32)lane;  // the scratch itself overflowed (retryable)
-  }
-  const u32 first_fail = __reduce_min_sync(0xffffffffu, fail);
-  // result: an error (header first, then the lowest failing statement) or the text
-  int src_lane = -1;
-  if (head_err) src_lane = j;
-  else if (first_fail != 0xFFFFFFFFu) src_lane = (int)(first_fail & 31u);
-  if (src_lane >= 0) {
-    if (lane == src_lane) {  // the failing context's status and message (emit_result)
-      Text none = {nullptr, 0, 0};
-      emit_result(P, E, r, none);
-    }
-    return;
-  }
-  const u32 head_len = __shfl_sync(0xffffffffu, head.n, j);
-  const u32 total = head_len + __reduce_add_sync(0xffffffffu, mine.n);
-  u64 off = 0;
-  int status = 0;
-  if (lane == j) {
-    const u64 resv = ((u64)total + 15) & ~(u64)15;
-    off = atomicAdd((unsigned long long*)P.out.text_used, (unsigned long long)resv);
-    if (off + resv > P.out.text_cap) status = UPY_ST_OUTPUT_OVERFLOW;
-    else copy_bytes((char*)P.out.text + off, head.d, head.n);
-  }
-  off = __shfl_sync(0xffffffffu, off, j);
-  status = __shfl_sync(0xffffffffu, status, j);
-  if (!status) {
-    u64 base = off + head_len;
-    for (u32 q = 0; 32ull * q < nb; q++) {  // round q: statements 32q .. 32q+31
-      const bool has = q < m;
-      const u32 beg = has ? (q ? ends[q - 1] : 0u) : 0u;
-      const u32 len = has ? ends[q] - beg : 0u;
-      u32 incl = len;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const u32 o = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= d) incl += o;
+    const u32 first_fail = __reduce_min_sync(0xffffffffu, fail);
+    if (first_fail != 0xFFFFFFFFu) {  // the first failing statement in order decides
+      if (lane == (int)(first_fail & 31u)) {
+        Text none = {nullptr, 0, 0};
+        emit_result(P, H, rj, none);
       }
-      if (len) copy_bytes((char*)P.out.text + base + (incl - len), mine.d + beg, len);
-      base += __shfl_sync(0xffffffffu, incl, 31);
+      continue;
     }
-  }
-  if (lane == j) {
-    P.out.text_off[r] = off;
-    P.out.text_len[r] = status ? 0 : total;
-    P.out.status[r] = status;
-    P.out.aux[2 * (u64)r] = 0;
-    P.out.aux[2 * (u64)r + 1] = 0;
+    const u32 head_len = __shfl_sync(0xffffffffu, head.n, j);
+    const u32 total = head_len + __reduce_add_sync(0xffffffffu, mine.n);
+    u64 off = 0;
+    int status = 0;
+    if (lane == j) {
+      const u64 resv = ((u64)total + 15) & ~(u64)15;
+      off = atomicAdd((unsigned long long*)P.out.text_used, (unsigned long long)resv);
+      if (off + resv > P.out.text_cap) status = UPY_ST_OUTPUT_OVERFLOW;
+      else if (head.n) copy16(P.out.text + off, head.d, head.n);  // both 16-B aligned; 16-B granular
+    }
+    off = __shfl_sync(0xffffffffu, off, j);
+    status = __shfl_sync(0xffffffffu, status, j);
+    if (!status) {
+      u64 pos = off + head_len;
+      for (u32 q = 0; 32ull * q < nb; q++) {  // round q: statements 32q .. 32q+31
+        const bool has = q < m;
+        const u32 beg = has ? (q ? ends[q - 1] : 0u) : 0u;
+        const u32 len = has ? ends[q] - beg : 0u;
+        u32 incl = len;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const u32 o = __shfl_up_sync(0xffffffffu, incl, d);
+          if (lane >= d) incl += o;
+        }
+        __syncwarp();  // the header's 16-B stores end before statement bytes land next to them
+        if (len) copy_bytes((char*)P.out.text + pos + (incl - len), mine.d + beg, len);
+        pos += __shfl_sync(0xffffffffu, incl, 31);
+      }
+    }
+    if (lane == j) {
+      P.out.text_off[rj] = off;
+      P.out.text_len[rj] = status ? 0 : total;
+      P.out.status[rj] = status;
+      P.out.aux[2 * (u64)rj] = 0;
+      P.out.aux[2 * (u64)rj + 1] = 0;
+    }
   }
 }
 
@@ -274,16 +290,10 @@ __global__ void __launch_bounds__(128, UPY_MINB) upy_decompile_kernel(KParams P)
       S.out = &none;
       if (has) decompile_tree(&C, &S);
       __syncwarp();
-      const u32 has_m = __ballot_sync(0xffffffffu, has);
-      const u32 err_m = __ballot_sync(0xffffffffu, has && C.err);
-      if (err_m & (1u << lane)) emit_result(P, C, r, none);  // failed before emit: its message
-      for (u32 todo = has_m & ~err_m; todo; todo &= todo - 1) {
-        const int j = __ffs((int)todo) - 1;
-        const u32 rj = __shfl_sync(0xffffffffu, r, j);
-        const u32 oj = __shfl_sync(0xffffffffu, S.oi, j);
-        NV* tj = (NV*)__shfl_sync(0xffffffffu, (unsigned long long)S.tree, j);
-        coemit_object(P, C, opt, j, rj, oj, tj);
-      }
+      if (has && C.err) emit_result(P, C, r, none);  // failed before emit: its message
+#ifndef UPY_SKIP_COEMIT  // timing experiment only: trees built, nothing emitted
+      coemit_round(P, C, opt, has && !C.err, r, S.oi, S.tree);
+#endif
       __syncwarp();
     }
     return;

@@ -110,6 +110,30 @@ dshape() {  # device-side opcode-shape orders (1, 2, 4 chained 64-bit sorts) vs 
       | tee -a gpurun_out/dshape.txt
   done
 }
+coemit2() {  # coemit v2 (parallel headers, one scratch per round): parity forced on + C3 / C4 timing
+  UPY_SCHEDULE=cost+coemit timeout 1500 python -m pytest -m gpu -x -q tests/test_golden_gpu.py tests/test_cli.py \
+    2>&1 | tail -3 | tee gpurun_out/pytest_coemit2.txt
+  for sc in cost cost+coemit cost cost+coemit; do
+    timeout 900 python bench.py --workload c3 --schedule $sc --no-cpu --pyc 0 --no-extra --steps 3 --warmup 2 \
+      2>&1 | tail -1 > gpurun_out/coemit2_c3_$sc.json
+    python -c "import json; d=json.load(open('gpurun_out/coemit2_c3_$sc.json')); print('c3 $sc', round(d['value']), d['kernel_ms'], d['parity'])" \
+      | tee -a gpurun_out/coemit2.txt
+  done
+  for sc in input+thread input+coemit; do
+    timeout 900 python bench.py --workload c4 --schedule $sc --no-cpu --pyc 0 --no-extra --steps 1 --warmup 1 \
+      2>&1 | tail -1 > gpurun_out/coemit2_c4_$sc.json
+    python -c "import json; d=json.load(open('gpurun_out/coemit2_c4_$sc.json')); print('c4 $sc', round(d['value']), d['kernel_ms'], d['parity'])" \
+      | tee -a gpurun_out/coemit2.txt
+  done
+}
+coemit_split() {  # where coemit's time goes on C3: tree + warp sync only (variant nocoemit) vs full
+  for v in base nocoemit base nocoemit; do
+    if [ $v = base ]; then L=; else L=$V/$v.so; fi
+    UPY_LIB=$L timeout 900 python bench.py --workload c3 --schedule cost+coemit --no-cpu --pyc 0 --no-extra --steps 3 \
+      2>&1 | tail -1 > gpurun_out/cs_$v.json
+    python -c "import json; d=json.load(open('gpurun_out/cs_$v.json')); print('$v', d['kernel_ms'])" | tee -a gpurun_out/coemit_split.txt
+  done
+}
 c5() {  # one 16M-object corpus on this GPU (strong-scaling shape at N=1) + torchrun N=1 lines
   timeout 1800 python bench.py --workload c5 --no-cpu --pyc 0 --steps 3 --warmup 3 2>&1 | tail -1 > gpurun_out/bench_c5.json
   timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29611 \
