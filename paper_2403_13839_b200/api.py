@@ -403,18 +403,21 @@ DEFAULT_SCHEDULE = os.environ.get("UPY_SCHEDULE", "cost")
 
 
 def run_arena(arena: Arena, style=None, device=None, retries=3, function_tree=False, output=0,
-              schedule=None) -> BatchResult:
+              schedule=None, first_arena_bytes=0, first_text_cap=None) -> BatchResult:
     """Decompile every root of a packed arena on the GPU.
 
     Roots that hit a device capacity limit (per-thread arena, output buffer) are
     re-run on the device with 4x larger limits per attempt, sized from the
     retried roots' own trees and capped by the device's free memory.  output=1
-    writes each root's CFG export (to_dot, csrc/dot.h) instead of its source."""
+    writes each root's CFG export (to_dot, csrc/dot.h) instead of its source.
+    first_arena_bytes / first_text_cap override the first attempt's capacities
+    (tests use them to drive the retry path)."""
     torch = _torch()
     dev = torch.device(device or "cuda")
     with torch.cuda.device(dev):
         da = DeviceArena(arena, style, dev, function_tree=function_tree, output=output,
-                         schedule=schedule or DEFAULT_SCHEDULE)
+                         schedule=schedule or DEFAULT_SCHEDULE, arena_bytes=first_arena_bytes,
+                         text_cap=first_text_cap)
         da.upload()
         da.run()
         res = da.fetch()

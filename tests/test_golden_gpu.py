@@ -109,3 +109,26 @@ def test_gpu_sharded_decompile_many_matches_reference():
     recs = [r for r in golden_cases(["c2", "c4", "fuzz"]) if not r.get("style")]
     got = [outcome(v) for v in api.decompile_many(inputs(recs), devices=["cuda:0", "cuda:0", "cuda:0"])]
     assert not mismatches(recs, got)
+
+
+@pytest.mark.parametrize("kind", ["arena", "text"])
+def test_gpu_capacity_retries_reproduce_reference(kind):
+    """Roots that overflow their per-thread arena slot (or the output buffer) on
+    the first attempt are re-run with larger capacities; the final texts are the
+    reference's.  The first attempt is forced small so the C4 objects overflow."""
+    from paper_2403_13839_b200 import api, arena
+    from paper_2403_13839_b200.api import DeviceArena
+    from paper_2403_13839_b200.errors import ST_ARENA_OVERFLOW, ST_OUTPUT_OVERFLOW
+
+    recs = [r for r in golden_cases(["c4"]) if not r.get("style")]
+    ar = arena.pack(inputs(recs))
+    small = dict(arena_bytes=96 << 10) if kind == "arena" else dict(text_cap=1 << 16)
+    da = DeviceArena(ar, **small)
+    da.upload()
+    da.run()
+    first = da.fetch()
+    want = ST_ARENA_OVERFLOW if kind == "arena" else ST_OUTPUT_OVERFLOW
+    assert (first.status == want).sum() >= 3  # the forced limit really bites
+    res = api.run_arena(ar, first_arena_bytes=small.get("arena_bytes", 0), first_text_cap=small.get("text_cap"))
+    got = [outcome(v) for v in res.values()]
+    assert not mismatches(recs, got)
