@@ -354,6 +354,36 @@ def time_stackscan(da, steps, barrier):
     return e0.elapsed_time(e1) / steps
 
 
+def time_gather(da, res, barrier):
+    """All-gather of every rank's per-root results (offsets, lengths, statuses,
+    aux, text) over NCCL from the device buffers (gather.py), after the timed
+    region: wall time of the collective incl. the copy of the gathered arrays to
+    the host, and the bytes this rank contributed."""
+    import torch
+
+    from paper_2403_13839_b200.gather import device_views, gather_results
+
+    n = da.n
+    used = len(res.text)
+    off, aux, lens, status = device_views(da.meta, da.text, n)
+    barrier()
+    t0 = time.perf_counter()
+    g = gather_results(off, aux, lens, status, da.text[:used])
+    barrier()
+    ms = 1000 * (time.perf_counter() - t0)
+    # this rank's slice of the gathered result must equal what it fetched itself
+    import torch.distributed as dist
+    first, cnt = g.ranks[dist.get_rank()]
+    own = slice(first, first + cnt)
+    base = int(g.text_off[first] - res.text_off[0]) if cnt else 0
+    same = (cnt == n and np.array_equal(g.status[own], res.status) and np.array_equal(g.text_len[own], res.text_len)
+            and np.array_equal(g.text_off[own] - np.uint64(base), res.text_off)
+            and np.array_equal(g.text[base:base + used], res.text))
+    return {"ms": ms, "own_slice_identical": bool(same), "bytes_per_rank": int(used + 32 * n), "roots_gathered": int(len(g.status)),
+            "how": "padded all-gathers of sizes, per-root rows and text over the process group (NCCL), "
+                   "then host copy; not part of a step"}
+
+
 def time_e2e(da, arena, args, local, barrier):
     """H2D of the packed arena from pinned memory, both kernels, D2H of statuses
     and text, every step; two buffer sets and three streams overlap the copies of
@@ -444,7 +474,10 @@ def run_workload(wl, args, rank, world, local, barrier, steps, warmup, e2e=True)
     else:
         res = da.fetch()
     checked, bad = verifier(res)
-    out = {"arena": arena, "res": res, "da_host": int(da.host.numel()), "da_meta": int(da.meta.numel()),
+    gather = None
+    if world > 1:  # the optional final gather, timed on its own
+        gather = time_gather(da, res, barrier)
+    out = {"arena": arena, "res": res, "gather": gather, "da_host": int(da.host.numel()), "da_meta": int(da.meta.numel()),
            "slots": int(da.opts.slots), "total_ms": total_ms, "dec_sum": dec_sum, "st_sum": st_sum,
            "e2e_ms": e2e_ms, "used": used, "double": double, "n_instr": n_instr, "checked": checked,
            "bad": bad, "clocks": clk.summary(), "t_gen": t_gen, "info": info, "n_roots": arena.n_roots,
@@ -629,6 +662,7 @@ def main():
         "e2e_api": e2e_api,
         "e2e_pyc": pyc,
         "extra": extra,
+        "gather": r["gather"],
         "gpu_launches": 4 * args.steps,
         "clocks": r["clocks"],
     }

@@ -208,3 +208,78 @@ def test_shape_order_is_lexicographic_on_opcodes():
         want = np.lexsort([np.arange(len(roots))] + [ops[:, c] for c in range(8 * nw - 1, -1, -1)])
         got = api.shape_order(torch.from_numpy(a.blob), a.offsets, a.counts, nw).numpy()
         assert np.array_equal(got, want), nw
+
+
+TENSOR_GATHER_WORKER = r"""
+import json, os, sys
+sys.path.insert(0, sys.argv[1])
+sys.path.insert(0, os.path.join(sys.argv[1], "tests"))
+import numpy as np, torch
+import torch.distributed as dist
+from paper_2403_13839_b200 import api, arena, hostcheck
+from paper_2403_13839_b200.errors import make_exception
+from paper_2403_13839_b200.gather import gather_results
+from conftest import golden_cases
+from helpers import inputs, mismatches, outcome
+dist.init_process_group("gloo")
+r, w = dist.get_rank(), dist.get_world_size()
+recs = [x for x in golden_cases(["c2", "c4", "mutant"]) if not x.get("style")]
+codes = inputs(recs)
+lo, hi = api.shard_plan(codes, w)[r]
+res = hostcheck.run(arena.pack(codes[lo:hi]))
+# this rank's results as the tensors the device path gathers (text at rank-local offsets)
+texts = [s.encode("utf-8", "surrogatepass") for _, s, _ in res]
+offs = np.cumsum([0] + [len(t) + 16 for t in texts])[:-1]  # gaps, like the 16-B reservations
+text = torch.zeros(int(offs[-1] + len(texts[-1])) if texts else 0, dtype=torch.uint8)
+for o, t in zip(offs, texts):
+    text[int(o):int(o) + len(t)] = torch.tensor(list(t), dtype=torch.uint8)
+g = gather_results(torch.tensor(offs, dtype=torch.int64),
+                   torch.tensor([list(a) for _, _, a in res], dtype=torch.int64).reshape(-1, 2),
+                   torch.tensor([len(t) for t in texts], dtype=torch.int32),
+                   torch.tensor([st for st, _, _ in res], dtype=torch.int32), text)
+vals = []
+for i in range(len(g.status)):
+    st, s = g.item(i)
+    vals.append(s if st == 0 else make_exception(st, s, g.aux[i]))
+bad = mismatches(recs, [outcome(v) for v in vals])
+# bench.time_gather on the same results laid out as a DeviceArena meta buffer
+import types
+import bench
+n = len(res)
+meta = torch.zeros(64 + 32 * n, dtype=torch.uint8)
+meta[:8] = torch.tensor([text.numel()], dtype=torch.int64).view(torch.uint8)
+meta[64:64 + 8 * n] = torch.tensor(offs, dtype=torch.int64).view(torch.uint8)
+meta[64 + 8 * n:64 + 24 * n] = torch.tensor([list(a) for _, _, a in res], dtype=torch.int64).view(-1).view(torch.uint8)
+meta[64 + 24 * n:64 + 28 * n] = torch.tensor([len(t) for t in texts], dtype=torch.int32).view(torch.uint8)
+meta[64 + 28 * n:64 + 32 * n] = torch.tensor([st for st, _, _ in res], dtype=torch.int32).view(torch.uint8)
+br = api.BatchResult(np.array([st for st, _, _ in res], np.int32), np.array(offs, np.uint64),
+                     np.array([len(t) for t in texts], np.uint32),
+                     np.array([list(a) for _, _, a in res], np.int64).reshape(-1, 2), text.numpy())
+tg = bench.time_gather(types.SimpleNamespace(n=n, meta=meta, text=text), br, dist.barrier)
+with open(os.path.join(sys.argv[2], f"ok_{r}"), "w") as f:
+    json.dump({"n": len(vals), "want": len(recs), "bad": len(bad), "ranks": g.ranks,
+               "bench_own": tg["own_slice_identical"], "bench_roots": tg["roots_gathered"]}, f)
+dist.destroy_process_group()
+"""
+
+
+def test_gloo_tensor_gather(tmp_path):
+    """gather.gather_results (the final all-gather of the sharded path, on the
+    device tensors in production) over gloo with CPU tensors, world size 2:
+    every rank ends up with all results in input order, equal to the goldens."""
+    import json
+    import socket
+
+    script = tmp_path / "g.py"
+    script.write_text(TENSOR_GATHER_WORKER)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(script), ROOT, str(tmp_path)]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    res = [json.loads((tmp_path / f"ok_{r}").read_text()) for r in range(2)]
+    assert all(x["n"] == x["want"] and x["bad"] == 0 for x in res), res
+    assert res[0]["ranks"][1][1] > 0  # rank 1 contributed
+    assert all(x["bench_own"] and x["bench_roots"] == x["want"] for x in res), res
