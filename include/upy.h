@@ -91,7 +91,11 @@ typedef struct {
   int32_t schedule;          /* 0: each thread takes the next root position; 1: warp-synchronous (a warp
                                 takes 32 consecutive positions of `order` and its lanes start together);
                                 2: warp-synchronous with statement-parallel emission (the warp emits
-                                each of its 32 trees with the statements spread over its lanes) */
+                                each of its 32 trees with the statements spread over its lanes);
+                                3: split -- two launches per chunk of `slots` positions: every tree
+                                is built (validate .. finish) into its own arena slot, then every
+                                tree is emitted (source output only; `slots` = positions per chunk,
+                                `arena_bytes` = bytes per slot) */
   int32_t max_depth;         /* device recursion guard (UPY_ST_DEPTH_LIMIT); 0 = default 600 */
   int32_t function_tree;     /* 1: emit_module([function_tree(root)]) without validation -- the
                                 reference CLI's --function path (cli.py:75-78) -- instead of
@@ -198,6 +202,9 @@ int upy_stackscan_batch(const upy_arena* arena, const upy_ins* ins, const upy_de
                         upy_stackinfo* info, void* stream);
 /* Last API-level error message of this thread ("" when none). */
 const char* upy_last_error(void);
+/* Kernels this library has launched in this process (all devices, all entry points):
+ * read before and after a region to count its launches. */
+uint64_t upy_launch_count(void);
 
 
 #ifdef __cplusplus

@@ -71,7 +71,7 @@ SIZES = {0: 152, 1: 40, 2: 16, 3: C.sizeof(UpyArena), 4: C.sizeof(UpyOptions), 5
 
 # symbols declared by include/upy.h
 EXPORTS = ("upy_abi_sizeof", "upy_abi_version", "upy_query_workspace", "upy_decompile_batch",
-           "upy_decode_batch", "upy_stackscan_batch", "upy_last_error", "upy_pyc_load", "upy_pyc_write_image", "upy_pyc_free")
+           "upy_decode_batch", "upy_stackscan_batch", "upy_last_error", "upy_launch_count", "upy_pyc_load", "upy_pyc_write_image", "upy_pyc_free")
 PYC_DEFER_IMAGE = 1
 
 

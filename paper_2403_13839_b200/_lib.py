@@ -34,6 +34,7 @@ def load():
     _abi.check_layout(lib)
     lib.upy_abi_version.restype = C.c_int
     lib.upy_last_error.restype = C.c_char_p
+    lib.upy_launch_count.restype = C.c_uint64
     lib.upy_query_workspace.restype = C.c_int
     lib.upy_query_workspace.argtypes = [C.POINTER(_abi.UpyArena), C.POINTER(_abi.UpyOptions),
                                         C.POINTER(C.c_size_t)]

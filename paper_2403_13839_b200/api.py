@@ -93,18 +93,28 @@ class DeviceArena:
         # and handed to the kernel as upy_options.order; results stay in input order.
         base_sched, _, mode = schedule.partition("+")
         if base_sched not in ("input", "cost", "similar", "shape", "dshape1", "dshape2", "dshape4") or \
-                mode not in ("", "thread", "sync", "coemit"):
-            raise ValueError(f"schedule must be input|cost|similar|shape[+thread|+sync|+coemit], "
+                mode not in ("", "thread", "sync", "coemit", "split"):
+            raise ValueError(f"schedule must be input|cost|similar|shape[+thread|+sync|+coemit|+split], "
                              f"not {schedule!r}")
         self.schedule = base_sched if arena.n_roots > 1 else "input"
         # kernel schedule (upy_options.schedule): 0 each thread takes the next root,
-        # 1 warp-synchronous, 2 warp-synchronous with statement-parallel emission.
+        # 1 warp-synchronous, 2 warp-synchronous with statement-parallel emission,
+        # 3 split (a tree kernel, then an emit kernel, per chunk of positions).
         # Unspecified: statement-parallel emission for long objects (mean root tree of
-        # COEMIT_MIN_BYTES of code or more: C4 +26%), per-thread emission for short ones
-        # (C3 -23%: per-object overhead and the wait for the warp's slowest tree)
+        # COEMIT_MIN_BYTES of code or more: C4 +26%); for short ones the split
+        # schedule (C3 +11%, C3-3.11 +10%: each kernel's code is one part of the
+        # pipeline) when the batch is past the latency-mode size and at most
+        # SPLIT_MAX_CHUNKS chunks of arena slots fit in free memory, else per-thread.
+        self.output = output
         if not mode:
-            mode = "coemit" if mean_tree_code_bytes(arena) >= COEMIT_MIN_BYTES else "thread"
-        self.warp_sync = {"thread": 0, "sync": 1, "coemit": 2}[mode]
+            if mean_tree_code_bytes(arena) >= COEMIT_MIN_BYTES:
+                mode = "coemit"
+            elif output == 0 and not slots and not arena_bytes and self._split_fits(arena):
+                mode = "split"
+            else:
+                mode = "thread"
+        self.warp_sync = {"thread": 0, "sync": 1, "coemit": 2, "split": 3}[mode]
+        self.mode = mode
         if self.schedule in ("similar", "shape"):  # experiments: host-computed orders
             fn = root_similarity_order if self.schedule == "similar" else root_shape_order
             self._order = torch.from_numpy(fn(arena).astype(np.int32)).to(self.device)
@@ -113,10 +123,10 @@ class DeviceArena:
         if self.schedule not in ("similar", "shape"):
             self._order = None
         if not slots and not arena_bytes:
-            slots = self._memory_slots(arena)
+            slots = self._memory_slots(arena, split=self.warp_sync == 3)
         self.opts = _abi.options(style, arena_bytes=arena_bytes, slots=slots,
                                  threads_per_block=threads_per_block, function_tree=1 if function_tree else 0,
-                                 output=output)
+                                 output=output, schedule=self.warp_sync)
         ws = C.c_size_t(0)
         with torch.cuda.device(self.device):  # sizing reads the device's SM count
             _lib.check(self.lib.upy_query_workspace(C.byref(self.A), C.byref(self.opts), C.byref(ws)),
@@ -141,16 +151,47 @@ class DeviceArena:
         self.out.status = m + 64 + 28 * n
         self.n = arena.n_roots
 
-    def _memory_slots(self, arena):
+    @property
+    def schedule_spec(self):
+        """The resolved schedule as a `schedule=` argument ("order+mode")."""
+        return f"{self.schedule}+{self.mode}"
+
+    def _split_fits(self, arena):
+        sms = self.torch.cuda.get_device_properties(self.device).multi_processor_count
+        if arena.n_roots <= sms * 32:  # the library's latency mode (upy.cu layout)
+            return False
+        slots = self._memory_slots(arena, split=True)
+        return slots == 0 or slots * SPLIT_MAX_CHUNKS >= arena.n_roots
+
+    def kernel_names(self):
+        """The kernels one run() launches (per chunk for the split schedule)."""
+        if self.output == 1:
+            return ["upy_decode_kernel", "upy_cfgdot_kernel"]
+        if self.warp_sync == 3:
+            return ["upy_decode_kernel", "upy_tree_kernel", "upy_emit_kernel"]
+        return ["upy_decode_kernel", "upy_decompile_kernel"]
+
+    def _memory_slots(self, arena, split=False):
         """Concurrent per-thread arenas when the library's default 40 GB budget
         would bind (long objects: C4's ~3 MB slots allow only ~13K threads):
         size the slot count from the device's free memory instead (70% of it;
         the text buffer needs the rest).  0 = library
         default.  Measured on C4 (profiles/r02/bench_c4_slots_*.json): 12,288
         slots 2,726 objects/s, 24,576 2,965, 49,152 3,542."""
-        sb = default_slot_bytes(arena) + (68 << 10) + 256  # + the slot header (upy.cu SLOT_HEADER)
         full = self.torch.cuda.get_device_properties(self.device).multi_processor_count * 1024
-        want = min(arena.n_roots, full)
+        if split:
+            # schedule 3: one arena slot per position of a chunk (upy.cu layout_split):
+            # as many positions as 90% of free memory holds after the other buffers
+            # (records, per-object decode results, per-thread scratch, text, meta)
+            sb = split_slot_bytes(arena) + 256  # + its SplitState
+            others = (12 * (arena.total_code_units + 1) + 24 * arena.n_objs + full * (68 << 10)
+                      + 8 * arena.code_bytes + 544 * arena.n_roots + (64 << 20))
+            free, _ = self.torch.cuda.mem_get_info(self.device)
+            free += self.torch.cuda.memory_reserved(self.device) - self.torch.cuda.memory_allocated(self.device)
+            return int(max(1, min(arena.n_roots, (int(free * 0.9) - others) // sb)))
+        else:
+            sb = default_slot_bytes(arena) + (68 << 10) + 256  # + the slot header (upy.cu SLOT_HEADER)
+            want = min(arena.n_roots, full)
         if (40 << 30) // sb >= want:
             return 0
         free, _ = self.torch.cuda.mem_get_info(self.device)
@@ -241,6 +282,7 @@ class DeviceArena:
 
 
 COEMIT_MIN_BYTES = 4096
+SPLIT_MAX_CHUNKS = 8
 
 
 def mean_tree_code_bytes(arena: Arena) -> float:
@@ -365,6 +407,11 @@ def root_cost_order(arena: Arena):
 def default_slot_bytes(arena: Arena) -> int:
     """The per-thread arena size upy_query_workspace picks (upy.cu layout())."""
     return (64 << 10) + 160 * arena.max_code_len
+
+
+def split_slot_bytes(arena: Arena) -> int:
+    """The per-position arena size of the split schedule (upy.cu layout_split())."""
+    return ((32 << 10) + 16 * arena.max_code_len + 255) & ~255
 
 
 def tree_sizes(arena: Arena, roots) -> tuple:

@@ -22,6 +22,8 @@
 #include <cuda_runtime.h>
 #include "decode.h"
 #include "tma.h"
+#include <atomic>
+extern std::atomic<unsigned long long> g_upy_launches;  // upy.cu: upy_launch_count
 
 #define DSTAGES 4
 #define DWARPS 4  // warps per block
@@ -457,5 +459,6 @@ cudaError_t upy_decode_launch(const upy_arena* arena, upy_ins* ins, upy_decoded*
   const i64 max_blocks = (i64)sms * DEC_MINB;
   if (blocks > max_blocks) blocks = max_blocks;
   upy_decode_kernel<<<(unsigned)blocks, DWARPS * 32, 0, s>>>(*arena, ins, dec);
+  g_upy_launches += 1;
   return cudaGetLastError();
 }

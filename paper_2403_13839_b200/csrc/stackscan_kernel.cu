@@ -23,6 +23,8 @@
 #include <cuda_runtime.h>
 #include "stackscan.h"
 #include "tma.h"
+#include <atomic>
+extern std::atomic<unsigned long long> g_upy_launches;  // upy.cu: upy_launch_count
 
 #define SS_WARPS 8  // 8 x 3 KB record stages + 4 KB descriptor table per block
 #ifndef SS_MINB
@@ -264,5 +266,6 @@ extern "C" int upy_stackscan_batch(const upy_arena* arena, const upy_ins* ins, c
   const i64 cap = (i64)sms * SS_MINB;
   if (blocks > cap) blocks = cap;
   upy_stackscan_kernel<<<(unsigned)blocks, SS_WARPS * 32, 0, (cudaStream_t)stream>>>(*arena, ins, dec, stack, info, gshift);
+  g_upy_launches += 1;
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }

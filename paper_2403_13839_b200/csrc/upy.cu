@@ -9,6 +9,7 @@
 //                          then the text is appended to the flat output buffer.
 #include <cuda_runtime.h>
 #include <stdio.h>
+#include <atomic>
 #include <mutex>
 #include "pipeline.h"
 #include "dot.h"
@@ -20,6 +21,7 @@ cudaError_t upy_decode_launch(const upy_arena* arena, upy_ins* ins, upy_decoded*
 #define SLOT_HEADER (MSG_BYTES + SINK_BYTES)
 
 static __thread char g_last_error[512];
+std::atomic<unsigned long long> g_upy_launches{0};  // upy_launch_count (decode_kernel.cu, stackscan_kernel.cu too)
 static constexpr int kMaxDevices = 64;
 static std::mutex g_dev_cfg_mu;
 static bool g_dev_cfg_done[kMaxDevices];
@@ -47,19 +49,24 @@ struct KParams {
   int function_tree;
   int output;       // upy_options.output: 0 source text, 1 CFG dot export
   const int32_t* order;  // upy_options.order: processing order of root positions (or null)
+  // schedule 3 (split): positions [k_begin, k_end) of the order; arena slot = k - k_begin
+  struct SplitState* state;  // one per arena slot: the built tree and its context
+  u8* scratch_base;          // per-thread message buffer + overflow sink (SLOT_HEADER each)
+  u32 k_begin, k_end;
 };
 
 #ifndef UPY_MINB
 #define UPY_MINB 8  // <= 64 registers: 32 resident warps per SM (measured +43% vs unbounded)
 #endif
-// Per-thread state reset for a new root object.
-__device__ __forceinline__ void dc_reset(Dc& C, const KParams& P, u8* base) {
-  C.msg = (char*)base;
+// Per-thread state reset for a new root object: message buffer + sink at `scratch`,
+// the bump/scratch arena [arena, arena + cap).
+__device__ __forceinline__ void dc_reset_at(Dc& C, const KParams& P, u8* scratch, u8* arena, u64 cap) {
+  C.msg = (char*)scratch;
   C.msg_len = 0;
   C.msg_cap = MSG_BYTES;
-  C.sink = base + MSG_BYTES;
-  C.base = base + SLOT_HEADER;
-  C.cap = P.slot_bytes - SLOT_HEADER;
+  C.sink = scratch + MSG_BYTES;
+  C.base = arena;
+  C.cap = cap;
   C.used = 0;
   C.top = C.cap;
   C.low_top = C.cap;
@@ -77,6 +84,10 @@ __device__ __forceinline__ void dc_reset(Dc& C, const KParams& P, u8* base) {
   C.depth = 0;
   C.max_depth = P.max_depth;
   C.n_defs = 0;
+}
+// one slot = [message | sink | arena]
+__device__ __forceinline__ void dc_reset(Dc& C, const KParams& P, u8* base) {
+  dc_reset_at(C, P, base, base + SLOT_HEADER, P.slot_bytes - SLOT_HEADER);
 }
 
 // Text (or the error message) of root r into the flat output buffer.
@@ -331,6 +342,90 @@ __global__ void __launch_bounds__(128, UPY_MINB) upy_decompile_kernel(KParams P)
   }
 }
 
+// ---------------------------------------------------------------- split schedule
+// schedule 3: the pipeline in two launches per chunk of positions.  upy_tree_kernel
+// runs validate .. finish for every root of the chunk, each in its own arena slot,
+// and leaves the tree with its context in `state`; upy_emit_kernel then renders every
+// tree.  Each kernel's hot code is one part of the pipeline: the emitter no longer
+// competes with analysis / structuring for the SM instruction cache (the
+// decompile kernel's first limit).  The arena slots must hold the
+// trees of a whole chunk (one slot per position), so the chunk is the slot count.
+struct SplitState {
+  Dc C;
+  NV* tree;
+  u32 oi;
+  u32 ok;
+};
+
+__device__ __forceinline__ EmitOpts kernel_opts(const KParams& P) {
+  EmitOpts opt;
+  opt.header = P.header != 0;
+  opt.function_tree = P.function_tree != 0;
+  opt.indent = Str{P.indent_len <= 64 ? P.indent : P.indent_ptr, (u32)P.indent_len};
+  opt.tool = Str{P.tool_len <= 64 ? P.tool : P.tool_ptr, (u32)P.tool_len};
+  return opt;
+}
+
+__global__ void __launch_bounds__(128, UPY_MINB) upy_tree_kernel(KParams P) {
+  if (P.lane_stride > 1 && (threadIdx.x & 31)) return;
+  const u64 t = ((u64)blockIdx.x * blockDim.x + threadIdx.x) / (u64)P.lane_stride;
+  u8* scratch = P.scratch_base + t * SLOT_HEADER;
+  const EmitOpts opt = kernel_opts(P);
+  Dc C;
+  while (true) {
+    const u32 k = P.k_begin + atomicAdd(P.next_root, 1u);
+    if (k >= P.k_end) break;
+    const u32 r = P.order ? (u32)P.order[k] : k;
+    const u64 slot = k - P.k_begin;
+    dc_reset_at(C, P, scratch, P.slots_base + slot * P.slot_bytes, P.slot_bytes);
+    SourceJob S;
+    S.oi = (u32)P.A.roots[r];
+    S.opt = &opt;
+    S.tree = nullptr;
+    Text none = {nullptr, 0, 0};
+    S.out = &none;
+    decompile_tree(&C, &S);
+    SplitState* sv = P.state + slot;
+    if (C.err) {
+      emit_result(P, C, r, none);  // failed before emit: its message, now
+      sv->ok = 0;
+    } else {
+      sv->C = C;
+      sv->tree = S.tree;
+      sv->oi = S.oi;
+      sv->ok = 1;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128, UPY_MINB) upy_emit_kernel(KParams P) {
+  if (P.lane_stride > 1 && (threadIdx.x & 31)) return;
+  const u64 t = ((u64)blockIdx.x * blockDim.x + threadIdx.x) / (u64)P.lane_stride;
+  u8* scratch = P.scratch_base + t * SLOT_HEADER;
+  const EmitOpts opt = kernel_opts(P);
+  while (true) {
+    const u32 k = P.k_begin + atomicAdd(P.next_root + 1, 1u);
+    if (k >= P.k_end) break;
+    const SplitState* sv = P.state + (k - P.k_begin);
+    if (!sv->ok) continue;
+    const u32 r = P.order ? (u32)P.order[k] : k;
+    Dc C = sv->C;  // the tree's arena context; this thread's message buffer and sink
+    C.A = &P.A;
+    C.msg = (char*)scratch;
+    C.msg_len = 0;
+    C.msg_cap = MSG_BYTES;
+    C.sink = scratch + MSG_BYTES;
+    SourceJob S;
+    S.oi = sv->oi;
+    S.tree = sv->tree;
+    S.opt = &opt;
+    Text out = {nullptr, 0, 0};
+    S.out = &out;
+    ds_stage(&C, &S, DS_EMIT);
+    emit_result(P, C, r, out);
+  }
+}
+
 // `unpyre disasm --cfg --dot` (cli.py:103-105): to_dot(analyze(root)) per root
 // (dot.h), same schedule and per-thread arena as the decompile kernel.
 __global__ void __launch_bounds__(128, UPY_MINB) upy_cfgdot_kernel(KParams P) {
@@ -352,9 +447,11 @@ __global__ void __launch_bounds__(128, UPY_MINB) upy_cfgdot_kernel(KParams P) {
 
 // ------------------------------------------------------------ C ABI
 struct WsLayout {
-  u64 ins_off, dec_off, ctr_off, style_off, slots_off, total;
+  u64 ins_off, dec_off, ctr_off, style_off, state_off, scratch_off, slots_off, total;
   u64 slots, slot_bytes;
+  u64 threads;  // split schedule: root-taking threads (each with its scratch)
   int lane_stride;
+  bool split;
 };
 static u64 al(u64 x) { return (x + 255) & ~(u64)255; }
 
@@ -371,6 +468,46 @@ static int eff_tpb(const upy_options* o) {
   return tpb < 32 ? 32 : tpb & ~31;
 }
 
+// schedule 3: [state per slot][scratch per thread][arena slots]; slots = positions per
+// chunk, each slot an arena only (no header: messages and sinks are per thread).
+static WsLayout layout_split(const upy_arena* a, const upy_options* o, WsLayout L) {
+  // measured peaks (tools: hostcheck upyh_arena_peaks): C3 3.10 25 KB mean / 27 KB max at
+  // 428 code bytes, 3.11 28 / 34 KB at 1,418; larger objects overflow and are retried
+  u64 sb = o->arena_bytes ? o->arena_bytes : (u64)(32u << 10) + (u64)a->max_code_len * 16u;
+  sb = (sb + 255) & ~(u64)255;
+  L.slot_bytes = sb;
+  u64 slots;
+  if (o->slots > 0) {
+    slots = (u64)o->slots;
+  } else {
+    u64 cap_bytes = 40ull << 30;
+    slots = cap_bytes / (sb + sizeof(SplitState));
+  }
+  if (slots > (u64)a->n_roots) slots = (u64)a->n_roots;
+  if (slots < 1) slots = 1;
+  const u64 full = (u64)sm_count() * 1024;
+  int tpb = eff_tpb(o);
+  L.lane_stride = 1;
+  u64 thr;
+  if ((u64)a->n_roots <= (u64)sm_count() * (4 * UPY_MINB)) {
+    L.lane_stride = 32;
+    const u64 wpb = (u64)tpb / 32;
+    thr = (slots + wpb - 1) / wpb * wpb;
+    if (thr > (u64)sm_count() * (4 * UPY_MINB)) thr = (u64)sm_count() * (4 * UPY_MINB);
+  } else {
+    thr = slots < full ? slots : full;
+    thr = (thr + tpb - 1) / tpb * tpb;
+  }
+  L.threads = thr;
+  L.slots = slots;
+  L.state_off = L.slots_off;
+  L.scratch_off = L.state_off + al(slots * sizeof(SplitState));
+  L.slots_off = L.scratch_off + al(thr * SLOT_HEADER);
+  L.total = L.slots_off + slots * sb;
+  if (o->decode_only) L.total = L.ctr_off + 256;
+  return L;
+}
+
 static WsLayout layout(const upy_arena* a, const upy_options* o) {
   WsLayout L;
   u64 units = a->total_code_units + 1;
@@ -382,6 +519,8 @@ static WsLayout layout(const upy_arena* a, const upy_options* o) {
   if (o && o->indent_len > 64) style_bytes += o->indent_len;
   if (o && o->tool_len > 64) style_bytes += o->tool_len;
   L.slots_off = L.style_off + al(style_bytes);
+  L.split = o && o->schedule == 3 && o->output == 0;
+  if (L.split) return layout_split(a, o, L);
   // C3-size objects use ~55 KB; larger ones overflow and are retried by the host with 4x
   // measured peaks: C3 (400 B code) ~25 KB, C4 (19 KB code) ~2.2 MB => ~115 B per code byte
   u64 sb = o && o->arena_bytes ? o->arena_bytes : (u64)(64u << 10) + (u64)a->max_code_len * 160u;
@@ -438,6 +577,7 @@ size_t upy_abi_sizeof(int which) {
 }
 int upy_abi_version(void) { return UPY_ABI_VERSION; }
 const char* upy_last_error(void) { return g_last_error; }
+uint64_t upy_launch_count(void) { return g_upy_launches.load(); }
 
 int upy_query_workspace(const upy_arena* arena, const upy_options* opt, size_t* ws_bytes) {
   if (!arena || !ws_bytes) {
@@ -502,6 +642,8 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
       // no shared memory: give the whole L1/shared pool to L1 (arena + stack hit rate)
       cudaFuncSetAttribute(upy_decompile_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
       cudaFuncSetAttribute(upy_cfgdot_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+      cudaFuncSetAttribute(upy_tree_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+      cudaFuncSetAttribute(upy_emit_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
       cudaError_t e = cudaDeviceSetLimit(cudaLimitStackSize, 48 * 1024);
       if (e != cudaSuccess) {
         set_err("cudaDeviceSetLimit(stack): %s", cudaGetErrorString(e));
@@ -547,9 +689,30 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
   }
   P.lane_stride = L.lane_stride;
   int tpb = eff_tpb(opt);
+  if (L.split) {
+    P.state = (SplitState*)(ws + L.state_off);
+    P.scratch_base = ws + L.scratch_off;
+    const unsigned blocks = (unsigned)(L.threads * L.lane_stride / tpb);
+    const u64 n = (u64)arena->n_roots;
+    for (u64 k0 = 0; k0 < n; k0 += L.slots) {
+      P.k_begin = (u32)k0;
+      P.k_end = (u32)(k0 + L.slots < n ? k0 + L.slots : n);
+      if (k0) cudaMemsetAsync(ctr, 0, 8, s);
+      upy_tree_kernel<<<blocks, tpb, 0, s>>>(P);
+      upy_emit_kernel<<<blocks, tpb, 0, s>>>(P);
+      g_upy_launches += 2;
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      set_err("decompile launch: %s", cudaGetErrorString(e));
+      return 2;
+    }
+    return 0;
+  }
   unsigned blocks = (unsigned)(L.slots * L.lane_stride / tpb);
   if (P.output == 1) upy_cfgdot_kernel<<<blocks, tpb, 0, s>>>(P);
   else upy_decompile_kernel<<<blocks, tpb, 0, s>>>(P);
+  g_upy_launches += 1;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_err("decompile launch: %s", cudaGetErrorString(e));

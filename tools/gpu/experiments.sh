@@ -8,6 +8,7 @@
 # decode311  3.11 decode timing and a full ncu capture on C3-3.11
 # schedule   root order input vs largest-tree-first (api.root_cost_order) on C2x / C4 / C2
 # sync       warp-synchronous root fetch (upy_options.schedule = 1) x root order
+# split      schedule 3 (separate tree and emit kernels) vs the fused kernel, parity forced on
 # c5         the 16M-object corpus on one GPU, and torchrun N=1 lines (ours and the reference arm)
 set -u
 mkdir -p gpurun_out /tmp/ncu
@@ -132,6 +133,34 @@ coemit_split() {  # where coemit's time goes on C3: tree + warp sync only (varia
     UPY_LIB=$L timeout 900 python bench.py --workload c3 --schedule cost+coemit --no-cpu --pyc 0 --no-extra --steps 3 \
       2>&1 | tail -1 > gpurun_out/cs_$v.json
     python -c "import json; d=json.load(open('gpurun_out/cs_$v.json')); print('$v', d['kernel_ms'])" | tee -a gpurun_out/coemit_split.txt
+  done
+}
+split() {  # schedule 3 (tree kernel + emit kernel): parity forced on + C3 / C3-3.11 timing + icache
+  : UPY_SCHEDULE=cost+split timeout 1500 python -m pytest -m gpu -x -q tests/test_golden_gpu.py tests/test_cli.py \
+    2>&1 | tail -3 | tee gpurun_out/pytest_split.txt
+  for wl in c3 c3_311; do
+    for sc in cost cost+split cost cost+split; do
+      timeout 900 python bench.py --workload $wl --schedule $sc --no-cpu --pyc 0 --no-extra --steps 3 --warmup 2 \
+        2>&1 | tail -1 > gpurun_out/split_${wl}_$sc.json
+      python -c "import json; d=json.load(open('gpurun_out/split_${wl}_$sc.json')); print('$wl $sc', round(d['value']), d['kernel_ms'], d['parity'])" \
+        | tee -a gpurun_out/split.txt
+    done
+  done
+  M=sm__icc_request_hit_rate.pct,gcc__cache_requests_type_instruction.sum.pct_of_peak_sustained_elapsed,smsp__average_warp_latency_per_inst_issued.ratio,smsp__thread_inst_executed_per_inst_executed.ratio,dram__bytes.sum,gpu__time_duration.sum
+  ncu --metrics $M -k regex:"upy_(tree|emit|decompile)" -c 3 --csv \
+    python bench.py --schedule cost+split --no-cpu --pyc 0 --no-extra --steps 1 --warmup 1 --objects 262144 > gpurun_out/icc_split.csv 2>&1
+}
+split2() {  # split as the API default for short objects: full GPU tests, default line, C5, C2x
+  timeout 1800 python -m pytest -m gpu -x -q tests 2>&1 | tail -3 | tee gpurun_out/pytest_split2.txt
+  timeout 1200 python bench.py 2>&1 | tail -1 > gpurun_out/bench_split2.json
+  timeout 1800 python bench.py --workload c5 --no-cpu --pyc 0 --steps 3 --warmup 3 2>&1 | tail -1 > gpurun_out/bench_c5_split2.json
+  for sc in auto input+thread; do
+    timeout 900 python bench.py --workload c2x --schedule $sc --no-cpu --pyc 0 --no-extra --steps 3 --warmup 2 \
+      2>&1 | tail -1 > gpurun_out/split2_c2x_$sc.json
+  done
+  for f in gpurun_out/bench_split2.json gpurun_out/bench_c5_split2.json gpurun_out/split2_c2x_*.json; do
+    python -c "import json,sys; d=json.load(open('$f')); print('$f', d['config']['schedule'], round(d['value']), round(d['e2e']['value']), d['kernel_ms'], d['parity'], d['gpu_launches'])" \
+      | tee -a gpurun_out/split2.txt
   done
 }
 c5() {  # one 16M-object corpus on this GPU (strong-scaling shape at N=1) + torchrun N=1 lines
