@@ -58,6 +58,12 @@ struct KParams {
 #ifndef UPY_MINB
 #define UPY_MINB 8  // <= 64 registers: 32 resident warps per SM (measured +43% vs unbounded)
 #endif
+#ifndef UPY_TREE_MINB  // split schedule: resident 128-thread blocks per SM of each kernel
+#define UPY_TREE_MINB UPY_MINB
+#endif
+#ifndef UPY_EMIT_MINB
+#define UPY_EMIT_MINB UPY_MINB
+#endif
 // Per-thread state reset for a new root object: message buffer + sink at `scratch`,
 // the bump/scratch arena [arena, arena + cap).
 __device__ __forceinline__ void dc_reset_at(Dc& C, const KParams& P, u8* scratch, u8* arena, u64 cap) {
@@ -366,7 +372,7 @@ __device__ __forceinline__ EmitOpts kernel_opts(const KParams& P) {
   return opt;
 }
 
-__global__ void __launch_bounds__(128, UPY_MINB) upy_tree_kernel(KParams P) {
+__global__ void __launch_bounds__(128, UPY_TREE_MINB) upy_tree_kernel(KParams P) {
   if (P.lane_stride > 1 && (threadIdx.x & 31)) return;
   const u64 t = ((u64)blockIdx.x * blockDim.x + threadIdx.x) / (u64)P.lane_stride;
   u8* scratch = P.scratch_base + t * SLOT_HEADER;
@@ -398,7 +404,7 @@ __global__ void __launch_bounds__(128, UPY_MINB) upy_tree_kernel(KParams P) {
   }
 }
 
-__global__ void __launch_bounds__(128, UPY_MINB) upy_emit_kernel(KParams P) {
+__global__ void __launch_bounds__(128, UPY_EMIT_MINB) upy_emit_kernel(KParams P) {
   if (P.lane_stride > 1 && (threadIdx.x & 31)) return;
   const u64 t = ((u64)blockIdx.x * blockDim.x + threadIdx.x) / (u64)P.lane_stride;
   u8* scratch = P.scratch_base + t * SLOT_HEADER;
@@ -485,8 +491,9 @@ static WsLayout layout_split(const upy_arena* a, const upy_options* o, WsLayout 
   }
   if (slots > (u64)a->n_roots) slots = (u64)a->n_roots;
   if (slots < 1) slots = 1;
-  const u64 full = (u64)sm_count() * 1024;
+  const int mb = UPY_TREE_MINB > UPY_EMIT_MINB ? UPY_TREE_MINB : UPY_EMIT_MINB;
   int tpb = eff_tpb(o);
+  const u64 full = (u64)sm_count() * mb * tpb;  // resident threads of the larger grid
   L.lane_stride = 1;
   u64 thr;
   if ((u64)a->n_roots <= (u64)sm_count() * (4 * UPY_MINB)) {
@@ -692,14 +699,18 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
   if (L.split) {
     P.state = (SplitState*)(ws + L.state_off);
     P.scratch_base = ws + L.scratch_off;
-    const unsigned blocks = (unsigned)(L.threads * L.lane_stride / tpb);
+    // each kernel's grid: the scratch threads, at most its resident blocks per SM
+    const u64 blocks_all = L.threads * L.lane_stride / tpb;
+    const u64 sms = (u64)sm_count();
+    const unsigned tree_blocks = (unsigned)(blocks_all < sms * UPY_TREE_MINB ? blocks_all : sms * UPY_TREE_MINB);
+    const unsigned emit_blocks = (unsigned)(blocks_all < sms * UPY_EMIT_MINB ? blocks_all : sms * UPY_EMIT_MINB);
     const u64 n = (u64)arena->n_roots;
     for (u64 k0 = 0; k0 < n; k0 += L.slots) {
       P.k_begin = (u32)k0;
       P.k_end = (u32)(k0 + L.slots < n ? k0 + L.slots : n);
       if (k0) cudaMemsetAsync(ctr, 0, 8, s);
-      upy_tree_kernel<<<blocks, tpb, 0, s>>>(P);
-      upy_emit_kernel<<<blocks, tpb, 0, s>>>(P);
+      upy_tree_kernel<<<tree_blocks, tpb, 0, s>>>(P);
+      upy_emit_kernel<<<emit_blocks, tpb, 0, s>>>(P);
       g_upy_launches += 2;
     }
     cudaError_t e = cudaGetLastError();

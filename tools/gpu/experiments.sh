@@ -163,6 +163,31 @@ split2() {  # split as the API default for short objects: full GPU tests, defaul
       | tee -a gpurun_out/split2.txt
   done
 }
+split_minb() {  # split kernels' launch bounds: variants em6/em12 (emit) tr6/tr10 (tree) vs base, C3 + C2x
+  for round in 1 2; do
+    for v in base em6 em12 tr6 tr10; do
+      if [ $v = base ]; then L=; else L=$V/$v.so; fi
+      for wl in c3 c2x; do
+        UPY_LIB=$L timeout 900 python bench.py --workload $wl --schedule auto --no-cpu --pyc 0 --no-extra --steps 3 --warmup 2 \
+          2>&1 | tail -1 > gpurun_out/minb_${wl}_$v.json
+        python -c "import json; d=json.load(open('gpurun_out/minb_${wl}_$v.json')); print('$wl $v', d['config']['schedule'], round(d['value']), d['kernel_ms'], d['parity']['mismatches'])" \
+          | tee -a gpurun_out/split_minb.txt
+      done
+    done
+  done
+}
+split_big() {  # split on many chunks (C5 16M) and on long objects (C4, explicit 2.5 MB slots)
+  for sc in cost+split cost+thread; do
+    timeout 1800 python bench.py --workload c5 --schedule $sc --no-cpu --pyc 0 --no-extra --steps 2 --warmup 3 \
+      2>&1 | tail -1 > gpurun_out/big_c5_$sc.json
+    python -c "import json; d=json.load(open('gpurun_out/big_c5_$sc.json')); print('c5 $sc', d['config']['schedule'], d['config']['slots'], round(d['value']), d['kernel_ms'], d['parity']['mismatches'], d['gpu_launches'])" \
+      | tee -a gpurun_out/split_big.txt
+  done
+  timeout 1200 python bench.py --workload c4 --schedule input+split --slots 45000 --arena-bytes 2621440 --no-cpu --pyc 0 --no-extra --steps 1 --warmup 1 \
+    2>&1 | tail -1 > gpurun_out/big_c4_split.json
+  python -c "import json; d=json.load(open('gpurun_out/big_c4_split.json')); print('c4 input+split', d['config']['slots'], round(d['value']), d['kernel_ms'], d['parity']['mismatches'], d['gpu_launches'])" \
+    | tee -a gpurun_out/split_big.txt
+}
 c5() {  # one 16M-object corpus on this GPU (strong-scaling shape at N=1) + torchrun N=1 lines
   timeout 1800 python bench.py --workload c5 --no-cpu --pyc 0 --steps 3 --warmup 3 2>&1 | tail -1 > gpurun_out/bench_c5.json
   timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29611 \
