@@ -103,8 +103,9 @@ class DeviceArena:
         # Unspecified: statement-parallel emission for long objects (mean root tree of
         # COEMIT_MIN_BYTES of code or more: C4 +26%); for short ones the split
         # schedule (C3 +11%, C3-3.11 +10%: each kernel's code is one part of the
-        # pipeline) when the batch is past the latency-mode size and at most
-        # SPLIT_MAX_CHUNKS chunks of arena slots fit in free memory, else per-thread.
+        # pipeline) when the batch is past the latency-mode size and free memory holds
+        # arena slots for chunks of SPLIT_MIN_WAVES objects per resident thread (or all
+        # roots), else per-thread.
         self.output = output
         if not mode:
             if mean_tree_code_bytes(arena) >= COEMIT_MIN_BYTES:
@@ -161,7 +162,9 @@ class DeviceArena:
         if arena.n_roots <= sms * 32:  # the library's latency mode (upy.cu layout)
             return False
         slots = self._memory_slots(arena, split=True)
-        return slots == 0 or slots * SPLIT_MAX_CHUNKS >= arena.n_roots
+        # chunks of at least SPLIT_MIN_WAVES objects per resident thread (C5, 16M roots in
+        # 26 chunks of 669K: +24% over per-thread), or all roots in one
+        return slots >= min(arena.n_roots, SPLIT_MIN_WAVES * sms * 1024)
 
     def kernel_names(self):
         """The kernels one run() launches (per chunk for the split schedule)."""
@@ -181,14 +184,14 @@ class DeviceArena:
         full = self.torch.cuda.get_device_properties(self.device).multi_processor_count * 1024
         if split:
             # schedule 3: one arena slot per position of a chunk (upy.cu layout_split):
-            # as many positions as 90% of free memory holds after the other buffers
+            # as many positions as 80% of free memory holds after the other buffers
             # (records, per-object decode results, per-thread scratch, text, meta)
             sb = split_slot_bytes(arena) + 256  # + its SplitState
             others = (12 * (arena.total_code_units + 1) + 24 * arena.n_objs + full * (68 << 10)
                       + 8 * arena.code_bytes + 544 * arena.n_roots + (64 << 20))
             free, _ = self.torch.cuda.mem_get_info(self.device)
             free += self.torch.cuda.memory_reserved(self.device) - self.torch.cuda.memory_allocated(self.device)
-            return int(max(1, min(arena.n_roots, (int(free * 0.9) - others) // sb)))
+            return int(max(1, min(arena.n_roots, (int(free * 0.8) - others) // sb)))
         else:
             sb = default_slot_bytes(arena) + (68 << 10) + 256  # + the slot header (upy.cu SLOT_HEADER)
             want = min(arena.n_roots, full)
@@ -282,7 +285,7 @@ class DeviceArena:
 
 
 COEMIT_MIN_BYTES = 4096
-SPLIT_MAX_CHUNKS = 8
+SPLIT_MIN_WAVES = 4
 
 
 def mean_tree_code_bytes(arena: Arena) -> float:

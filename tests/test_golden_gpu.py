@@ -47,12 +47,15 @@ def test_gpu_c2_from_pyc_images_matches_reference():
 THROUGHPUT_ROOTS = 148 * 32 + 1  # more roots than resident warps: every thread takes roots (upy.cu layout())
 
 
+@pytest.mark.parametrize("schedule", ["cost", "input+thread"])
 @pytest.mark.parametrize("gset", ["c1", "c2", "c3", "c4", "snippets", "fuzz", "mutant", "mutant2", "mutant3"])
-def test_gpu_tiled_throughput_schedule_matches_reference(gset):
-    """The golden sets tiled past the small-batch threshold, so the kernel runs its
+def test_gpu_tiled_throughput_schedule_matches_reference(gset, schedule):
+    """The golden sets tiled past the small-batch threshold, so the kernels run a
     throughput schedule (32 root-taking threads per warp, divergent lanes) rather
-    than the one-thread-per-warp latency mode every untiled set above gets.  Every
-    tile's output is compared with the reference's text."""
+    than the one-thread-per-warp latency mode every untiled set above gets: the
+    API's default (split tree + emit kernels for short objects, statement-parallel
+    emission for long ones) and the fused per-thread kernel.  Every tile's output is
+    compared with the reference's text."""
     import math
 
     from paper_2403_13839_b200 import api, arena
@@ -65,7 +68,7 @@ def test_gpu_tiled_throughput_schedule_matches_reference(gset):
     for _, group in by_style.items():
         base = arena.pack(inputs(group))
         reps = math.ceil(THROUGHPUT_ROOTS / len(group))
-        res = api.run_arena(arena.tile(base, reps), style_of(group[0]))
+        res = api.run_arena(arena.tile(base, reps), style_of(group[0]), schedule=schedule)
         assert len(res.status) == reps * len(group) >= THROUGHPUT_ROOTS
         vals = res.values()
         for t in range(reps):
@@ -132,3 +135,40 @@ def test_gpu_capacity_retries_reproduce_reference(kind):
     res = api.run_arena(ar, first_arena_bytes=small.get("arena_bytes", 0), first_text_cap=small.get("text_cap"))
     got = [outcome(v) for v in res.values()]
     assert not mismatches(recs, got)
+
+
+@pytest.mark.parametrize("slots", [1000, 0])
+def test_gpu_split_schedule_chunks_match_reference(slots):
+    """The split schedule (upy_options.schedule = 3: a tree kernel, then an emit
+    kernel, per chunk of arena slots) with the roots spread over several chunks
+    (1,000 slots: every chunk boundary is crossed by the cost order's permutation)
+    and in one chunk (slots=0: the library default, 40 GB of slots); errors raised
+    before and during emission included."""
+    import math
+
+    from paper_2403_13839_b200 import arena
+    from paper_2403_13839_b200.api import DeviceArena
+
+    recs = [r for r in golden_cases(["c2", "c4", "fuzz", "mutant", "snippets"]) if not r.get("style")]
+    base = arena.pack(inputs(recs))
+    reps = math.ceil(THROUGHPUT_ROOTS / len(recs))
+    kw = dict(slots=slots, arena_bytes=4 << 20)  # C4 goldens need up to ~1 MB
+    da = DeviceArena(arena.tile(base, reps), schedule="cost+split", **kw)
+    assert da.warp_sync == 3
+    da.upload()
+    da.run()
+    vals = da.fetch().values()
+    bad = []
+    for t in range(reps):
+        bad += [(t,) + b for b in mismatches(recs, [outcome(v) for v in vals[t * len(recs):(t + 1) * len(recs)]])]
+    assert not bad, bad[:3]
+
+
+def test_gpu_split_schedule_small_batch_and_retry():
+    """Split schedule in the latency mode (one root-taking thread per warp) and its
+    arena-overflow retry: slots forced small, so C4 objects overflow and are re-run."""
+    from paper_2403_13839_b200 import api, arena
+
+    recs = [r for r in golden_cases(["c4", "c2"]) if not r.get("style")]
+    res = api.run_arena(arena.pack(inputs(recs)), schedule="input+split", first_arena_bytes=64 << 10)
+    assert not mismatches(recs, [outcome(v) for v in res.values()])
