@@ -551,7 +551,7 @@ def main():
     ap.add_argument("--schedule", default="auto",
                     choices=["auto", "input", "cost", "similar", "shape", "input+sync", "cost+sync", "similar+sync",
                              "shape+sync", "cost+coemit", "input+coemit", "shape+coemit", "dshape1", "dshape2",
-                             "dshape4", "cost+thread", "input+thread", "cost+split", "input+split"],
+                             "dshape4", "cost+thread", "input+thread", "cost+split", "input+split", "cost+split3", "input+split3"],
                     help="root order of the decompile kernel: cost = largest tree first (the API default); "
                          "auto = cost on distinct corpora, input on tiled pools (a size order would put a "
                          "pool object's copies side by side and the warps would run them in lockstep)")

@@ -95,7 +95,8 @@ typedef struct {
                                 3: split -- two launches per chunk of `slots` positions: every tree
                                 is built (validate .. finish) into its own arena slot, then every
                                 tree is emitted (source output only; `slots` = positions per chunk,
-                                `arena_bytes` = bytes per slot) */
+                                `arena_bytes` = bytes per slot); 4: as 3 with validate + analyze and
+                                structure + finish in two launches (three per chunk) */
   int32_t max_depth;         /* device recursion guard (UPY_ST_DEPTH_LIMIT); 0 = default 600 */
   int32_t function_tree;     /* 1: emit_module([function_tree(root)]) without validation -- the
                                 reference CLI's --function path (cli.py:75-78) -- instead of

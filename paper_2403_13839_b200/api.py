@@ -93,8 +93,8 @@ class DeviceArena:
         # and handed to the kernel as upy_options.order; results stay in input order.
         base_sched, _, mode = schedule.partition("+")
         if base_sched not in ("input", "cost", "similar", "shape", "dshape1", "dshape2", "dshape4") or \
-                mode not in ("", "thread", "sync", "coemit", "split"):
-            raise ValueError(f"schedule must be input|cost|similar|shape[+thread|+sync|+coemit|+split], "
+                mode not in ("", "thread", "sync", "coemit", "split", "split3"):
+            raise ValueError(f"schedule must be input|cost|similar|shape[+thread|+sync|+coemit|+split|+split3], "
                              f"not {schedule!r}")
         self.schedule = base_sched if arena.n_roots > 1 else "input"
         # kernel schedule (upy_options.schedule): 0 each thread takes the next root,
@@ -105,16 +105,18 @@ class DeviceArena:
         # schedule (C3 +11%, C3-3.11 +10%: each kernel's code is one part of the
         # pipeline) when the batch is past the latency-mode size and free memory holds
         # arena slots for chunks of SPLIT_MIN_WAVES objects per resident thread (or all
-        # roots), else per-thread.
+        # roots), three kernels (split3) when the roots carry nested code, else per-thread.
         self.output = output
         if not mode:
             if mean_tree_code_bytes(arena) >= COEMIT_MIN_BYTES:
                 mode = "coemit"
             elif output == 0 and not slots and not arena_bytes and self._split_fits(arena):
-                mode = "split"
+                # roots with nested code (modules, classes): validate + analyze in a
+                # kernel of their own as well (C2x +10%; flat C3 objects: +0.3 / -0.8%)
+                mode = "split3" if arena.n_objs > SPLIT3_MIN_OBJS_PER_ROOT * arena.n_roots else "split"
             else:
                 mode = "thread"
-        self.warp_sync = {"thread": 0, "sync": 1, "coemit": 2, "split": 3}[mode]
+        self.warp_sync = {"thread": 0, "sync": 1, "coemit": 2, "split": 3, "split3": 4}[mode]
         self.mode = mode
         if self.schedule in ("similar", "shape"):  # experiments: host-computed orders
             fn = root_similarity_order if self.schedule == "similar" else root_shape_order
@@ -124,7 +126,7 @@ class DeviceArena:
         if self.schedule not in ("similar", "shape"):
             self._order = None
         if not slots and not arena_bytes:
-            slots = self._memory_slots(arena, split=self.warp_sync == 3)
+            slots = self._memory_slots(arena, split=self.warp_sync in (3, 4))
         self.opts = _abi.options(style, arena_bytes=arena_bytes, slots=slots,
                                  threads_per_block=threads_per_block, function_tree=1 if function_tree else 0,
                                  output=output, schedule=self.warp_sync)
@@ -172,6 +174,8 @@ class DeviceArena:
             return ["upy_decode_kernel", "upy_cfgdot_kernel"]
         if self.warp_sync == 3:
             return ["upy_decode_kernel", "upy_tree_kernel", "upy_emit_kernel"]
+        if self.warp_sync == 4:
+            return ["upy_decode_kernel", "upy_analyze_kernel", "upy_structure_kernel", "upy_emit_kernel"]
         return ["upy_decode_kernel", "upy_decompile_kernel"]
 
     def _memory_slots(self, arena, split=False):
@@ -286,6 +290,7 @@ class DeviceArena:
 
 COEMIT_MIN_BYTES = 4096
 SPLIT_MIN_WAVES = 4
+SPLIT3_MIN_OBJS_PER_ROOT = 1.25
 
 
 def mean_tree_code_bytes(arena: Arena) -> float:

@@ -358,6 +358,7 @@ __global__ void __launch_bounds__(128, UPY_MINB) upy_decompile_kernel(KParams P)
 // trees of a whole chunk (one slot per position), so the chunk is the slot count.
 struct SplitState {
   Dc C;
+  BodyJob body;  // the root body's analysis (schedule 4 hands it from analyze to structure)
   NV* tree;
   u32 oi;
   u32 ok;
@@ -372,31 +373,52 @@ __device__ __forceinline__ EmitOpts kernel_opts(const KParams& P) {
   return opt;
 }
 
-__global__ void __launch_bounds__(128, UPY_TREE_MINB) upy_tree_kernel(KParams P) {
+// Stages FIRST..LAST of decompile_source for every position of the chunk.  FIRST == 0
+// starts the object in its slot; otherwise the state the previous kernel left is
+// restored (its arena context on this thread's message buffer and sink).  A failure
+// writes the object's message at once; LAST == DS_EMIT writes the text.  `ctr` is the
+// kernel's own position counter.
+template <int FIRST, int LAST>
+__device__ __forceinline__ void stage_range(const KParams& P, u32* ctr) {
   if (P.lane_stride > 1 && (threadIdx.x & 31)) return;
   const u64 t = ((u64)blockIdx.x * blockDim.x + threadIdx.x) / (u64)P.lane_stride;
   u8* scratch = P.scratch_base + t * SLOT_HEADER;
   const EmitOpts opt = kernel_opts(P);
   Dc C;
   while (true) {
-    const u32 k = P.k_begin + atomicAdd(P.next_root, 1u);
+    const u32 k = P.k_begin + atomicAdd(ctr, 1u);
     if (k >= P.k_end) break;
-    const u32 r = P.order ? (u32)P.order[k] : k;
     const u64 slot = k - P.k_begin;
-    dc_reset_at(C, P, scratch, P.slots_base + slot * P.slot_bytes, P.slot_bytes);
-    SourceJob S;
-    S.oi = (u32)P.A.roots[r];
-    S.opt = &opt;
-    S.tree = nullptr;
-    Text none = {nullptr, 0, 0};
-    S.out = &none;
-    decompile_tree(&C, &S);
     SplitState* sv = P.state + slot;
-    if (C.err) {
-      emit_result(P, C, r, none);  // failed before emit: its message, now
+    if (FIRST > 0 && !sv->ok) continue;
+    const u32 r = P.order ? (u32)P.order[k] : k;
+    SourceJob S;
+    S.opt = &opt;
+    Text out = {nullptr, 0, 0};
+    S.out = &out;
+    if (FIRST == 0) {
+      dc_reset_at(C, P, scratch, P.slots_base + slot * P.slot_bytes, P.slot_bytes);
+      S.oi = (u32)P.A.roots[r];
+      S.tree = nullptr;
+    } else {
+      C = sv->C;
+      C.A = &P.A;
+      C.msg = (char*)scratch;
+      C.msg_len = 0;
+      C.msg_cap = MSG_BYTES;
+      C.sink = scratch + MSG_BYTES;
+      S.oi = sv->oi;
+      S.body = sv->body;
+      S.tree = sv->tree;
+    }
+#pragma unroll 1
+    for (int st = FIRST; st <= LAST; st++) ds_stage(&C, &S, st);
+    if (LAST == DS_EMIT || C.err) {
+      emit_result(P, C, r, out);  // the text, or the message of the failing stage
       sv->ok = 0;
     } else {
       sv->C = C;
+      sv->body = S.body;
       sv->tree = S.tree;
       sv->oi = S.oi;
       sv->ok = 1;
@@ -404,32 +426,19 @@ __global__ void __launch_bounds__(128, UPY_TREE_MINB) upy_tree_kernel(KParams P)
   }
 }
 
+// schedule 3: build every tree, then emit every tree
+__global__ void __launch_bounds__(128, UPY_TREE_MINB) upy_tree_kernel(KParams P) {
+  stage_range<DS_VALIDATE, DS_FINISH>(P, P.next_root);
+}
 __global__ void __launch_bounds__(128, UPY_EMIT_MINB) upy_emit_kernel(KParams P) {
-  if (P.lane_stride > 1 && (threadIdx.x & 31)) return;
-  const u64 t = ((u64)blockIdx.x * blockDim.x + threadIdx.x) / (u64)P.lane_stride;
-  u8* scratch = P.scratch_base + t * SLOT_HEADER;
-  const EmitOpts opt = kernel_opts(P);
-  while (true) {
-    const u32 k = P.k_begin + atomicAdd(P.next_root + 1, 1u);
-    if (k >= P.k_end) break;
-    const SplitState* sv = P.state + (k - P.k_begin);
-    if (!sv->ok) continue;
-    const u32 r = P.order ? (u32)P.order[k] : k;
-    Dc C = sv->C;  // the tree's arena context; this thread's message buffer and sink
-    C.A = &P.A;
-    C.msg = (char*)scratch;
-    C.msg_len = 0;
-    C.msg_cap = MSG_BYTES;
-    C.sink = scratch + MSG_BYTES;
-    SourceJob S;
-    S.oi = sv->oi;
-    S.tree = sv->tree;
-    S.opt = &opt;
-    Text out = {nullptr, 0, 0};
-    S.out = &out;
-    ds_stage(&C, &S, DS_EMIT);
-    emit_result(P, C, r, out);
-  }
+  stage_range<DS_EMIT, DS_EMIT>(P, P.next_root + 1);
+}
+// schedule 4: validate + analyze, then structure + finish, then emit
+__global__ void __launch_bounds__(128, UPY_TREE_MINB) upy_analyze_kernel(KParams P) {
+  stage_range<DS_VALIDATE, DS_ANALYZE>(P, P.next_root + 2);
+}
+__global__ void __launch_bounds__(128, UPY_TREE_MINB) upy_structure_kernel(KParams P) {
+  stage_range<DS_STRUCTURE, DS_FINISH>(P, P.next_root);
 }
 
 // `unpyre disasm --cfg --dot` (cli.py:103-105): to_dot(analyze(root)) per root
@@ -526,7 +535,7 @@ static WsLayout layout(const upy_arena* a, const upy_options* o) {
   if (o && o->indent_len > 64) style_bytes += o->indent_len;
   if (o && o->tool_len > 64) style_bytes += o->tool_len;
   L.slots_off = L.style_off + al(style_bytes);
-  L.split = o && o->schedule == 3 && o->output == 0;
+  L.split = o && (o->schedule == 3 || o->schedule == 4) && o->output == 0;
   if (L.split) return layout_split(a, o, L);
   // C3-size objects use ~55 KB; larger ones overflow and are retried by the host with 4x
   // measured peaks: C3 (400 B code) ~25 KB, C4 (19 KB code) ~2.2 MB => ~115 B per code byte
@@ -651,6 +660,8 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
       cudaFuncSetAttribute(upy_cfgdot_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
       cudaFuncSetAttribute(upy_tree_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
       cudaFuncSetAttribute(upy_emit_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+      cudaFuncSetAttribute(upy_analyze_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+      cudaFuncSetAttribute(upy_structure_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
       cudaError_t e = cudaDeviceSetLimit(cudaLimitStackSize, 48 * 1024);
       if (e != cudaSuccess) {
         set_err("cudaDeviceSetLimit(stack): %s", cudaGetErrorString(e));
@@ -708,8 +719,14 @@ int upy_decompile_batch(const upy_arena* arena, const upy_options* opt, const up
     for (u64 k0 = 0; k0 < n; k0 += L.slots) {
       P.k_begin = (u32)k0;
       P.k_end = (u32)(k0 + L.slots < n ? k0 + L.slots : n);
-      if (k0) cudaMemsetAsync(ctr, 0, 8, s);
-      upy_tree_kernel<<<tree_blocks, tpb, 0, s>>>(P);
+      if (k0) cudaMemsetAsync(ctr, 0, 16, s);
+      if (P.schedule == 4) {
+        upy_analyze_kernel<<<tree_blocks, tpb, 0, s>>>(P);
+        upy_structure_kernel<<<tree_blocks, tpb, 0, s>>>(P);
+        g_upy_launches += 1;
+      } else {
+        upy_tree_kernel<<<tree_blocks, tpb, 0, s>>>(P);
+      }
       upy_emit_kernel<<<emit_blocks, tpb, 0, s>>>(P);
       g_upy_launches += 2;
     }

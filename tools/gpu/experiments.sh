@@ -188,6 +188,19 @@ split_big() {  # split on many chunks (C5 16M) and on long objects (C4, explicit
   python -c "import json; d=json.load(open('gpurun_out/big_c4_split.json')); print('c4 input+split', d['config']['slots'], round(d['value']), d['kernel_ms'], d['parity']['mismatches'], d['gpu_launches'])" \
     | tee -a gpurun_out/split_big.txt
 }
+split3() {  # schedule 4 (analyze | structure | emit kernels) vs 3 (tree | emit): parity + timing
+  UPY_SCHEDULE=cost+split3 timeout 1500 python -m pytest -m gpu -x -q tests/test_golden_gpu.py tests/test_cli.py \
+    2>&1 | tail -3 | tee gpurun_out/pytest_split3.txt
+  for wl in c3 c3_311 c2x; do
+    for sc in split split3 split split3; do
+      o=cost; [ $wl = c2x ] && o=input
+      timeout 900 python bench.py --workload $wl --schedule $o+$sc --no-cpu --pyc 0 --no-extra --steps 3 --warmup 2 \
+        2>&1 | tail -1 > gpurun_out/s3_${wl}_$sc.json
+      python -c "import json; d=json.load(open('gpurun_out/s3_${wl}_$sc.json')); print('$wl $sc', round(d['value']), d['kernel_ms'], d['parity']['mismatches'])" \
+        | tee -a gpurun_out/split3.txt
+    done
+  done
+}
 c5() {  # one 16M-object corpus on this GPU (strong-scaling shape at N=1) + torchrun N=1 lines
   timeout 1800 python bench.py --workload c5 --no-cpu --pyc 0 --steps 3 --warmup 3 2>&1 | tail -1 > gpurun_out/bench_c5.json
   timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29611 \
