@@ -1,6 +1,6 @@
 """Attribute ncu source-page samples of the decompile kernel to source lines.
 
-    python tools/ncu_source_lines.py <source.csv[.gz]> <libupy_cuda.so the profile ran>
+    python tools/ncu_source_lines.py <source.csv[.gz]> <libupy_cuda.so the profile ran> [kernel substring]
 
 `ncu --page source --csv` only lists SASS; this maps each SASS address to the
 file:line nvdisasm -g reports for the profiled library (built with -lineinfo),
@@ -39,8 +39,8 @@ def line_map(so_path, kernel="decompile"):
     return amap
 
 
-def main(src_csv, so_path):
-    amap = line_map(so_path)
+def main(src_csv, so_path, kernel="decompile"):
+    amap = line_map(so_path, kernel)
     opener = gzip.open if src_csv.endswith(".gz") else open
     rows = csv.reader(opener(src_csv, "rt"))
     next(rows)
@@ -83,4 +83,4 @@ def main(src_csv, so_path):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(*sys.argv[1:4])
