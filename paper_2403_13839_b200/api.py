@@ -166,7 +166,7 @@ class DeviceArena:
         slots = self._memory_slots(arena, split=True)
         # chunks of at least SPLIT_MIN_WAVES objects per resident thread (C5, 16M roots in
         # 26 chunks of 669K: +24% over per-thread), or all roots in one
-        return slots >= min(arena.n_roots, SPLIT_MIN_WAVES * sms * 1024)
+        return slots == 0 or slots >= min(arena.n_roots, SPLIT_MIN_WAVES * sms * 1024)
 
     def kernel_names(self):
         """The kernels one run() launches (per chunk for the split schedule)."""
@@ -191,6 +191,11 @@ class DeviceArena:
             # as many positions as 80% of free memory holds after the other buffers
             # (records, per-object decode results, per-thread scratch, text, meta)
             sb = split_slot_bytes(arena) + 256  # + its SplitState
+            if (40 << 30) // sb >= arena.n_roots:
+                # the library's default 40 GB budget holds every root: no device query
+                # (cudaMemGetInfo waits behind other host threads' pinned allocations,
+                # e.g. the .pyc loader's next sub-batch)
+                return 0
             others = (12 * (arena.total_code_units + 1) + 24 * arena.n_objs + full * (68 << 10)
                       + 8 * arena.code_bytes + 544 * arena.n_roots + (64 << 20))
             free, _ = self.torch.cuda.mem_get_info(self.device)

@@ -172,3 +172,20 @@ def test_gpu_split_schedule_small_batch_and_retry():
     recs = [r for r in golden_cases(["c4", "c2"]) if not r.get("style")]
     res = api.run_arena(arena.pack(inputs(recs)), schedule="input+split", first_arena_bytes=64 << 10)
     assert not mismatches(recs, [outcome(v) for v in res.values()])
+
+
+def test_gpu_default_schedule_policy():
+    """The API's kernel-mode choice: split for flat short objects past the
+    latency-mode size, three kernels when roots carry nested code, statement-
+    parallel emission for long objects, the fused kernel for small batches."""
+    from paper_2403_13839_b200 import arena
+    from paper_2403_13839_b200.api import DeviceArena
+    from paper_2403_13839_b200.bench_pools import pool_objects
+    from paper_2403_13839_b200.synth import c3fast
+
+    assert DeviceArena(c3fast.c3_arena(8192, 10, 0), schedule="cost").mode == "split"
+    assert DeviceArena(c3fast.c3_arena(64, 10, 0), schedule="cost").mode == "thread"
+    c2 = arena.pack(pool_objects("c2_310"))
+    assert DeviceArena(arena.tile(c2, 64), schedule="cost").mode == "split3"
+    c4 = arena.pack(pool_objects("c4_310", 0, 2))
+    assert DeviceArena(arena.tile(c4, 4), schedule="cost").mode == "coemit"
