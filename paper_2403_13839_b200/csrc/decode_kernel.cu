@@ -40,14 +40,12 @@ struct __align__(128) DecWarpSmem {
 };
 
 
-// chunks an object streams through the ring (0: handled from global memory).
-// 3.8-3.10: any size, decoded chunk by chunk.  3.11: objects of at most
-// DSTAGES chunks, which the consumer gathers whole (the inline-cache passes need
-// every unit) -- their code is prefetched by TMA while earlier objects decode.
-#define X11_RING_BYTES (DSTAGES * 512u)
+// chunks an object streams through the ring (0: handled elsewhere).  3.8-3.10:
+// any size, decoded chunk by chunk; 3.11 objects go to the lane kernel below or,
+// when it rejects them, to decode311_warp.
 __device__ __forceinline__ u32 n_chunks(u32 len, u32 minor) {
   if (len == 0 || (len & 1)) return 0;
-  if (minor == 11) return len <= X11_RING_BYTES ? (len + 511u) >> 9 : 0;
+  if (minor == 11) return 0;  // lane kernel (upy_decode311_lane_kernel) or decode311_warp
   if (minor < 8 || minor > 10) return 0;
   return ((len >> 1) + 255) >> 8;
 }
@@ -251,6 +249,197 @@ __device__ __noinline__ void decode311_warp(const u8* __restrict__ gcode, u32 le
   decode311_body(len, rec, res, tab, S);
 }
 
+
+// ---------------------------------------------------------------------------
+// 3.11, lane-serial (upy_decode311_lane_kernel, launched before the main kernel).
+// In 3.11 the instruction starts are a serial chain (each instruction skips its
+// inline-cache units), so the cheapest exact decoder is the reference's own walk
+// (disasm.py:71-122) run by ONE LANE PER OBJECT.  Lanes are independent: lane L
+// of warp w walks objects 32*g + L for the warp's groups g = w, w + nw, ...,
+// eight units (one 16-B load, prefetched two steps ahead) per step, and takes
+// its next object as soon as one ends, so the warp never waits for its longest
+// object.  Records are packed one word each into the lane's shared row
+// (unit index 11 b | code unit 16 b | cache count 4 b | has_arg 1 b -- objects
+// of at most 2048 units); rows that are nearly full, or whose object ended, are
+// expanded and copied out by the whole warp (one lane's row at a time, lane t
+// writing record t: coalesced).
+// The walk covers the common case only -- no EXTENDED_ARG, no jumps, every
+// opcode known, no cache run past the end.  A lane that meets anything else marks
+// its object L11_REDO and the main kernel, which runs next, decodes it from
+// scratch with decode311_warp (error reporting in decode_scalar's reference
+// order).  For the objects it keeps, the records are exactly decode_scalar's:
+// offset = 2u, arg = the arg byte when the opcode has an argument, n_prefixes 0,
+// cache_units, flags = has_arg (no jump targets: there are no jumps).
+#define L11_MAX 4096u   // bytes of code (2048 units: the packed row word's 11-bit unit index)
+#define L11_R 88u       // records per lane row (odd row stride: L11_R + 1)
+#define L11_WARPS 4     // warps per block
+#define L11_REDO 0x7ffffff0  // dec status: the main kernel decodes the object
+#ifndef L11_MINB
+#define L11_MINB 4      // blocks per SM (~46 KB of shared memory each)
+#endif
+// opcode entry of the walk: bits 0-3 cache count, bit 4 reject (unknown opcode,
+// EXTENDED_ARG, jump), bits 27-30 cache count and bit 31 has_arg (the packed
+// record's fields, in place)
+#define L11_REJECT (1u << 4)
+
+// the lane kernel takes a 3.11 object iff this holds
+__device__ __forceinline__ bool l11_eligible(u32 len, const upy_ins* rec) {
+  return len && !(len & 1) && len <= L11_MAX && (reinterpret_cast<uintptr_t>(rec) & 15) == 0;
+}
+
+__device__ __forceinline__ void sts_if(bool p, u32* a, u32 v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q st.shared.u32 [%1], %2;\n}\n" ::"r"((u32)p),
+               "r"(smem_addr(a)), "r"(v)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(L11_WARPS * 32, L11_MINB) upy_decode311_lane_kernel(upy_arena A,
+                                                                                      upy_ins* __restrict__ ins,
+                                                                                      upy_decoded* __restrict__ dec) {
+  __shared__ u32 tab[256];
+  __shared__ u32 rows_all[L11_WARPS][32][L11_R + 1];  // odd stride: lane L's word k in bank (L + k) % 32
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    const u32 e = UPY_OPTABLE_DEV[3][i];
+    const u32 k = UPY_ENT_KIND(e);
+    const u32 cache = UPY_ENT_CACHE(e);
+    const bool reject = !e || i == EXT_OP || k == K_JUMP_REL || k == K_JUMP_ABS || k == K_JUMP_BACK;
+    tab[i] = cache | (reject ? L11_REJECT : 0u) | (cache << 27) | ((u32)UPY_ENT_HASARG(e) << 31);
+  }
+  __syncthreads();
+  u32* const row = rows_all[wid][lane];
+  const i64 nw = (i64)gridDim.x * L11_WARPS;
+  const i64 n_groups = (A.n_objs + 31) >> 5;
+  i64 g = (i64)blockIdx.x * L11_WARPS + wid;  // the lane's next group
+  // Objects move through two prefetch stages so that no load is waited on when a
+  // lane switches objects: the header of the lane's next candidate (h*) and the
+  // next eligible object with its first 48 code bytes (n*), both loaded one whole
+  // object walk before they are needed.
+  i64 hc = -1;
+  u64 hoff = 0;
+  u32 hlen = 0, hmin = 0;
+  auto load_hdr = [&]() {
+    hc = -1;
+    while (g < n_groups) {
+      const i64 c = g * 32 + lane;
+      g += nw;
+      if (c < A.n_objs) {
+        const upy_obj* ob = &A.objs[c];
+        hc = c;
+        hoff = ob->code_off;
+        hlen = ob->code_len;
+        hmin = ob->minor;
+        break;
+      }
+    }
+  };
+  i64 no = -1;
+  u64 noff = 0;
+  u32 nunits = 0;
+  uint4 nx0 = make_uint4(0, 0, 0, 0), nx1 = nx0, nx2 = nx0;
+  auto advance_next = [&]() {
+    no = -1;
+    while (hc >= 0) {
+      const i64 c = hc;
+      const u64 off = hoff;
+      const u32 len = hlen, mn = hmin;
+      load_hdr();
+      if (mn == 11 && l11_eligible(len, ins + (off >> 1))) {
+        no = c;
+        noff = off;
+        nunits = len >> 1;
+        const uint4* cp = reinterpret_cast<const uint4*>(A.bytes + off);
+        nx0 = cp[0];
+        if (nunits > 8) nx1 = cp[1];
+        if (nunits > 16) nx2 = cp[2];
+        break;
+      }
+    }
+  };
+  load_hdr();
+  advance_next();
+
+  // the lane's current object
+  i64 o = -1;
+  const u8* code = nullptr;
+  upy_ins* rec = nullptr;
+  u32 units = 0, u = 0, skip = 0, cnt = 0, nout = 0;
+  bool ok = false;
+  uint4 x0 = make_uint4(0, 0, 0, 0), x1 = x0, x2 = x0;
+  for (;;) {
+    if (o < 0 && no >= 0) {
+      o = no;
+      code = A.bytes + noff;
+      rec = ins + (noff >> 1);
+      units = nunits;
+      x0 = nx0, x1 = nx1, x2 = nx2;
+      u = skip = cnt = nout = 0;
+      ok = true;
+      advance_next();
+    }
+    if (!__any_sync(0xffffffffu, o >= 0)) break;
+    bool done = false;
+    if (o >= 0) {
+      const uint4 x = x0;
+      x0 = x1;
+      x1 = x2;
+      if (u + 24 < units) x2 = *reinterpret_cast<const uint4*>(code + 2 * (u + 24));
+      const u32 wd[4] = {x.x, x.y, x.z, x.w};
+      const u32 left = units - u;  // >= 1
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        const u32 unit = (wd[q >> 1] >> (16 * (q & 1))) & 0xFFFFu;
+        const u32 e = tab[unit & 0xFFu];
+        const u32 cache = e & 15u;
+        const bool start = ok && (u32)q < left && skip == 0;
+        const bool bad = start && ((e & L11_REJECT) || u + q + 1 + cache > units);
+        const bool emit = start && !bad;
+        sts_if(emit, row + cnt, (u + q) | (unit << 11) | (e & 0xF8000000u));
+        cnt += emit;
+        skip = start ? cache : (skip ? skip - 1 : 0u);
+        ok = ok && !bad;
+      }
+      u += 8;
+      done = !ok || u >= units;
+    }
+    // rows that are nearly full or complete go out, expanded to upy_ins records
+    u32 who = __ballot_sync(0xffffffffu, ok && cnt && (done || cnt > L11_R - 8));
+    if (who) {
+      __syncwarp();
+      const u32 mine = who;
+      while (who) {
+        const int L = __ffs(who) - 1;
+        who &= who - 1;
+        const u32 c = __shfl_sync(0xffffffffu, cnt, L);
+        const u32 base = __shfl_sync(0xffffffffu, nout, L);
+        upy_ins* dst = reinterpret_cast<upy_ins*>(__shfl_sync(0xffffffffu, reinterpret_cast<u64>(rec), L)) + base;
+        const u32* src = rows_all[wid][L];
+        for (u32 t = lane; t < c; t += 32) {
+          const u32 p = src[t];
+          const u32 has = p >> 31;
+          u32* d = reinterpret_cast<u32*>(dst + t);
+          d[0] = 2u * (p & 0x7FFu);
+          d[1] = has ? (p >> 19) & 0xFFu : 0u;
+          d[2] = ((p >> 11) & 0xFFu) | (((p >> 27) & 15u) << 16) | (has << 24);
+        }
+      }
+      __syncwarp();
+      if ((mine >> lane) & 1u) {
+        nout += cnt;
+        cnt = 0;
+      }
+    }
+    if (done) {
+      upy_decoded* r = &dec[o];
+      r->status = ok ? UPY_ST_OK : L11_REDO;
+      r->n_instrs = ok ? (i32)nout : 0;
+      r->aux0 = r->aux1 = 0;
+      o = -1;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(DWARPS * 32, DEC_MINB) upy_decode_kernel(upy_arena A, upy_ins* __restrict__ ins,
                                                                     upy_decoded* __restrict__ dec) {
   __shared__ u32 tab[4][256];  // 3.8-3.11 opcode tables
@@ -347,6 +536,7 @@ __global__ void __launch_bounds__(DWARPS * 32, DEC_MINB) upy_decode_kernel(upy_a
       const u32 nch = n_chunks(len, minor);
       upy_ins* rec = ins + (off >> 1);
       if (nch == 0) {
+        if (minor == 11 && l11_eligible(len, rec) && dec[o].status != L11_REDO) continue;  // lane kernel's
         if (minor == 11 && len && !(len & 1) && len <= 2 * X11_UNITS) {
           decode311_warp(A.bytes + off, len, rec, &dec[o], tab[3], S);
           continue;
@@ -360,24 +550,6 @@ __global__ void __launch_bounds__(DWARPS * 32, DEC_MINB) upy_decode_kernel(upy_a
             dec[o].aux0 = dec[o].aux1 = 0;
           }
         }
-        continue;
-      }
-      if (minor == 11) {
-        // all of the object's chunks are (or will be) in the ring: wait for them,
-        // gather them into S.out, release the stages and refill the ring before
-        // decoding, so the next objects' code is in flight meanwhile
-        for (u32 c = 0; c < nch; c++) {
-          pump();
-          mbar_wait(&S.bar[(cons + c) % DSTAGES], ((cons + c) / DSTAGES) & 1);
-        }
-        if (lane == 0) bulk_wait_all();  // S.out may still be read by a bulk store
-        __syncwarp();
-        uint4* buf = reinterpret_cast<uint4*>(&S.out[0][0]);
-        for (u32 k = lane; k < nch * 32u; k += 32) buf[k] = S.in[(cons + (k >> 5)) % DSTAGES][k & 31];
-        __syncwarp();
-        cons += nch;
-        pump();
-        decode311_body(len, rec, &dec[o], tab[3], S);
         continue;
       }
       ChunkState st;
@@ -455,6 +627,16 @@ __global__ void __launch_bounds__(DWARPS * 32, DEC_MINB) upy_decode_kernel(upy_a
 // Grid: at most 6 resident blocks of 4 warps per SM, one warp per 32-object group.
 cudaError_t upy_decode_launch(const upy_arena* arena, upy_ins* ins, upy_decoded* dec, cudaStream_t s, int sms) {
   const i64 groups = (arena->n_objs + 31) / 32;
+  // 3.11 objects first (a batch without any costs one pass over the object headers);
+  // the main kernel then decodes everything else, including the objects the lane
+  // walk handed back (L11_REDO)
+  i64 lblocks = (groups + L11_WARPS - 1) / L11_WARPS;
+  const i64 lmax = (i64)sms * L11_MINB;
+  if (lblocks > lmax) lblocks = lmax;
+  upy_decode311_lane_kernel<<<(unsigned)lblocks, L11_WARPS * 32, 0, s>>>(*arena, ins, dec);
+  g_upy_launches += 1;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
   i64 blocks = (groups + DWARPS - 1) / DWARPS;
   const i64 max_blocks = (i64)sms * DEC_MINB;
   if (blocks > max_blocks) blocks = max_blocks;
