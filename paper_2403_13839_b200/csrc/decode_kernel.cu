@@ -271,11 +271,15 @@ __device__ __noinline__ void decode311_warp(const u8* __restrict__ gcode, u32 le
 // offset = 2u, arg = the arg byte when the opcode has an argument, n_prefixes 0,
 // cache_units, flags = has_arg (no jump targets: there are no jumps).
 #define L11_MAX 4096u   // bytes of code (2048 units: the packed row word's 11-bit unit index)
-#define L11_R 88u       // records per lane row (odd row stride: L11_R + 1)
-#define L11_WARPS 4     // warps per block
+#define L11_R 38u       // records per lane row (odd row stride: L11_R + 1)
+#define L11_RING 128u   // code units per lane ring (a power of two)
+#define L11_CHUNK 16u   // units per ring refill (one cp.async group)
+#define L11_AHEAD 112u  // units kept buffered ahead of the walk: L11_RING - L11_CHUNK
+#define L11_PRE 8u      // 16-B pieces of the next object held in registers (its first 64 units)
+#define L11_WARPS 2     // warps per block
 #define L11_REDO 0x7ffffff0  // dec status: the main kernel decodes the object
 #ifndef L11_MINB
-#define L11_MINB 4      // blocks per SM (~46 KB of shared memory each)
+#define L11_MINB 7      // blocks per SM (~28 KB of shared memory each)
 #endif
 // opcode entry of the walk: bits 0-3 cache count, bit 4 reject (unknown opcode,
 // EXTENDED_ARG, jump), bits 27-30 cache count and bit 31 has_arg (the packed
@@ -286,6 +290,16 @@ __device__ __noinline__ void decode311_warp(const u8* __restrict__ gcode, u32 le
 __device__ __forceinline__ bool l11_eligible(u32 len, const upy_ins* rec) {
   return len && !(len & 1) && len <= L11_MAX && (reinterpret_cast<uintptr_t>(rec) & 15) == 0;
 }
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, u32 src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait3() { asm volatile("cp.async.wait_group 3;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait2() { asm volatile("cp.async.wait_group 2;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void sts_if(bool p, u32* a, u32 v) {
   asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q st.shared.u32 [%1], %2;\n}\n" ::"r"((u32)p),
@@ -298,6 +312,7 @@ __global__ void __launch_bounds__(L11_WARPS * 32, L11_MINB) upy_decode311_lane_k
                                                                                       upy_decoded* __restrict__ dec) {
   __shared__ u32 tab[256];
   __shared__ u32 rows_all[L11_WARPS][32][L11_R + 1];  // odd stride: lane L's word k in bank (L + k) % 32
+  __shared__ __align__(16) u8 ring_all[L11_WARPS][32][L11_RING * 2 + 16];  // per-lane code ring (+16 B pad)
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
@@ -309,12 +324,13 @@ __global__ void __launch_bounds__(L11_WARPS * 32, L11_MINB) upy_decode311_lane_k
   }
   __syncthreads();
   u32* const row = rows_all[wid][lane];
+  u8* const ring = ring_all[wid][lane];
   const i64 nw = (i64)gridDim.x * L11_WARPS;
   const i64 n_groups = (A.n_objs + 31) >> 5;
   i64 g = (i64)blockIdx.x * L11_WARPS + wid;  // the lane's next group
   // Objects move through two prefetch stages so that no load is waited on when a
   // lane switches objects: the header of the lane's next candidate (h*) and the
-  // next eligible object with its first 48 code bytes (n*), both loaded one whole
+  // next eligible object with its first 128 code bytes (n*), both loaded one whole
   // object walk before they are needed.
   i64 hc = -1;
   u64 hoff = 0;
@@ -337,7 +353,7 @@ __global__ void __launch_bounds__(L11_WARPS * 32, L11_MINB) upy_decode311_lane_k
   i64 no = -1;
   u64 noff = 0;
   u32 nunits = 0;
-  uint4 nx0 = make_uint4(0, 0, 0, 0), nx1 = nx0, nx2 = nx0;
+  uint4 nx[L11_PRE];  // the next object's first L11_PRE * 8 code units
   auto advance_next = [&]() {
     no = -1;
     while (hc >= 0) {
@@ -350,9 +366,9 @@ __global__ void __launch_bounds__(L11_WARPS * 32, L11_MINB) upy_decode311_lane_k
         noff = off;
         nunits = len >> 1;
         const uint4* cp = reinterpret_cast<const uint4*>(A.bytes + off);
-        nx0 = cp[0];
-        if (nunits > 8) nx1 = cp[1];
-        if (nunits > 16) nx2 = cp[2];
+#pragma unroll
+        for (int k = 0; k < (int)L11_PRE; k++)
+          if (8u * k < nunits) nx[k] = cp[k];
         break;
       }
     }
@@ -360,51 +376,71 @@ __global__ void __launch_bounds__(L11_WARPS * 32, L11_MINB) upy_decode311_lane_k
   load_hdr();
   advance_next();
 
-  // the lane's current object
+  // the lane's current object; its code units [F - L11_RING, F) sit in the ring at
+  // index u % L11_RING, the newest chunks possibly still in flight (cp.async)
   i64 o = -1;
   const u8* code = nullptr;
   upy_ins* rec = nullptr;
-  u32 units = 0, u = 0, skip = 0, cnt = 0, nout = 0;
+  u32 units = 0, u = 0, cnt = 0, nout = 0, F = 0, lim = 0;
   bool ok = false;
-  uint4 x0 = make_uint4(0, 0, 0, 0), x1 = x0, x2 = x0;
+  // refill: the next chunk of code units behind F (zero-filled past the object's
+  // readable 16-B-rounded end)
+  auto refill = [&]() {
+#pragma unroll
+    for (int k = 0; k < L11_CHUNK / 8; k++) {
+      const u32 p = 2u * (F + 8u * k);
+      cp_async16(ring + 2u * ((F + 8u * k) & (L11_RING - 1)), code + (p < lim ? p : 0u), p < lim ? 16u : 0u);
+    }
+    cp_async_commit();
+    F += L11_CHUNK;
+  };
   for (;;) {
     if (o < 0 && no >= 0) {
+      cp_async_wait0();  // the previous object's ring writes
       o = no;
       code = A.bytes + noff;
       rec = ins + (noff >> 1);
       units = nunits;
-      x0 = nx0, x1 = nx1, x2 = nx2;
-      u = skip = cnt = nout = 0;
+      lim = (2u * units + 15u) & ~15u;
+      uint4* rq = reinterpret_cast<uint4*>(ring);
+#pragma unroll
+      for (int k = 0; k < (int)L11_PRE; k++) rq[k] = nx[k];
+      F = 8 * L11_PRE;
+      u = cnt = nout = 0;
       ok = true;
       advance_next();
     }
     if (!__any_sync(0xffffffffu, o >= 0)) break;
-    bool done = false;
-    if (o >= 0) {
-      const uint4 x = x0;
-      x0 = x1;
-      x1 = x2;
-      if (u + 24 < units) x2 = *reinterpret_cast<const uint4*>(code + 2 * (u + 24));
-      const u32 wd[4] = {x.x, x.y, x.z, x.w};
-      const u32 left = units - u;  // >= 1
-#pragma unroll
-      for (int q = 0; q < 8; q++) {
-        const u32 unit = (wd[q >> 1] >> (16 * (q & 1))) & 0xFFFFu;
-        const u32 e = tab[unit & 0xFFu];
-        const u32 cache = e & 15u;
-        const bool start = ok && (u32)q < left && skip == 0;
-        const bool bad = start && ((e & L11_REJECT) || u + q + 1 + cache > units);
-        const bool emit = start && !bad;
-        sts_if(emit, row + cnt, (u + q) | (unit << 11) | (e & 0xF8000000u));
-        cnt += emit;
-        skip = start ? cache : (skip ? skip - 1 : 0u);
-        ok = ok && !bad;
-      }
-      u += 8;
-      done = !ok || u >= units;
+    // Ring refill, once per round: keep L11_AHEAD units behind the walk issued, then
+    // wait for the chunks that start below u + 64 -- the four instructions below reach
+    // at most 64 units (the opcode plus at most 15 caches each); up to three newer
+    // chunks stay in flight.
+    if (o >= 0 && ok && u < units) {
+      while (F < u + L11_AHEAD && F < units) refill();
+      const u32 pend = F > u + 64 ? min((F - u - 64) / L11_CHUNK, 3u) : 0u;
+      if (pend == 3) cp_async_wait3();
+      else if (pend == 2) cp_async_wait2();
+      else if (pend == 1) cp_async_wait1();
+      else cp_async_wait0();
     }
+    // four instructions per lane: read the unit at u, look its opcode up, append the
+    // packed record, jump over the instruction's cache units
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const bool live = o >= 0 && ok && u < units;
+      const u32 unit = *reinterpret_cast<const unsigned short*>(ring + 2u * (u & (L11_RING - 1)));
+      const u32 e = tab[unit & 0xFFu];
+      const u32 cache = e & 15u;
+      const bool bad = (e & L11_REJECT) || u + 1 + cache > units;
+      const bool emit = live && !bad;
+      sts_if(emit, row + cnt, u | (unit << 11) | (e & 0xF8000000u));
+      cnt += emit;
+      u += live ? 1 + cache : 0u;
+      ok = ok && !(live && bad);
+    }
+    const bool done = o >= 0 && (!ok || u >= units);
     // rows that are nearly full or complete go out, expanded to upy_ins records
-    u32 who = __ballot_sync(0xffffffffu, ok && cnt && (done || cnt > L11_R - 8));
+    u32 who = __ballot_sync(0xffffffffu, ok && cnt && (done || cnt > L11_R - 4));
     if (who) {
       __syncwarp();
       const u32 mine = who;
@@ -527,16 +563,21 @@ __global__ void __launch_bounds__(DWARPS * 32, DEC_MINB) upy_decode_kernel(upy_a
 
   u32 ob = 0;  // output staging buffer toggle
   for (; g < n_groups; g += nw) {
+    // objects of this group the lane kernel already decoded (one coalesced status read)
+    const i64 ol = g * 32 + lane;
+    const bool l11_done = ol < A.n_objs && c_min == 11 && l11_eligible(c_len, ins + (c_off >> 1)) &&
+                          dec[ol].status != L11_REDO;
+    const u32 todo = ~__ballot_sync(0xffffffffu, l11_done);
     for (u32 j = 0; j < 32; j++) {
       const i64 o = g * 32 + j;
       if (o >= A.n_objs) break;
+      if (!((todo >> j) & 1u)) continue;
       const u64 off = __shfl_sync(0xffffffffu, c_off, j);
       const u32 len = __shfl_sync(0xffffffffu, c_len, j);
       const u32 minor = __shfl_sync(0xffffffffu, c_min, j);
       const u32 nch = n_chunks(len, minor);
       upy_ins* rec = ins + (off >> 1);
       if (nch == 0) {
-        if (minor == 11 && l11_eligible(len, rec) && dec[o].status != L11_REDO) continue;  // lane kernel's
         if (minor == 11 && len && !(len & 1) && len <= 2 * X11_UNITS) {
           decode311_warp(A.bytes + off, len, rec, &dec[o], tab[3], S);
           continue;
