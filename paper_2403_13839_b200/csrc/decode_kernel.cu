@@ -279,7 +279,7 @@ __device__ __noinline__ void decode311_warp(const u8* __restrict__ gcode, u32 le
 #define L11_WARPS 2     // warps per block
 #define L11_REDO 0x7ffffff0  // dec status: the main kernel decodes the object
 #ifndef L11_MINB
-#define L11_MINB 7      // blocks per SM (~28 KB of shared memory each)
+#define L11_MINB 7      // blocks per SM (~28 KB of shared memory each; 64-unit ring: 2.06 ms, 256: 1.97 ms, 128: 1.55 ms)
 #endif
 // opcode entry of the walk: bits 0-3 cache count, bit 4 reject (unknown opcode,
 // EXTENDED_ARG, jump), bits 27-30 cache count and bit 31 has_arg (the packed
@@ -412,22 +412,25 @@ __global__ void __launch_bounds__(L11_WARPS * 32, L11_MINB) upy_decode311_lane_k
     }
     if (!__any_sync(0xffffffffu, o >= 0)) break;
     // Ring refill, once per round: keep L11_AHEAD units behind the walk issued, then
-    // wait for the chunks that start below u + 64 -- the four instructions below reach
-    // at most 64 units (the opcode plus at most 15 caches each); up to three newer
-    // chunks stay in flight.
+    // wait only for the chunk holding unit u (the walk reads the opcode unit of each
+    // instruction, never its cache units); newer chunks stay in flight (<= 3) and
+    // an instruction whose opcode unit is not in shared memory yet (u >= V) waits
+    // for the next round.
+    u32 V = 0;
     if (o >= 0 && ok && u < units) {
       while (F < u + L11_AHEAD && F < units) refill();
-      const u32 pend = F > u + 64 ? min((F - u - 64) / L11_CHUNK, 3u) : 0u;
+      const u32 pend = min((F - u - 1) / L11_CHUNK, 3u);
       if (pend == 3) cp_async_wait3();
       else if (pend == 2) cp_async_wait2();
       else if (pend == 1) cp_async_wait1();
       else cp_async_wait0();
+      V = F - L11_CHUNK * pend;
     }
     // four instructions per lane: read the unit at u, look its opcode up, append the
     // packed record, jump over the instruction's cache units
 #pragma unroll
     for (int k = 0; k < 4; k++) {
-      const bool live = o >= 0 && ok && u < units;
+      const bool live = o >= 0 && ok && u < units && u < V;
       const u32 unit = *reinterpret_cast<const unsigned short*>(ring + 2u * (u & (L11_RING - 1)));
       const u32 e = tab[unit & 0xFFu];
       const u32 cache = e & 15u;
