@@ -392,26 +392,50 @@ __device__ __forceinline__ int decode_chunk(const u8* __restrict__ code, u32 len
 // be called by all 32 lanes after the records are visible to the warp.
 __device__ __forceinline__ void mark_jump_targets(upy_ins* rec, u32 n, u32 unit_lo, u32 nbits, int minor,
                                                   const u32* __restrict__ tab, u32* bm) {
+  // Both passes load MJ_U records per lane before using any of them, so a warp has
+  // 32 * MJ_U record loads in flight instead of 32 (the records of a long object are
+  // in global memory: one load round trip per 32 records made C4 decode latency-bound).
+  constexpr int MJ_U = 8;
   const int lane = threadIdx.x & 31;
   const u32 nw = (nbits + 31) >> 5;
   for (u32 k = lane; k < nw; k += 32) bm[k] = 0;
   __syncwarp();
-  for (u32 k = lane; k < n; k += 32) {
-    const u32* w = reinterpret_cast<const u32*>(rec + k);
-    const u32 w2 = w[2];
-    const u32 e = tab[w2 & 0xFFu];
-    if (!((e >> ENT_JUMP_BIT) & 1u) || ((w2 >> 24) & 2u)) continue;
-    bool ok;
-    const i64 t = jump_target_u64(minor, UPY_ENT_KIND(e), (u64)w[0] + 2ull * ((w2 >> 8) & 0xFFu), w[1], &ok);
-    if (t < 0 || (t & 1)) continue;
-    const u64 u = (u64)(t >> 1) - unit_lo;
-    if ((t >> 1) >= (i64)unit_lo && u < nbits) atomicOr(&bm[u >> 5], 1u << (u & 31));
+  for (u32 base = 0; base < n; base += 32 * MJ_U) {
+    u32 w0[MJ_U], w1[MJ_U], w2[MJ_U];
+#pragma unroll
+    for (int j = 0; j < MJ_U; j++) {
+      const u32 k = base + 32 * j + lane;
+      const u32* w = reinterpret_cast<const u32*>(rec + (k < n ? k : 0));
+      w0[j] = w[0];
+      w1[j] = w[1];
+      w2[j] = k < n ? w[2] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < MJ_U; j++) {
+      const u32 e = tab[w2[j] & 0xFFu];
+      if (!w2[j] || !((e >> ENT_JUMP_BIT) & 1u) || ((w2[j] >> 24) & 2u)) continue;
+      bool ok;
+      const i64 t = jump_target_u64(minor, UPY_ENT_KIND(e), (u64)w0[j] + 2ull * ((w2[j] >> 8) & 0xFFu), w1[j], &ok);
+      if (t < 0 || (t & 1)) continue;
+      const u64 u = (u64)(t >> 1) - unit_lo;
+      if ((t >> 1) >= (i64)unit_lo && u < nbits) atomicOr(&bm[u >> 5], 1u << (u & 31));
+    }
   }
   __syncwarp();
-  for (u32 k = lane; k < n; k += 32) {
-    u32* w = reinterpret_cast<u32*>(rec + k);
-    const u32 u = (w[0] >> 1) - unit_lo;
-    if ((w[0] >> 1) >= unit_lo && u < nbits && ((bm[u >> 5] >> (u & 31)) & 1u)) w[2] |= 4u << 24;
+  for (u32 base = 0; base < n; base += 32 * MJ_U) {
+    u32 w0[MJ_U];
+#pragma unroll
+    for (int j = 0; j < MJ_U; j++) {
+      const u32 k = base + 32 * j + lane;
+      w0[j] = k < n ? reinterpret_cast<const u32*>(rec + k)[0] : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int j = 0; j < MJ_U; j++) {
+      if (w0[j] == 0xFFFFFFFFu) continue;
+      const u32 u = (w0[j] >> 1) - unit_lo;
+      if ((w0[j] >> 1) >= unit_lo && u < nbits && ((bm[u >> 5] >> (u & 31)) & 1u))
+        atomicOr(reinterpret_cast<u32*>(rec + base + 32 * j + lane) + 2, 4u << 24);  // RED: no round trip
+    }
   }
   __syncwarp();
 }
