@@ -271,7 +271,10 @@ __device__ __noinline__ void decode311_warp(const u8* __restrict__ gcode, u32 le
 // offset = 2u, arg = the arg byte when the opcode has an argument, n_prefixes 0,
 // cache_units, flags = has_arg (no jump targets: there are no jumps).
 #define L11_MAX 4096u   // bytes of code (2048 units: the packed row word's 11-bit unit index)
-#define L11_R 38u       // records per lane row (odd row stride: L11_R + 1)
+#ifndef L11_ROUND
+#define L11_ROUND 8     // instructions per lane per round (refill, flush check once per round)
+#endif
+#define L11_R (32u + L11_ROUND) // records per lane row: a 32-record flush + one round (row stride L11_R + 1)
 #define L11_RING 128u   // code units per lane ring (a power of two)
 #define L11_CHUNK 16u   // units per ring refill (one cp.async group)
 #define L11_AHEAD 112u  // units kept buffered ahead of the walk: L11_RING - L11_CHUNK
@@ -426,10 +429,10 @@ __global__ void __launch_bounds__(L11_WARPS * 32, L11_MINB) upy_decode311_lane_k
       else cp_async_wait0();
       V = F - L11_CHUNK * pend;
     }
-    // four instructions per lane: read the unit at u, look its opcode up, append the
-    // packed record, jump over the instruction's cache units
+    // L11_ROUND instructions per lane: read the unit at u, look its opcode up, append
+    // the packed record, jump over the instruction's cache units
 #pragma unroll
-    for (int k = 0; k < 4; k++) {
+    for (int k = 0; k < L11_ROUND; k++) {
       const bool live = o >= 0 && ok && u < units && u < V;
       const u32 unit = *reinterpret_cast<const unsigned short*>(ring + 2u * (u & (L11_RING - 1)));
       const u32 e = tab[unit & 0xFFu];
@@ -442,15 +445,18 @@ __global__ void __launch_bounds__(L11_WARPS * 32, L11_MINB) upy_decode311_lane_k
       ok = ok && !(live && bad);
     }
     const bool done = o >= 0 && (!ok || u >= units);
-    // rows that are nearly full or complete go out, expanded to upy_ins records
-    u32 who = __ballot_sync(0xffffffffu, ok && cnt && (done || cnt > L11_R - 4));
+    // rows holding 32 records, or whose object ended, go out, expanded to upy_ins
+    // records: 32 at a time (one full store round per row) while the object runs,
+    // everything at its end
+    const u32 fc = done ? cnt : 32u;
+    u32 who = __ballot_sync(0xffffffffu, ok && cnt && (done || cnt >= 32));
     if (who) {
       __syncwarp();
       const u32 mine = who;
       while (who) {
         const int L = __ffs(who) - 1;
         who &= who - 1;
-        const u32 c = __shfl_sync(0xffffffffu, cnt, L);
+        const u32 c = __shfl_sync(0xffffffffu, fc, L);
         const u32 base = __shfl_sync(0xffffffffu, nout, L);
         upy_ins* dst = reinterpret_cast<upy_ins*>(__shfl_sync(0xffffffffu, reinterpret_cast<u64>(rec), L)) + base;
         const u32* src = rows_all[wid][L];
@@ -465,8 +471,9 @@ __global__ void __launch_bounds__(L11_WARPS * 32, L11_MINB) upy_decode311_lane_k
       }
       __syncwarp();
       if ((mine >> lane) & 1u) {
-        nout += cnt;
-        cnt = 0;
+        for (u32 k = fc; k < cnt; k++) row[k - fc] = row[k];  // the < 4 records past the first 32
+        nout += fc;
+        cnt -= fc;
       }
     }
     if (done) {
