@@ -272,7 +272,7 @@ __device__ __noinline__ void decode311_warp(const u8* __restrict__ gcode, u32 le
 // cache_units, flags = has_arg (no jump targets: there are no jumps).
 #define L11_MAX 4096u   // bytes of code (2048 units: the packed row word's 11-bit unit index)
 #ifndef L11_ROUND
-#define L11_ROUND 8     // instructions per lane per round (refill, flush check once per round)
+#define L11_ROUND 16    // instructions per lane per round (refill, flush check once per round)
 #endif
 #define L11_R (32u + L11_ROUND) // records per lane row: a 32-record flush + one round (row stride L11_R + 1)
 #define L11_RING 128u   // code units per lane ring (a power of two)
