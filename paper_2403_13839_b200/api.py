@@ -168,15 +168,19 @@ class DeviceArena:
         # 26 chunks of 669K: +24% over per-thread), or all roots in one
         return slots == 0 or slots >= min(arena.n_roots, SPLIT_MIN_WAVES * sms * 1024)
 
+    DECODE_KERNELS = ("upy_decode311_lane_kernel", "upy_decode_kernel")  # upy_decode_batch's two launches
+
     def kernel_names(self):
-        """The kernels one run() launches (per chunk for the split schedule)."""
+        """The kernels one run() launches (per chunk for the split schedule): the
+        decode kernels, then the decompile kernels."""
+        dec = list(self.DECODE_KERNELS)
         if self.output == 1:
-            return ["upy_decode_kernel", "upy_cfgdot_kernel"]
+            return dec + ["upy_cfgdot_kernel"]
         if self.warp_sync == 3:
-            return ["upy_decode_kernel", "upy_tree_kernel", "upy_emit_kernel"]
+            return dec + ["upy_tree_kernel", "upy_emit_kernel"]
         if self.warp_sync == 4:
-            return ["upy_decode_kernel", "upy_analyze_kernel", "upy_structure_kernel", "upy_emit_kernel"]
-        return ["upy_decode_kernel", "upy_decompile_kernel"]
+            return dec + ["upy_analyze_kernel", "upy_structure_kernel", "upy_emit_kernel"]
+        return dec + ["upy_decompile_kernel"]
 
     def _memory_slots(self, arena, split=False):
         """Concurrent per-thread arenas when the library's default 40 GB budget
