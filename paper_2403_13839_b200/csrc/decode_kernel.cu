@@ -272,7 +272,7 @@ __device__ __noinline__ void decode311_warp(const u8* __restrict__ gcode, u32 le
 // cache_units, flags = has_arg (no jump targets: there are no jumps).
 #define L11_MAX 4096u   // bytes of code (2048 units: the packed row word's 11-bit unit index)
 #ifndef L11_ROUND
-#define L11_ROUND 16    // instructions per lane per round (refill, flush check once per round)
+#define L11_ROUND 8     // instructions per lane per round (refill, flush check once per round)
 #endif
 #define L11_R (32u + L11_ROUND) // records per lane row: a 32-record flush + one round (row stride L11_R + 1)
 #define L11_RING 128u   // code units per lane ring (a power of two)
@@ -282,7 +282,7 @@ __device__ __noinline__ void decode311_warp(const u8* __restrict__ gcode, u32 le
 #define L11_WARPS 2     // warps per block
 #define L11_REDO 0x7ffffff0  // dec status: the main kernel decodes the object
 #ifndef L11_MINB
-#define L11_MINB 7      // blocks per SM (~28 KB of shared memory each; 64-unit ring: 2.06 ms, 256: 1.97 ms, 128: 1.55 ms)
+#define L11_MINB 8      // blocks per SM (~28 KB of shared memory each; 64-unit ring: 2.06 ms, 256: 1.97 ms, 128: 1.55 ms)
 #endif
 // opcode entry of the walk: bits 0-3 cache count, bit 4 reject (unknown opcode,
 // EXTENDED_ARG, jump), bits 27-30 cache count and bit 31 has_arg (the packed
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(L11_WARPS * 32, L11_MINB) upy_decode311_lane_k
                                                                                       upy_decoded* __restrict__ dec) {
   __shared__ u32 tab[256];
   __shared__ u32 rows_all[L11_WARPS][32][L11_R + 1];  // odd stride: lane L's word k in bank (L + k) % 32
-  __shared__ __align__(16) u8 ring_all[L11_WARPS][32][L11_RING * 2 + 16];  // per-lane code ring (+16 B pad)
+  __shared__ __align__(16) u8 ring_all[L11_WARPS][32][L11_RING * 2];  // per-lane code ring
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
