@@ -274,7 +274,10 @@ __device__ __noinline__ void decode311_warp(const u8* __restrict__ gcode, u32 le
 #ifndef L11_ROUND
 #define L11_ROUND 8     // instructions per lane per round (refill, flush check once per round)
 #endif
-#define L11_R (32u + L11_ROUND) // records per lane row: a 32-record flush + one round (row stride L11_R + 1)
+#ifndef L11_FLUSH
+#define L11_FLUSH 32u   // records per row flush while an object runs (one full store round; 16: 1.47 ms vs 1.20)
+#endif
+#define L11_R (L11_FLUSH + L11_ROUND) // records per lane row: one flush + one round (row stride L11_R + 1)
 #define L11_RING 128u   // code units per lane ring (a power of two)
 #define L11_CHUNK 16u   // units per ring refill (one cp.async group)
 #define L11_AHEAD 112u  // units kept buffered ahead of the walk: L11_RING - L11_CHUNK
@@ -445,11 +448,11 @@ __global__ void __launch_bounds__(L11_WARPS * 32, L11_MINB) upy_decode311_lane_k
       ok = ok && !(live && bad);
     }
     const bool done = o >= 0 && (!ok || u >= units);
-    // rows holding 32 records, or whose object ended, go out, expanded to upy_ins
+    // rows holding L11_FLUSH records, or whose object ended, go out, expanded to upy_ins
     // records: 32 at a time (one full store round per row) while the object runs,
     // everything at its end
-    const u32 fc = done ? cnt : 32u;
-    u32 who = __ballot_sync(0xffffffffu, ok && cnt && (done || cnt >= 32));
+    const u32 fc = done ? cnt : L11_FLUSH;
+    u32 who = __ballot_sync(0xffffffffu, ok && cnt && (done || cnt >= L11_FLUSH));
     if (who) {
       __syncwarp();
       const u32 mine = who;
@@ -471,7 +474,7 @@ __global__ void __launch_bounds__(L11_WARPS * 32, L11_MINB) upy_decode311_lane_k
       }
       __syncwarp();
       if ((mine >> lane) & 1u) {
-        for (u32 k = fc; k < cnt; k++) row[k - fc] = row[k];  // the < 4 records past the first 32
+        for (u32 k = fc; k < cnt; k++) row[k - fc] = row[k];  // the records past the flushed ones
         nout += fc;
         cnt -= fc;
       }
