@@ -499,11 +499,16 @@ def extra_line(wl, args, local, barrier):
     torch.cuda.empty_cache()  # the previous leg's buffers
     r = run_workload(wl, args, 0, 1, local, barrier, steps=2, warmup=1, e2e=False)
     ms = r["total_ms"] / 2
+    alg_dec, _ = algorithmic_bytes(r["arena"], r["n_instr"], 0)
+    peak, _ = peaks()
+    dec_gbs = alg_dec / (r["dec_sum"] / 2 / 1e3) / 1e9
     return {"workload": WORKLOADS[wl]["desc"], "value": r["n_roots"] / (ms / 1000.0), "unit": "objects/s",
             "steps": 2, "warmup": 1, "ms_per_step": ms,
             "kernel_ms": {"decode": r["dec_sum"] / 2, "decompile": r["st_sum"] / 2, "stackscan": r["stackscan_ms"]},
             "instructions": r["n_instr"], "code_bytes": r["arena"].code_bytes,
-            "decode_gbs_alg": None, "parity": {"checked": r["checked"], "mismatches": r["bad"]},
+            "decode_gbs_alg": dec_gbs, "decode_frac": dec_gbs / peak,
+            "decode_algorithmic_bytes_per_launch": alg_dec,
+            "parity": {"checked": r["checked"], "mismatches": r["bad"]},
             "slots": r["slots"], "corpus": r["info"]["corpus"], "schedule": r["info"]["schedule"],
             "clocks": r["clocks"]}
 
