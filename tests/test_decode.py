@@ -150,3 +150,78 @@ def test_decode_kernel_tiled_matches_reference(gset):
         sub_ins = ins[shift:shift + ar.total_code_units + 1]
         bad = compare(gset, ar, sub_ins, sub_dec)
         assert not bad, (r, bad[:5])
+
+
+def _lane_edge_codes():
+    """3.11 objects around the lane kernel's limits (decode_kernel.cu: <= 4096 code
+    bytes, no EXTENDED_ARG, no jump) plus ones it must hand back, interleaved with
+    3.10 objects: straight-line code of random known opcodes with their cache units,
+    at lengths 2046-2050 units; variants with an EXTENDED_ARG, a forward jump, an
+    unknown opcode and a cache run past the end."""
+    import random
+
+    from paper_2403_13839_b200._optables import TABLES
+    from paper_2403_13839_b200.model import CodeObject, VersionTag
+
+    rng = random.Random(0x311)
+    t11 = TABLES[11]
+    plain = [op for op, v in t11.items() if v and v[2] == "none" and op not in (0, 144)]
+    jumps = [op for op, v in t11.items() if v and v[2] == "jump_rel"]
+
+    def body(units, variant):
+        out = bytearray()
+        while len(out) < 2 * units:
+            op = rng.choice(plain)
+            out += bytes([op, rng.randrange(256) if t11[op][1] else 0])
+            out += bytes(2 * t11[op][3])
+        out = out[:2 * units]
+        if variant == "cut" and len(out) >= 2:
+            out[-2:] = bytes([next(op for op in plain if t11[op][3] > 0), 1])  # caches past the end
+        k = 2 * rng.randrange(1, max(2, units // 2))
+        # re-align k to an instruction start by walking the instruction chain
+        i = 0
+        while i + 2 <= len(out) and i < k:
+            i += 2 * (1 + t11.get(out[i], ("", False, "", 0))[3]) if out[i] in t11 and t11[out[i]] else 2
+        k = min(i, len(out) - 4)
+        if variant == "ext" and k >= 0:
+            out[k:k + 4] = bytes([144, 0, rng.choice([op for op in plain if t11[op][1] and t11[op][3] == 0]), 1])
+        elif variant == "jump" and k >= 0:
+            out[k:k + 2] = bytes([jumps[0], 0])
+        elif variant == "unknown" and k >= 0:
+            out[k] = next(op for op in range(256) if op not in t11 or not t11[op])
+        return bytes(out)
+
+    def obj(minor, code):
+        return CodeObject(VersionTag(3, minor), 0, 0, 0, 0, 0, 0, code, (), (), (), (), (), "f", "f.py", 1)
+
+    codes = []
+    for units in (1, 7, 8, 200, 2046, 2047, 2048, 2049, 2050):
+        for variant in ("plain", "plain", "ext", "jump", "unknown", "cut"):
+            codes.append(obj(11, body(units, variant)))
+            codes.append(obj(10, bytes([100, 0, 83, 0])))  # LOAD_CONST 0; RETURN_VALUE
+    return codes
+
+
+@pytest.mark.gpu
+def test_decode_lane_kernel_edges_match_scalar():
+    """The 3.11 lane kernel and its hand-back path against the reference-order
+    scalar decoder (decode_scalar on the host, pinned to the reference above) on
+    objects at and past the lane kernel's size limit, with EXTENDED_ARG, jumps,
+    unknown opcodes and truncated caches, tiled so every warp mixes them."""
+    from paper_2403_13839_b200 import arena, hostcheck
+
+    ar = arena.tile(arena.pack(_lane_edge_codes()), 5)
+    want_ins, want_dec = hostcheck.decode(ar)
+    ins, dec = device_decode(ar)
+    objs = ar.section("objs")
+    bad = []
+    for o in range(ar.n_objs):
+        if tuple(dec[o]) != tuple(want_dec[o]):
+            bad.append((o, tuple(dec[o]), tuple(want_dec[o])))
+            continue
+        if int(dec[o]["status"]) == 0:
+            base, n = int(objs[o]["code_off"]) >> 1, int(dec[o]["n_instrs"])
+            if ins[base:base + n].tobytes() != want_ins[base:base + n].tobytes():
+                bad.append((o, "records differ"))
+    assert not bad, bad[:5]
+    assert int(np.count_nonzero(dec["status"] == 0)) > ar.n_objs // 2
