@@ -526,14 +526,18 @@ def api_e2e(wl, n_sample, local):
     dev = f"cuda:{local}"
     api.decompile_many(codes[:1024], device=dev)  # warm-up
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    out = api.decompile_many(codes, device=dev)
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
+    times = []
+    for _ in range(3):  # host-bound and noisy: the median of three calls
+        t0 = time.perf_counter()
+        out = api.decompile_many(codes, device=dev)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    dt = sorted(times)[1]
     ok = sum(1 for v in out if isinstance(v, str))
     return {"value": n_sample / dt, "unit": "objects/s", "objects": n_sample, "seconds": dt, "ok": ok,
+            "seconds_all": times,
             "call": "paper_2403_13839_b200.decompile_many(codes) on model.CodeObject inputs",
-            "timing": "wall clock of one call after a warm-up call (host packing included)"}
+            "timing": "wall clock, median of three calls after a warm-up call (host packing included)"}
 
 
 def main():
