@@ -662,7 +662,11 @@ def main():
         "roofline": {"bound": "hbm", "kernel": " + ".join(r["kernels"][n_dec:]), "achieved": ach_struct, "peak": peak,
                      "unit": "GB/s", "frac": ach_struct / peak,
                      "traffic": measured_traffic(args.workload, r["kernels"][n_dec:]),
-                     "algorithmic_bytes_per_launch": alg_struct, "peak_source": peak_src},
+                     "algorithmic_bytes_per_launch": alg_struct, "peak_source": peak_src,
+                     "limiter": "not HBM bandwidth: one root per thread, pointer-chasing through per-thread "
+                                "arenas; ~7 active lanes per warp instruction, issue-active ~8.5%, stalls on "
+                                "memory latency and instruction fetch (profiles/r02/split/tree_summary.txt, "
+                                "DESIGN.md 3.2)"},
         "roofline_decode": {"bound": "hbm", "kernel": " + ".join(r["kernels"][:n_dec]), "achieved": ach_dec,
                             "peak": peak, "unit": "GB/s", "frac": ach_dec / peak,
                             "traffic": measured_traffic(args.workload, r["kernels"][:n_dec]),
